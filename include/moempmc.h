@@ -1,0 +1,173 @@
+/*
+ * moempmc.h -- C ABI of the B200 (sm_100a) MoE-MPMC inference hot path.
+ *
+ * The reference (arXiv 2605.11537, package `moesim`, pure Python/numpy) has no
+ * FFI: its boundary is the Python module API. Each entry point below replaces
+ * the reference function cited next to it; the Python host layer
+ * (paper_2605_11537_b200/*.py) keeps the reference signatures and calls these
+ * through ctypes. INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless stated otherwise; buffers are
+ *    caller-owned; `ws` is a caller-provided device workspace.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *    asynchronous on that stream and never synchronise the device.
+ *  - int32 indices; bf16 = IEEE bfloat16 stored as uint16; row-major arrays.
+ *  - Return value: MP_OK or an error code mapped 1:1 onto the reference
+ *    exception classes (src/errors.py); mp_last_error() returns the message.
+ */
+#ifndef MOEMPMC_H
+#define MOEMPMC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define MP_API __attribute__((visibility("default")))
+#else
+#define MP_API
+#endif
+
+#define MP_ABI_VERSION 1
+
+#define MP_OK 0
+#define MP_ERR_CONFIG 1     /* ConfigurationError       src/errors.py:8-9   */
+#define MP_ERR_NUMERIC 2    /* NumericError             src/errors.py:26-27 */
+#define MP_ERR_PLACEMENT 3  /* PlacementError           src/errors.py:30-31 */
+#define MP_ERR_INFEASIBLE 4 /* InfeasibleCapacityError  src/errors.py:34-41 */
+#define MP_ERR_CUDA 5       /* CUDA runtime failure (no reference analogue)  */
+
+/* token_event encoding (src/placement.py:22-24 LOAD / REPLICATE) */
+#define MP_EVENT_NONE (-1)
+#define MP_EVENT_KIND_SHIFT 24
+#define MP_EVENT_LOAD 1
+#define MP_EVENT_REPLICATE 2
+
+MP_API int mp_abi_version(void);
+MP_API const char* mp_last_error(void);
+MP_API int mp_device_info(int* sm_count, int* cc_major, int* cc_minor); /* host out-params */
+
+/* ------------------------------------------------------------------ K4
+ * Load histogram. demand[l*E+e] = #{t : assign[l*T+t] == e}.
+ * Replaces HashTable._histograms (src/predictor.py:122-127) and
+ * demand_counts (src/planner.py:27-33). assign values must lie in [0,E).
+ */
+MP_API int mp_histogram(const int32_t* assign, int L, int T, int E, int32_t* demand, void* stream);
+
+/* Capped replica plan per layer, bit-exact with cap_replicas
+ * (src/planner.py:36-72) via its closed-form water-fill; plan_all_layers
+ * (src/planner.py:75-85) is the L>1 case. Demand may be expressed in tokens
+ * (unit_rows = 1, reference semantics) or in M-tiles (unit_rows = 128:
+ * ceil(n/128) per expert). caps[l*E+e] = 0 for undemanded experts.
+ * infeasible[l] = 1 when #distinct > capacity (caps row left 0). */
+MP_API int mp_cap_replicas(const int32_t* demand, int L, int E, int capacity, int unit_rows, int32_t* caps,
+                    int32_t* infeasible, void* stream);
+
+/* ------------------------------------------------------------------ K4+K6
+ * Residency update + token walk of apply_layer (src/placement.py:109-165),
+ * folded over L layers like apply_batch (src/placement.py:168-180).
+ *   caps[l*E+e]       planned replica caps (0 = not in plan)          (in)
+ *   res[l*E+e]        resident replica count per expert            (in/out)
+ *   token_to_slot     index into the sorted (expert, ordinal) slot list (out)
+ *   token_event       MP_EVENT_NONE or kind<<24 | ordinal per token    (out)
+ *   offloads[l*E+e]   OFFLOAD pops for expert e (reclaim or full offload)(out)
+ *   fallback[l]       1 when the layer fell back to distinct-only      (out)
+ *   num_slots[l]      resident slots after placement                   (out)
+ */
+MP_API size_t mp_place_workspace_bytes(int L, int T, int E);
+MP_API int mp_place(const int32_t* assign, int L, int T, int E, const int32_t* caps, int plan_capacity, int state_capacity,
+             int32_t* res, int32_t* token_to_slot, int32_t* token_event, int32_t* offloads, int32_t* fallback,
+             int32_t* num_slots, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ K6
+ * Execution map of BatchRunner._run_predicted (src/simulator.py:185-203):
+ * tokens run on their TRUE expert, round-robin over the resident replicas;
+ * an expert with no resident replica gets one corrective LOAD (persisted in
+ * res). Also emits the replica-segment permutation consumed by the grouped
+ * GEMM: rows are grouped by slot (expert-major, replica-minor), a slot's rows
+ * in token order; pieces are the GEMM work units (one per slot, or per 128-row
+ * M-tile of a slot when split_m != 0).
+ *   max_slots  >= max over layers of resident slots + corrective loads
+ *   per layer l (strides): token_to_slot/row_of_token/tok_of_row: T;
+ *   piece_row/piece_rows: max_slots + ceil(T/128); exp_begin: E + 1.
+ */
+MP_API size_t mp_exec_workspace_bytes(int L, int T, int E, int max_slots);
+MP_API int mp_exec_map(const int32_t* route, int L, int T, int E, int max_slots, int split_m, int32_t* res,
+                int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
+                int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin, void* ws,
+                size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ K1 / generic
+ * C[M x ldc] = epi(A[M x K] * B[N x K]^T) on tcgen05 (bf16 in, fp32 acc).
+ * K % 64 == 0, N % 64 == 0 (pad with zero rows), 16-byte aligned rows.
+ * c_dtype: 0 = bf16, 1 = fp32.  act: 0 none, 1 relu, 2 sigmoid(v+bias[n])
+ * for n >= sig_from (columns below sig_from get +bias only when bias != NULL).
+ */
+MP_API int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc,
+                 const float* bias, int act, int sig_from, void* stream);
+
+/* ------------------------------------------------------------------ K1+K2
+ * One SRU layer over a token sequence (src/predictor.py:157-195):
+ *   [u | f | r] = x W_cat^T (+ b), f,r = sigmoid   (tcgen05 GEMM, fused epilogue)
+ *   c_t = f c_{t-1} + (1-f) u ;  h_t = r tanh(c_t) + (1-r) x_t   (chunked scan)
+ * x_bf16/x_f32: T x d (d % 64 == 0), w_cat: 3d x d bf16, b_cat: 3d fp32
+ * (zeros for the u block). Outputs h_f32 and h_bf16 (T x d).
+ * ws >= mp_sru_workspace_bytes(T, d).
+ */
+MP_API size_t mp_sru_workspace_bytes(int T, int d);
+MP_API int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* w_cat, const float* b_cat, int T, int d,
+                 float* h_f32, void* h_bf16, int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ K3
+ * Predicted expert per (layer, token) = argmax_e h_t . heads[l,e]
+ * (= argmax(sparsemax(.)), src/predictor.py:212-223). heads: ceil64(L*Eg) x d bf16 (zero rows pad),
+ * layer l in rows [l*Eg, l*Eg+E), Eg = E rounded up to a power of two >= 32.
+ */
+MP_API int mp_heads_argmax(const void* h_bf16, const void* heads, int T, int d, int L, int E, int Eg, int32_t* assign,
+                    void* stream);
+
+/* ------------------------------------------------------------------ K5
+ * True top-1 routing route_top1 (src/router_oracle.py:90-98) for a token
+ * stream: fp64-faithful argmax of W_r x. The tensor-core pass uses split-bf16
+ * (x_hi.w_hi + x_hi.w_lo + x_lo.w_hi, fp32 acc); tokens whose top-2 gap is
+ * inside the error bound are re-decided in fp64 from the fp32 inputs.
+ *   x: T x ldx fp32 (d valid columns); w_hl: Eg x 2d bf16 [w_hi | w_lo];
+ *   w_f32: E x d fp32. ws >= mp_router_workspace_bytes(T, d).
+ */
+MP_API size_t mp_router_workspace_bytes(int T, int d);
+MP_API int mp_route_top1(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32, int E, int Eg,
+                         float w_norm_max, int32_t* route, void* ws, size_t ws_bytes, void* stream);
+/* Same with a precomputed per-column bound w_abs[k] = max_e |w_ek| (mp_router_weight_absmax),
+ * the form the device-resident engine uses (weights are static). */
+MP_API int mp_router_weight_absmax(const float* w_f32, int E, int d, float* w_abs, void* stream);
+MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
+                            const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
+                            void* stream);
+
+/* ------------------------------------------------------------------ K6 gather + K7 + K8
+ * One MoE layer's expert FFNs over replica segments, fused with the ungated
+ * residual combine (src/router_oracle.py:101-111, 127-134):
+ *   xperm[row]   = bf16(x[tok_of_row[row]])                       (gather)
+ *   hid[row]     = relu(xperm[row] . U_e^T)                        (GEMM1)
+ *   x[tok][:]   += hid[row] . V_e^T                                (GEMM2, scatter epilogue)
+ * u: (E*Fp) x dp bf16, v: (E*dp) x Fp bf16 (zero padded, dp%64==0, Fp%256==0),
+ * x: T x dp fp32 updated in place. Pieces from mp_exec_map (one layer).
+ */
+MP_API size_t mp_ffn_workspace_bytes(int T, int dp, int Fp);
+MP_API int mp_moe_ffn(float* x, int T, int dp, int Fp, int E, const void* u, const void* v, const int32_t* tok_of_row,
+               const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
+               size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ K9
+ * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):
+ * dst <- src, `bytes` long, device-to-device (or peer) on `stream`. */
+MP_API int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOEMPMC_H */

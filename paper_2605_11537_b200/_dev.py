@@ -1,0 +1,77 @@
+"""Device plumbing shared by the host API: CUDA checks, streams, workspaces.
+
+PyTorch is used only for device memory, streams and events; every computation
+on the hot path is a call into ``libmoempmc.so``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DeviceError
+
+_checked = False
+
+
+def require_device() -> torch.device:
+    """The CUDA device the kernels run on; raises if there is none (no CPU fallback)."""
+    global _checked
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the MoE-MPMC hot path runs only on sm_100a (B200)")
+    if not _checked:
+        _lib.load_library()
+        major, minor = torch.cuda.get_device_capability()
+        if (major, minor) != (10, 0):
+            raise DeviceError(f"libmoempmc.so is built for sm_100a; device is sm_{major}{minor}")
+        _checked = True
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream: torch.cuda.Stream | None = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise DeviceError("expected a CUDA tensor")
+    return int(t.data_ptr())
+
+
+def to_device_i32(a, dev) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=torch.int32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(dev)
+
+
+class Workspace:
+    """Grow-only device scratch buffers keyed by purpose."""
+
+    def __init__(self) -> None:
+        self._bufs: dict[str, torch.Tensor] = {}
+
+    def get(self, key: str, nbytes: int, device: torch.device) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes or buf.device != device:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+WORKSPACE = Workspace()
+
+
+def round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def pow2_at_least(x: int, lo: int) -> int:
+    p = lo
+    while p < x:
+        p *= 2
+    return p

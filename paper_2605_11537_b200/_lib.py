@@ -1,0 +1,114 @@
+"""ctypes binding of ``libmoempmc.so`` (include/moempmc.h).
+
+This is the only way the Python layer reaches the GPU kernels. There is no
+CPU fallback: if the library or a CUDA device is missing, every entry point
+raises :class:`DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+from .errors import (
+    ConfigurationError,
+    DeviceError,
+    InfeasibleCapacityError,
+    NumericError,
+    PlacementError,
+)
+
+LIB_PATH = Path(__file__).resolve().with_name("libmoempmc.so")
+
+MP_OK, MP_ERR_CONFIG, MP_ERR_NUMERIC, MP_ERR_PLACEMENT, MP_ERR_INFEASIBLE, MP_ERR_CUDA = range(6)
+MP_EVENT_NONE = -1
+MP_EVENT_KIND_SHIFT = 24
+MP_EVENT_LOAD = 1
+MP_EVENT_REPLICATE = 2
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_Z = ctypes.c_size_t
+_F = ctypes.c_float
+
+# name -> (restype, argtypes); mirrors include/moempmc.h
+SIGNATURES: dict[str, tuple] = {
+    "mp_abi_version": (_I, []),
+    "mp_last_error": (ctypes.c_char_p, []),
+    "mp_device_info": (_I, [_P, _P, _P]),
+    "mp_histogram": (_I, [_P, _I, _I, _I, _P, _P]),
+    "mp_cap_replicas": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
+    "mp_place_workspace_bytes": (_Z, [_I, _I, _I]),
+    "mp_place": (_I, [_P, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_exec_workspace_bytes": (_Z, [_I, _I, _I, _I]),
+    "mp_exec_map": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
+    "mp_sru_workspace_bytes": (_Z, [_I, _I]),
+    "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _Z, _P]),
+    "mp_heads_argmax": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
+    "mp_router_workspace_bytes": (_Z, [_I, _I]),
+    "mp_route_top1": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _Z, _P]),
+    "mp_router_weight_absmax": (_I, [_P, _I, _I, _P, _P]),
+    "mp_route_top1_ex": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
+    "mp_ffn_workspace_bytes": (_Z, [_I, _I, _I]),
+    "mp_moe_ffn": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
+}
+
+_ERRORS = {
+    MP_ERR_CONFIG: ConfigurationError,
+    MP_ERR_NUMERIC: NumericError,
+    MP_ERR_PLACEMENT: PlacementError,
+    MP_ERR_INFEASIBLE: InfeasibleCapacityError,
+    MP_ERR_CUDA: DeviceError,
+}
+
+_lock = threading.Lock()
+_lib: ctypes.CDLL | None = None
+
+
+def load_library(path: Path | str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the native library. Does not touch the GPU."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise DeviceError(
+                f"native library {p} is missing; build it with "
+                "`python -m paper_2605_11537_b200.build` (nvcc, sm_100a)"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a C-ABI status onto the reference exception classes."""
+    if status == MP_OK:
+        return
+    msg = (load_library().mp_last_error() or b"").decode(errors="replace")
+    exc = _ERRORS.get(status, DeviceError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+def call(name: str, *args) -> int:
+    """Call an int-returning entry point and raise on a non-OK status."""
+    fn = getattr(load_library(), name)
+    status = fn(*args)
+    check(status, name)
+    return status
+
+
+def size_query(name: str, *args) -> int:
+    return int(getattr(load_library(), name)(*args))

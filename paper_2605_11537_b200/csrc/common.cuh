@@ -1,0 +1,105 @@
+// Shared device helpers and host-side error plumbing for the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "moempmc.h"
+
+namespace mp {
+
+constexpr int kChunk = 128;       // tokens per rank/histogram chunk (= GEMM M tile)
+constexpr int kBlockMRows = 128;  // rows per GEMM M tile (pieces in split_m mode)
+
+__host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// Block-wide inclusive sum for up to 1024 threads (blockDim multiple of 32).
+__device__ inline int block_sum(int v, int* red /* >= 32 ints smem */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int t = (lane < nw) ? red[lane] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+__device__ inline int block_max(int v, int* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int t = (lane < nw) ? red[lane] : INT_MIN;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t = max(t, __shfl_xor_sync(0xffffffffu, t, o));
+  return t;
+}
+
+// In-place exclusive scan of n ints in shared memory by the whole block.
+// Returns the total. Each thread owns a contiguous run (keeps order).
+__device__ inline int block_exclusive_scan(int* a, int n, int* red /* >= 33 ints */) {
+  const int nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int b = threadIdx.x * per, e = min(n, b + per);
+  int s = 0;
+  for (int i = b; i < e; ++i) s += a[i];
+  // exclusive scan of per-thread sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = nt >> 5;
+  int incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) red[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = (lane < nw) ? red[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < nw) red[lane] = wi - w;  // exclusive warp offsets
+    if (lane == 31) red[32] = wi;       // total
+  }
+  __syncthreads();
+  int run = red[warp] + incl - s;
+  for (int i = b; i < e; ++i) {
+    const int x = a[i];
+    a[i] = run;
+    run += x;
+  }
+  const int total = red[32];
+  __syncthreads();
+  return total;
+}
+
+}  // namespace mp
+
+#define MP_CUDA_TRY(expr)                                                                  \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      mp_set_last_error("%s:%d: %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return MP_ERR_CUDA;                                                                  \
+    }                                                                                      \
+  } while (0)
+
+#define MP_REQUIRE(cond, code, ...)      \
+  do {                                   \
+    if (!(cond)) {                       \
+      mp_set_last_error(__VA_ARGS__);    \
+      return (code);                     \
+    }                                    \
+  } while (0)
+
+// defined in capi.cu
+extern "C" void mp_set_last_error(const char* fmt, ...);

@@ -1,0 +1,88 @@
+// K6 gather + K7 grouped expert FFN (tcgen05) + K8 residual combine fused into
+// the GEMM2 epilogue.
+//
+// Reference: expert_forward  v @ relu(u @ x)   (src/router_oracle.py:101-111)
+//            _run_layers     stream[t] = stream[t] + delta (src/router_oracle.py:127-134)
+// Weights keep the reference layouts, which are already K-major for the B
+// operand: expert_u (E, F, d) -> rows e*F + f, K = d; expert_v (E, d, F) ->
+// rows e*d + j, K = F (zero padded to dp % 64 == 0, Fp % 256 == 0).
+// Rows are the slot-grouped permutation from mp_exec_map, so every replica
+// segment is a contiguous run of A rows; replicas of one expert alias the same
+// weight rows (no copies on one GPU).
+#include "epilogues.cuh"
+#include "launch.cuh"
+
+namespace mp {
+
+// xperm[row] = bf16(x[tok_of_row[row]]); one warp per row, 8-byte lanes.
+__global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const int32_t* __restrict__ tok_of_row,
+                              __nv_bfloat16* __restrict__ xperm) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= T) return;
+  const int t = __ldg(&tok_of_row[row]);
+  const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * dp);
+  uint2* dst = reinterpret_cast<uint2*>(xperm + (size_t)row * dp);
+  for (int k = lane; k < dp / 4; k += 32) {
+    const float4 v = __ldg(&src[k]);
+    uint2 w;
+    w.x = pack_bf16x2(v.x, v.y);
+    w.y = pack_bf16x2(v.z, v.w);
+    dst[k] = w;
+  }
+}
+
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
+  return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp);
+}
+
+extern "C" int mp_moe_ffn(float* x, int T, int dp, int Fp, int E, const void* u, const void* v,
+                          const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                          const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(T >= 1 && E >= 1, MP_ERR_CONFIG, "mp_moe_ffn: bad T/E");
+  MP_REQUIRE(dp % 64 == 0 && Fp % 256 == 0, MP_ERR_CONFIG, "mp_moe_ffn: need dp%%64==0 and Fp%%256==0 (dp=%d Fp=%d)",
+             dp, Fp);
+  MP_REQUIRE(ws_bytes >= mp_ffn_workspace_bytes(T, dp, Fp), MP_ERR_CONFIG, "mp_moe_ffn: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  __nv_bfloat16* xperm = (__nv_bfloat16*)ws;
+  __nv_bfloat16* hid = (__nv_bfloat16*)((char*)ws + al(sizeof(__nv_bfloat16) * (size_t)T * dp));
+
+  k_gather_rows<<<cdiv(T * 32, 256), 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+  MP_CUDA_TRY(cudaGetLastError());
+
+  const int grid = num_sms();
+  // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
+  {
+    CUtensorMap ta, tb;
+    int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
+    if (rc) return rc;
+    rc = make_tmap_bf16(&tb, u, (uint64_t)E * Fp, dp, dp, 256);
+    if (rc) return rc;
+    SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64};
+    EpiStoreBf16 e{hid, Fp, nullptr, 1, 0};
+    rc = launch_gemm<256, 4>(ta, tb, s, e, grid, st);
+    if (rc) return rc;
+  }
+  // GEMM2: x[tok] += hid . V_e^T   [rows x dp]
+  {
+    const int bn = (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64);
+    CUtensorMap ta, tb;
+    int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
+    if (rc) return rc;
+    rc = make_tmap_bf16(&tb, v, (uint64_t)E * dp, Fp, Fp, bn);
+    if (rc) return rc;
+    SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64};
+    EpiScatterAdd e{x, dp, tok_of_row};
+    if (bn == 256) rc = launch_gemm<256, 4>(ta, tb, s, e, grid, st);
+    else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, s, e, grid, st);
+    else rc = launch_gemm<64, 8>(ta, tb, s, e, grid, st);
+    if (rc) return rc;
+  }
+  return MP_OK;
+}

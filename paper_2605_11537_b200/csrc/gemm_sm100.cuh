@@ -1,0 +1,264 @@
+// Persistent warp-specialised tcgen05 GEMM core for sm_100a.
+//
+//   D[128 x BN] = A[128 x K] * B[BN x K]^T      (bf16 in, fp32 accumulate in TMEM)
+//
+// Roles (256 threads, one CTA per SM):
+//   warp 0 lane 0 : TMA producer  (A and B k-blocks of 64 bf16 = one 128 B swizzle atom)
+//   warp 1 lane 0 : MMA issuer    (4 x tcgen05.mma 128xBNx16 per k-block)
+//   warp 2        : TMEM allocator (2 accumulator stages x BN columns)
+//   warps 4..7    : epilogue       (tcgen05.ld -> registers -> caller's Epilogue)
+// Pipelines: smem ring full/empty (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue).
+//
+// Work is expressed as "units": a unit is a run of rows [a_row, a_row+rows) of A
+// multiplied by one BN-wide slice of B starting at row b_row. A unit with more
+// than 128 rows is processed as consecutive 128-row M-tiles by the SAME CTA --
+// this is how a replica slot (reference: src/simulator.py:66-81, one server
+// draining its queue) maps onto the GPU; splitting an expert into replicas
+// splits its rows into independent units. Units are assigned to CTAs
+// round-robin (static persistent schedule), so every role walks the same list.
+#pragma once
+#include "ptx.cuh"
+
+namespace mp {
+
+constexpr int kBlockM = 128;
+constexpr int kBlockK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B atom row
+constexpr int kGemmThreads = 256;
+
+struct Unit {
+  int a_row;  // first row of A (and of the row-indexed output)
+  int rows;   // rows in this unit (>0); ceil(rows/128) M-tiles
+  int b_row;  // first row of B (e.g. expert * N + n0)
+  int n0;     // output column offset of this BN slice
+};
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int kABytes = kBlockM * kBlockK * 2;
+  static constexpr int kBBytes = BN * kBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBarOffset = STAGES * kStageBytes;
+  static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;  // +1024 alignment slack
+};
+
+// Scheduler concept:
+//   int num_units() const; Unit unit(int u) const; int num_kb() const;
+//   int a_kcol(int kb) const; int b_kcol(int kb) const;
+// Epilogue concept:
+//   template<int BN> void run(const Unit&, int mt, int r, uint32_t taddr) const
+//   (r = row inside the 128-row tile owned by this thread; taddr = TMEM address of
+//    (lane quadrant, accumulator stage, column 0)).
+
+template <int BN, int STAGES, class Sched, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched,
+                Epi epi) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nunits = sched.num_units();
+  const int nkb = sched.num_kb();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      uint32_t stage = 0, phase = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const Unit U = sched.unit(u);
+        const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
+        for (int mt = 0; mt < mtiles; ++mt) {
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * L::kStageBytes;
+            uint8_t* sb = sa + L::kABytes;
+            mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+            tma_load_2d(sa, &tmA, &full[stage], sched.a_kcol(kb), U.a_row + mt * kBlockM);
+            tma_load_2d(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(kBlockM, BN);
+      uint32_t stage = 0, phase = 0, tile = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const Unit U = sched.unit(u);
+        const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
+        for (int mt = 0; mt < mtiles; ++mt, ++tile) {
+          const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
+          mbar_wait(&tempty[as], aph ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + as * BN;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint8_t* sa = smem + stage * L::kStageBytes;
+            const uint64_t adesc = sw128_kmajor_desc(smem_u32(sa));
+            const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sa + L::kABytes));
+#pragma unroll
+            for (int k = 0; k < kBlockK / 16; ++k) {
+              // advance 16 bf16 = 32 B inside the swizzle atom: +2 in the >>4 address field
+              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            }
+            umma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(&tfull[as]);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue
+    const int q = warp & 3;          // TMEM lane quadrant this warp may access
+    const int r = q * 32 + lane;     // row of the tile owned by this thread
+    uint32_t tile = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const Unit U = sched.unit(u);
+      const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
+      for (int mt = 0; mt < mtiles; ++mt, ++tile) {
+        const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
+        mbar_wait(&tfull[as], aph);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+        epi.template run<BN>(U, mt, r, taddr);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[as]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+#endif
+}
+
+// ------------------------------------------------------------------ schedulers
+
+// Dense C[M x N] = A[M x K] B[N x K]^T, units = (m block, n block), n fastest.
+struct DenseSched {
+  int M, n_tiles, kb, bn;
+  __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
+  __device__ Unit unit(int u) const {
+    const int mb = u / n_tiles, nb = u - mb * n_tiles;
+    Unit U;
+    U.a_row = mb * kBlockM;
+    U.rows = min(kBlockM, M - U.a_row);
+    U.b_row = nb * bn;
+    U.n0 = nb * bn;
+    return U;
+  }
+  __device__ int num_kb() const { return kb; }
+  __device__ int a_kcol(int k) const { return k * kBlockK; }
+  __device__ int b_kcol(int k) const { return k * kBlockK; }
+};
+
+// Device-built unit list (grouped GEMM over replica segments).
+struct ListSched {
+  const int4* units;      // {a_row, rows, b_row, n0}
+  const int* num_units_p;  // device scalar, written by the planner
+  int kb;
+  __device__ int num_units() const { return *reinterpret_cast<const volatile int*>(num_units_p); }
+  __device__ Unit unit(int u) const {
+    const int4 v = __ldg(&units[u]);
+    return Unit{v.x, v.y, v.z, v.w};
+  }
+  __device__ int num_kb() const { return kb; }
+  __device__ int a_kcol(int k) const { return k * kBlockK; }
+  __device__ int b_kcol(int k) const { return k * kBlockK; }
+};
+
+// Grouped GEMM over replica-segment pieces (built on device by mp_exec_map):
+// pieces of expert e are [exp_begin[e], exp_begin[e+1]); units are ordered
+// expert-major, then BN slice, then piece, so consecutive units (running on
+// neighbouring SMs at the same time) share one weight tile through L2.
+struct SegSched {
+  const int32_t* piece_row;
+  const int32_t* piece_rows;
+  const int32_t* exp_begin;  // E + 1 entries
+  int E, n_tiles, bn, n_per_expert, kb;
+  __device__ int num_units() const { return exp_begin[E] * n_tiles; }
+  __device__ Unit unit(int u) const {
+    int lo = 0, hi = E;  // exp_begin[lo]*n_tiles <= u < exp_begin[hi]*n_tiles
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (exp_begin[mid] * n_tiles <= u) lo = mid; else hi = mid;
+    }
+    const int b = exp_begin[lo], cnt = exp_begin[lo + 1] - b;
+    const int local = u - b * n_tiles;
+    const int nt = local / cnt;
+    const int p = b + (local - nt * cnt);
+    return Unit{piece_row[p], piece_rows[p], lo * n_per_expert + nt * bn, nt * bn};
+  }
+  __device__ int num_kb() const { return kb; }
+  __device__ int a_kcol(int k) const { return k * kBlockK; }
+  __device__ int b_kcol(int k) const { return k * kBlockK; }
+};
+
+// Split-bf16 "3-pass" product for fp32-faithful dot products on the tensor
+// core: A = [x_hi | x_lo], B = [w_hi | w_lo] (each 2*Kd wide) and
+//   acc = x_hi.w_hi + x_hi.w_lo + x_lo.w_hi
+// expressed as 3*nk k-blocks with remapped k coordinates.
+struct Split3Sched {
+  int M, n_tiles, nk, bn, kd;  // kd = padded real K (multiple of 64)
+  __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
+  __device__ Unit unit(int u) const {
+    const int mb = u / n_tiles, nb = u - mb * n_tiles;
+    Unit U;
+    U.a_row = mb * kBlockM;
+    U.rows = min(kBlockM, M - U.a_row);
+    U.b_row = nb * bn;
+    U.n0 = nb * bn;
+    return U;
+  }
+  __device__ int num_kb() const { return 3 * nk; }
+  __device__ int a_kcol(int k) const {
+    return k < 2 * nk ? (k % nk) * kBlockK : kd + (k - 2 * nk) * kBlockK;
+  }
+  __device__ int b_kcol(int k) const {
+    return k < nk ? k * kBlockK : (k < 2 * nk ? kd + (k - nk) * kBlockK : (k - 2 * nk) * kBlockK);
+  }
+};
+
+}  // namespace mp

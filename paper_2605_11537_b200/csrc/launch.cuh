@@ -1,0 +1,33 @@
+// Host-side helpers: TMA tensor-map encoding (driver entry point fetched at
+// run time, no -lcuda link) and the persistent GEMM launcher.
+#pragma once
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gemm_sm100.cuh"
+
+namespace mp {
+
+int num_sms();
+
+// 2-D bf16 row-major [rows x cols] tensor map, box = [box_rows x 64 cols], SWIZZLE_128B.
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                   uint32_t box_rows);
+
+template <int BN, int STAGES, class Sched, class Epi>
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched, const Epi& epi, int grid,
+                cudaStream_t st) {
+  auto kern = k_umma_gemm<BN, STAGES, Sched, Epi>;
+  const int smem = GemmSmem<BN, STAGES>::kBytes;
+  static bool configured = false;  // one attribute call per instantiation
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  if (grid < 1) grid = 1;
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+}  // namespace mp

@@ -1,0 +1,192 @@
+"""Kernel-level checks of libmoempmc.so against plain PyTorch references.
+
+These call the C-ABI directly (ctypes) on device tensors; the API-level parity
+against the CPU oracle lives in test_parity_gpu.py.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_11537_b200 import _lib  # noqa: E402
+from paper_2605_11537_b200._dev import ptr, require_device, stream_ptr  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return require_device()
+
+
+def _rel(a, b):
+    a = a.double()
+    b = b.double()
+    return float((a - b).abs().max() / max(b.abs().max().item(), 1e-30))
+
+
+@pytest.mark.parametrize(
+    "M,N,K",
+    [(128, 256, 64), (200, 256, 128), (1000, 384, 768), (77, 64, 64), (300, 128, 192), (4096, 2304, 768)],
+)
+@pytest.mark.parametrize("c_dtype", [0, 1])
+def test_dense_gemm(dev, M, N, K, c_dtype):
+    g = torch.Generator(device=dev).manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, device=dev, generator=g).bfloat16()
+    B = torch.randn(N, K, device=dev, generator=g).bfloat16()
+    C = torch.zeros(M, N, device=dev, dtype=torch.bfloat16 if c_dtype == 0 else torch.float32)
+    _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, c_dtype, N, None, 0, 0, stream_ptr())
+    ref = A.float() @ B.float().T
+    torch.cuda.synchronize()
+    assert _rel(C.float(), ref) < (1e-2 if c_dtype == 0 else 1e-5)
+
+
+def test_dense_gemm_bias_sigmoid_relu(dev):
+    M, N, K = 257, 384, 128
+    A = torch.randn(M, K, device=dev).bfloat16()
+    B = torch.randn(N, K, device=dev).bfloat16()
+    bias = torch.randn(N, device=dev)
+    C = torch.empty(M, N, device=dev)
+    _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 1, N, ptr(bias), 2, 128, stream_ptr())
+    ref = A.float() @ B.float().T + bias
+    ref[:, 128:] = torch.sigmoid(ref[:, 128:])
+    assert _rel(C, ref) < 1e-5
+    _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 1, N, None, 1, 0, stream_ptr())
+    assert _rel(C, (A.float() @ B.float().T).relu()) < 1e-5
+
+
+def test_histogram_and_caps(dev):
+    rng = np.random.default_rng(0)
+    L, T, E = 3, 1000, 37
+    a = rng.integers(0, E, size=(L, T)).astype(np.int32)
+    at = torch.from_numpy(a).to(dev)
+    dem = torch.empty(L, E, dtype=torch.int32, device=dev)
+    _lib.call("mp_histogram", ptr(at), L, T, E, ptr(dem), stream_ptr())
+    ref = np.stack([np.bincount(r, minlength=E) for r in a])
+    assert (dem.cpu().numpy() == ref).all()
+
+
+def test_heads_argmax(dev):
+    T, d, L, E, Eg = 500, 128, 3, 20, 32
+    h = torch.randn(T, d, device=dev).bfloat16()
+    heads = torch.zeros(((L * Eg + 63) // 64) * 64, d, device=dev)
+    w = torch.randn(L, E, d, device=dev)
+    for l in range(L):
+        heads[l * Eg : l * Eg + E] = w[l]
+    heads = heads.bfloat16()
+    out = torch.full((L, T), -1, dtype=torch.int32, device=dev)
+    _lib.call("mp_heads_argmax", ptr(h), ptr(heads), T, d, L, E, Eg, ptr(out), stream_ptr())
+    logits = torch.einsum("td,led->lte", h.float(), heads[: L * Eg].float().view(L, Eg, d)[:, :E])
+    ref = logits.argmax(-1)
+    agree = (out.long() == ref).float().mean().item()
+    assert agree > 0.999
+
+
+def test_router_exact(dev):
+    T, d, E, Eg = 1000, 128, 12, 64
+    x = torch.randn(T, d, device=dev)
+    w = torch.randn(E, d, device=dev)
+    w[5] = w[3]  # exact tie -> lower index
+    w_hi = w.bfloat16()
+    w_lo = (w - w_hi.float()).bfloat16()
+    whl = torch.zeros(Eg, 2 * d, device=dev, dtype=torch.bfloat16)
+    whl[:E, :d] = w_hi
+    whl[:E, d:] = w_lo
+    route = torch.full((T,), -1, dtype=torch.int32, device=dev)
+    nbytes = _lib.size_query("mp_router_workspace_bytes", T, d)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _lib.call("mp_route_top1", ptr(x), d, T, d, ptr(whl), ptr(w), E, Eg, 0.0, ptr(route), ptr(ws), nbytes,
+              stream_ptr())
+    ref = (x.double() @ w.double().T).argmax(-1)
+    assert (route.long() == ref).all()
+
+
+def test_sru_layer_matches_fp64(dev):
+    T, d = 700, 128
+    g = torch.Generator().manual_seed(5)
+    bound = 1.0 / np.sqrt(d)
+    W = (torch.rand(3 * d, d, generator=g, dtype=torch.float64) * 2 - 1) * bound
+    b = torch.zeros(3 * d, dtype=torch.float64)
+    b[d:] = (torch.rand(2 * d, generator=g, dtype=torch.float64) * 2 - 1) * bound
+    x = torch.randn(T, d, generator=g, dtype=torch.float64)
+    # fp64 reference (src/predictor.py:157-195)
+    proj = x @ W.T + b
+    u, f, r = proj[:, :d], torch.sigmoid(proj[:, d:2 * d]), torch.sigmoid(proj[:, 2 * d:])
+    c = torch.zeros(d, dtype=torch.float64)
+    href = torch.empty_like(x)
+    for t in range(T):
+        c = f[t] * c + (1 - f[t]) * u[t]
+        href[t] = r[t] * torch.tanh(c) + (1 - r[t]) * x[t]
+    xd = x.float().to(dev)
+    xb = xd.bfloat16()
+    Wd = W.to(dev).bfloat16()
+    bd = b.float().to(dev)
+    h32 = torch.empty(T, d, device=dev)
+    h16 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+    nf = torch.zeros(1, dtype=torch.int32, device=dev)
+    nbytes = _lib.size_query("mp_sru_workspace_bytes", T, d)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _lib.call("mp_sru_layer", ptr(xb), ptr(xd), ptr(Wd), ptr(bd), T, d, ptr(h32), ptr(h16), ptr(nf), ptr(ws), nbytes,
+              stream_ptr())
+    assert int(nf.item()) == 0
+    err = float((h32.double().cpu() - href).abs().max() / href.abs().max())
+    assert err < 1e-2, err
+
+
+def test_exec_map_and_ffn(dev):
+    rng = np.random.default_rng(3)
+    T, E, d, F = 1500, 10, 128, 256
+    route = rng.choice(E, size=T, p=np.array([0.5] + [0.5 / (E - 1)] * (E - 1))).astype(np.int32)
+    res = np.zeros(E, dtype=np.int32)
+    res[0] = 4  # expert 0 has 4 replicas
+    res[3] = 2
+    max_slots = int(res.sum()) + E
+    rt = torch.from_numpy(route).to(dev)
+    rs = torch.from_numpy(res).to(dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    tts = torch.empty(T, **i32)
+    corr = torch.empty(E, **i32)
+    ns = torch.empty(1, **i32)
+    rot = torch.empty(T, **i32)
+    tor = torch.full((T,), -1, **i32)
+    pstride = max_slots + (T + 127) // 128
+    prow = torch.empty(pstride, **i32)
+    prows = torch.empty(pstride, **i32)
+    eb = torch.empty(E + 1, **i32)
+    nbytes = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    for split in (0, 1):
+        rs = torch.from_numpy(res).to(dev)
+        _lib.call("mp_exec_map", ptr(rt), 1, T, E, max_slots, split, ptr(rs), ptr(tts), ptr(corr), ptr(ns), ptr(rot),
+                  ptr(tor), ptr(prow), ptr(prows), ptr(eb), ptr(ws), nbytes, stream_ptr())
+        torch.cuda.synchronize()
+        # closed form F6 on host
+        cnt = np.where(res > 0, res, (np.bincount(route, minlength=E) > 0).astype(np.int32))
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        seen = np.zeros(E, dtype=np.int64)
+        exp_slot = np.empty(T, dtype=np.int64)
+        for t, e in enumerate(route):
+            exp_slot[t] = off[e] + seen[e] % cnt[e]
+            seen[e] += 1
+        assert (tts.cpu().numpy() == exp_slot).all()
+        assert sorted(tor.cpu().numpy().tolist()) == list(range(T))
+        assert (rs.cpu().numpy() == cnt).all()
+        # FFN
+        dp, Fp = d, F
+        U = torch.randn(E, Fp, dp, device=dev) / np.sqrt(dp)
+        V = torch.randn(E, dp, Fp, device=dev) / np.sqrt(Fp)
+        x = torch.randn(T, dp, device=dev)
+        x0 = x.clone()
+        Ub, Vb = U.bfloat16().contiguous(), V.bfloat16().contiguous()
+        fb = _lib.size_query("mp_ffn_workspace_bytes", T, dp, Fp)
+        fws = torch.empty(fb, dtype=torch.uint8, device=dev)
+        _lib.call("mp_moe_ffn", ptr(x), T, dp, Fp, E, ptr(Ub), ptr(Vb), ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+                  ptr(fws), fb, stream_ptr())
+        xb = x0.bfloat16().float()
+        ref = x0.clone()
+        rl = torch.from_numpy(route).long().to(dev)
+        for e in range(E):
+            m = rl == e
+            hid = (xb[m] @ Ub[e].float().T).relu().bfloat16().float()
+            ref[m] += hid @ Vb[e].float().T
+        assert _rel(x - x0, ref - x0) < 1e-3
