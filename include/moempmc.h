@@ -101,6 +101,16 @@ MP_API int mp_exec_map(const int32_t* route, int L, int T, int E, int max_slots,
                 int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin, void* ws,
                 size_t ws_bytes, void* stream);
 
+/* Replica segments from an explicit token -> slot map (a reference Placement,
+ * src/router_oracle.py:64-74, as consumed by moe_forward :160-175): rows are
+ * grouped by slot (stable in token order); slot_expert[s] must be
+ * non-decreasing (slots sorted by (expert, ordinal)). Outputs as mp_exec_map
+ * for one layer; piece arrays hold S + ceil(T/128) entries, exp_begin E + 1. */
+MP_API size_t mp_segments_workspace_bytes(int T, int S);
+MP_API int mp_segments_from_slots(const int32_t* token_to_slot, const int32_t* slot_expert, int T, int S, int E,
+                                  int split_m, int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows,
+                                  int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------ K1 / generic
  * C[M x ldc] = epi(A[M x K] * B[N x K]^T) on tcgen05 (bf16 in, fp32 acc).
  * K % 64 == 0, N % 64 == 0 (pad with zero rows), 16-byte aligned rows.
@@ -120,7 +130,15 @@ MP_API int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int
  */
 MP_API size_t mp_sru_workspace_bytes(int T, int d);
 MP_API int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* w_cat, const float* b_cat, int T, int d,
-                 float* h_f32, void* h_bf16, int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
+                        const float* c0, float* h_f32, void* h_bf16, float* c_last, int32_t* nonfinite, void* ws,
+                        size_t ws_bytes, void* stream);
+/* c0 (d floats, NULL = zeros, src/predictor.py:190) is the cell state entering token 0 --
+ * sru_cell's c_prev, or the carry of a preceding token shard; c_last (nullable) receives the
+ * cell state after the last token. nonfinite (1 int) is OR-ed with 1 on NaN/inf state
+ * (reference raises NumericError, src/predictor.py:170-171). */
+
+/* sparsemax of n rows of E float64 logits (src/predictor.py:198-209), E <= 256. */
+MP_API int mp_sparsemax_rows(const double* z, int n, int E, double* out, void* stream);
 
 /* ------------------------------------------------------------------ K3
  * Predicted expert per (layer, token) = argmax_e h_t . heads[l,e]
@@ -153,14 +171,16 @@ MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w
  * residual combine (src/router_oracle.py:101-111, 127-134):
  *   xperm[row]   = bf16(x[tok_of_row[row]])                       (gather)
  *   hid[row]     = relu(xperm[row] . U_e^T)                        (GEMM1)
- *   x[tok][:]   += hid[row] . V_e^T                                (GEMM2, scatter epilogue)
+ *   y[tok][:]   += hid[row] . V_e^T                                (GEMM2, scatter epilogue)
  * u: (E*Fp) x dp bf16, v: (E*dp) x Fp bf16 (zero padded, dp%64==0, Fp%256==0),
- * x: T x dp fp32 updated in place. Pieces from mp_exec_map (one layer).
+ * x, y: T x dp fp32; y == x gives the in-place residual stream update,
+ * y = zeros gives expert_forward alone. Pieces from mp_exec_map /
+ * mp_segments_from_slots (one layer). ws >= mp_ffn_workspace_bytes(T, dp, Fp).
  */
 MP_API size_t mp_ffn_workspace_bytes(int T, int dp, int Fp);
-MP_API int mp_moe_ffn(float* x, int T, int dp, int Fp, int E, const void* u, const void* v, const int32_t* tok_of_row,
-               const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
-               size_t ws_bytes, void* stream);
+MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,
+                      const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                      const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ K9
  * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):

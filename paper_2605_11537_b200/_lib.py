@@ -45,14 +45,17 @@ SIGNATURES: dict[str, tuple] = {
     "mp_exec_map": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
     "mp_sru_workspace_bytes": (_Z, [_I, _I]),
-    "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _Z, _P]),
+    "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_sparsemax_rows": (_I, [_P, _I, _I, _P, _P]),
+    "mp_segments_workspace_bytes": (_Z, [_I, _I]),
+    "mp_segments_from_slots": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_heads_argmax": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P]),
     "mp_router_workspace_bytes": (_Z, [_I, _I]),
     "mp_route_top1": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _Z, _P]),
     "mp_router_weight_absmax": (_I, [_P, _I, _I, _P, _P]),
     "mp_route_top1_ex": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
     "mp_ffn_workspace_bytes": (_Z, [_I, _I, _I]),
-    "mp_moe_ffn": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_moe_ffn": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
 }
 

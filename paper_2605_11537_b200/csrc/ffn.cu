@@ -42,7 +42,7 @@ extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
   return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp);
 }
 
-extern "C" int mp_moe_ffn(float* x, int T, int dp, int Fp, int E, const void* u, const void* v,
+extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,
                           const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                           const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
   MP_REQUIRE(T >= 1 && E >= 1, MP_ERR_CONFIG, "mp_moe_ffn: bad T/E");
@@ -78,7 +78,7 @@ extern "C" int mp_moe_ffn(float* x, int T, int dp, int Fp, int E, const void* u,
     rc = make_tmap_bf16(&tb, v, (uint64_t)E * dp, Fp, Fp, bn);
     if (rc) return rc;
     SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64};
-    EpiScatterAdd e{x, dp, tok_of_row};
+    EpiScatterAdd e{y, dp, tok_of_row};
     if (bn == 256) rc = launch_gemm<256, 4>(ta, tb, s, e, grid, st);
     else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, s, e, grid, st);
     else rc = launch_gemm<64, 8>(ta, tb, s, e, grid, st);

@@ -7,8 +7,8 @@
 //   cap_replicas  src/planner.py:36-72   water-fill: L* = max level with
 //                 sum_e min(d_e, L*) <= C; +1 to the first C - sum experts with
 //                 d_e > L* ordered by (d_e desc, e asc).
-//   apply_layer   src/placement.py:109-165  slot(t) = off[e] + (rank_e(t) + r_e) mod cap_e,
-//                 r_e = min(res_prev_e, cap_e); events: rank k < cap_e - r_e gives
+//   apply_layer   src/placement.py:109-165  slot(t) = off[e] + (rank_e(t) + r_e) mod cnt_e,
+//                 r_e = min(res_prev_e, cap_e), cnt_e = min(cap_e, r_e + n_e); rank k < cnt_e - r_e gives
 //                 LOAD (r_e = 0, k = 0) or REPLICATE ordinal r_e + k.
 //   execution     src/simulator.py:185-203  cnt_e = res_e or 1 corrective LOAD,
 //                 slot(t) = off'[e] + rank_e(t) mod cnt_e.
@@ -147,13 +147,13 @@ __global__ void k_place_layer(const int32_t* __restrict__ demand, int E, const i
     if (n > 0) {
       r = min(rp, cap);
       off = max(rp - cap, 0);  // reclaim above the new cap
-      rn = cap;
+      rn = min(cap, r + n);    // replicas are created only as tokens arrive
     } else {
       r = 0;
       off = rp;  // offload every replica of an unmentioned expert
       rn = 0;
     }
-    cap_eff[b + e] = n > 0 ? cap : 0;
+    cap_eff[b + e] = rn;
     r_eff[b + e] = r;
     offloads[b + e] = off;
     res[b + e] = rn;
@@ -298,6 +298,58 @@ __global__ void k_exec_rank(const int32_t* __restrict__ route, int T, int E, int
   tok_of_row[(size_t)l * T + row] = t;
 }
 
+// Segments from an explicit token -> slot map. grid 1, block 1024.
+// size[s] (from the chunk histogram) -> slot_row (scan) -> pieces (scan).
+__global__ void k_seg_layer(const int32_t* __restrict__ size, const int32_t* __restrict__ slot_expert, int S, int E,
+                            int split_m, int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
+                            int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin) {
+  extern __shared__ int sm[];
+  __shared__ int red[40];
+  int* s_row = sm;          // S + 1
+  int* s_pc = s_row + S + 1;  // S + 1
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int n = size[s];
+    s_row[s] = n;
+    s_pc[s] = split_m ? cdiv(n, kBlockMRows) : (n > 0 ? 1 : 0);
+  }
+  __syncthreads();
+  const int total = block_exclusive_scan(s_row, S, red);
+  const int P = block_exclusive_scan(s_pc, S, red);
+  if (threadIdx.x == 0) {
+    s_row[S] = total;
+    s_pc[S] = P;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    slot_row_g[s] = s_row[s];
+    const int row0 = s_row[s], n = s_row[s + 1] - row0;
+    const int p0 = s_pc[s], np = s_pc[s + 1] - p0;
+    for (int p = 0; p < np; ++p) {
+      piece_row[p0 + p] = split_m ? row0 + p * kBlockMRows : row0;
+      piece_rows[p0 + p] = split_m ? min(kBlockMRows, n - p * kBlockMRows) : n;
+    }
+  }
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) {
+    int lo = 0, hi = S;  // first slot with slot_expert >= e
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (slot_expert[mid] < e) lo = mid + 1; else hi = mid;
+    }
+    exp_begin[e] = s_pc[lo];
+  }
+}
+
+__global__ void k_seg_rank(const int32_t* __restrict__ key, int T, int S, int nch, const int32_t* __restrict__ cc,
+                           const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ tok_of_row) {
+  __shared__ int se[kChunk];
+  const int ch = blockIdx.x;
+  int s;
+  const int rin = chunk_rank(key, T, 0, ch, se, &s);
+  const int t = ch * kChunk + threadIdx.x;
+  if (t >= T) return;
+  tok_of_row[slot_row_g[s] + cc[(size_t)ch * S + s] + rin] = t;
+}
+
 static inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 static cudaError_t set_smem(const void* fn, size_t bytes) {
@@ -425,6 +477,36 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
                                       piece_row, piece_rows, exp_begin, pieces_stride, err);
   k_exec_rank<<<dim3(nch, L), kChunk, 0, st>>>(route, T, E, nch, max_slots, cc, off_g, slot_row, token_to_slot,
                                                row_of_token, tok_of_row);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" size_t mp_segments_workspace_bytes(int T, int S) {
+  const int nch = cdiv(T > 0 ? T : 1, kChunk);
+  return align_up(sizeof(int32_t) * (size_t)nch * S) + 2 * align_up(sizeof(int32_t) * ((size_t)S + 1));
+}
+
+extern "C" int mp_segments_from_slots(const int32_t* token_to_slot, const int32_t* slot_expert, int T, int S, int E,
+                                      int split_m, int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows,
+                                      int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(T >= 1 && S >= 1 && E >= 1, MP_ERR_CONFIG, "mp_segments_from_slots: bad sizes T=%d S=%d E=%d", T, S, E);
+  MP_REQUIRE(ws_bytes >= mp_segments_workspace_bytes(T, S), MP_ERR_CONFIG, "mp_segments_from_slots: workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nch = cdiv(T, kChunk);
+  char* p = (char*)ws;
+  int32_t* cc = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)nch * S);
+  int32_t* size = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * ((size_t)S + 1));
+  int32_t* slot_row = (int32_t*)p;
+  const size_t sm_h = sizeof(int) * (size_t)S, sm_s = sizeof(int) * 2 * ((size_t)S + 1);
+  MP_REQUIRE(sm_h <= 200 * 1024 && sm_s <= 200 * 1024, MP_ERR_CONFIG, "mp_segments_from_slots: S too large");
+  MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
+  MP_CUDA_TRY(set_smem((const void*)k_seg_layer, sm_s));
+  k_chunk_hist<<<dim3(nch, 1), kChunk, sm_h, st>>>(token_to_slot, T, S, nch, cc);
+  k_chunk_prefix<<<1, 256, 0, st>>>(cc, nch, S, size);
+  k_seg_layer<<<1, 1024, sm_s, st>>>(size, slot_expert, S, E, split_m, slot_row, piece_row, piece_rows, exp_begin);
+  k_seg_rank<<<nch, kChunk, 0, st>>>(token_to_slot, T, S, nch, cc, slot_row, tok_of_row);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

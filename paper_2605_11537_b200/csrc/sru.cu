@@ -48,10 +48,10 @@ __global__ void k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, i
 
 // pass B: carry_in[ch] per channel (c_0 = 0 at the start of every batch).
 __global__ void k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
-                             float* __restrict__ carry) {
+                             const float* __restrict__ c0, float* __restrict__ carry) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d) return;
-  float run = 0.f;
+  float run = c0 ? c0[c] : 0.f;
   for (int ch = 0; ch < nch; ++ch) {
     const size_t o = (size_t)ch * d + c;
     carry[o] = run;
@@ -62,7 +62,8 @@ __global__ void k_scan_carry(const float* __restrict__ aggA, const float* __rest
 // pass C: replay each chunk from its carry; h = r tanh(c) + (1 - r) x.
 __global__ void k_scan_output(const __nv_bfloat16* __restrict__ ufr, const float* __restrict__ x, int T, int d,
                               const float* __restrict__ carry, float* __restrict__ h32,
-                              __nv_bfloat16* __restrict__ h16, int32_t* __restrict__ nonfinite) {
+                              __nv_bfloat16* __restrict__ h16, float* __restrict__ c_last,
+                              int32_t* __restrict__ nonfinite) {
   const int cp = blockIdx.x * kScanThreads + threadIdx.x;
   if (2 * cp >= d) return;
   const int ch = blockIdx.y;
@@ -83,12 +84,50 @@ __global__ void k_scan_output(const __nv_bfloat16* __restrict__ ufr, const float
     *reinterpret_cast<float2*>(h32 + (size_t)t * d + 2 * cp) = make_float2(h0, h1);
     *reinterpret_cast<__nv_bfloat162*>(h16 + (size_t)t * d + 2 * cp) = __floats2bfloat162_rn(h0, h1);
   }
+  if (c_last && t1 == T) *reinterpret_cast<float2*>(c_last + 2 * cp) = make_float2(c0, c1);
   if (bad) atomicOr(nonfinite, 1);  // reference raises NumericError (src/predictor.py:170-171)
 }
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+// sparsemax rows (src/predictor.py:198-209) in float64, one thread per row:
+// insertion-sort descending into local memory, sorted-threshold tau.
+__global__ void k_sparsemax(const double* __restrict__ z, int n, int E, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double srt[256];
+  const double* zi = z + (size_t)i * E;
+  for (int j = 0; j < E; ++j) {
+    const double v = zi[j];
+    int k = j;
+    while (k > 0 && srt[k - 1] < v) {
+      srt[k] = srt[k - 1];
+      --k;
+    }
+    srt[k] = v;
+  }
+  double cum = 0.0, tau_cum = 0.0;
+  int ks = 1;
+  for (int k = 1; k <= E; ++k) {
+    cum += srt[k - 1];
+    if (1.0 + k * srt[k - 1] > cum) {
+      ks = k;
+      tau_cum = cum;
+    }
+  }
+  const double tau = (tau_cum - 1.0) / ks;
+  for (int j = 0; j < E; ++j) out[(size_t)i * E + j] = fmax(zi[j] - tau, 0.0);
+}
+
 }  // namespace mp
+
+extern "C" int mp_sparsemax_rows(const double* z, int n, int E, double* out, void* stream) {
+  MP_REQUIRE(n >= 0 && E >= 1 && E <= 256, MP_ERR_CONFIG, "sparsemax expects a nonempty 1-D vector (E <= 256)");
+  if (n == 0) return MP_OK;
+  mp::k_sparsemax<<<mp::cdiv(n, 128), 128, 0, (cudaStream_t)stream>>>(z, n, E, out);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
 
 using namespace mp;
 
@@ -98,8 +137,8 @@ extern "C" size_t mp_sru_workspace_bytes(int T, int d) {
 }
 
 extern "C" int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* w_cat, const float* b_cat, int T,
-                            int d, float* h_f32, void* h_bf16, int32_t* nonfinite, void* ws, size_t ws_bytes,
-                            void* stream) {
+                            int d, const float* c0, float* h_f32, void* h_bf16, float* c_last, int32_t* nonfinite,
+                            void* ws, size_t ws_bytes, void* stream) {
   MP_REQUIRE(T >= 1, MP_ERR_CONFIG, "batch must contain at least one token");
   MP_REQUIRE(d >= 64 && d % 64 == 0, MP_ERR_CONFIG, "mp_sru_layer: d=%d must be a multiple of 64 (pad)", d);
   MP_REQUIRE(ws_bytes >= mp_sru_workspace_bytes(T, d), MP_ERR_CONFIG, "mp_sru_layer: workspace too small");
@@ -119,8 +158,9 @@ extern "C" int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* 
   // K2
   const dim3 g(cdiv(d / 2, kScanThreads), nch);
   k_scan_aggregate<<<g, kScanThreads, 0, st>>>(ufr, T, d, aggA, aggB);
-  k_scan_carry<<<cdiv(d, 128), 128, 0, st>>>(aggA, aggB, nch, d, carry);
-  k_scan_output<<<g, kScanThreads, 0, st>>>(ufr, x_f32, T, d, carry, h_f32, (__nv_bfloat16*)h_bf16, nonfinite);
+  k_scan_carry<<<cdiv(d, 128), 128, 0, st>>>(aggA, aggB, nch, d, c0, carry);
+  k_scan_output<<<g, kScanThreads, 0, st>>>(ufr, x_f32, T, d, carry, h_f32, (__nv_bfloat16*)h_bf16, c_last,
+                                            nonfinite);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -126,8 +126,8 @@ def test_sru_layer_matches_fp64(dev):
     nf = torch.zeros(1, dtype=torch.int32, device=dev)
     nbytes = _lib.size_query("mp_sru_workspace_bytes", T, d)
     ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    _lib.call("mp_sru_layer", ptr(xb), ptr(xd), ptr(Wd), ptr(bd), T, d, ptr(h32), ptr(h16), ptr(nf), ptr(ws), nbytes,
-              stream_ptr())
+    _lib.call("mp_sru_layer", ptr(xb), ptr(xd), ptr(Wd), ptr(bd), T, d, None, ptr(h32), ptr(h16), None, ptr(nf),
+              ptr(ws), nbytes, stream_ptr())
     assert int(nf.item()) == 0
     err = float((h32.double().cpu() - href).abs().max() / href.abs().max())
     assert err < 1e-2, err
@@ -180,7 +180,7 @@ def test_exec_map_and_ffn(dev):
         Ub, Vb = U.bfloat16().contiguous(), V.bfloat16().contiguous()
         fb = _lib.size_query("mp_ffn_workspace_bytes", T, dp, Fp)
         fws = torch.empty(fb, dtype=torch.uint8, device=dev)
-        _lib.call("mp_moe_ffn", ptr(x), T, dp, Fp, E, ptr(Ub), ptr(Vb), ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+        _lib.call("mp_moe_ffn", ptr(x), ptr(x), T, dp, Fp, E, ptr(Ub), ptr(Vb), ptr(tor), ptr(prow), ptr(prows), ptr(eb),
                   ptr(fws), fb, stream_ptr())
         xb = x0.bfloat16().float()
         ref = x0.clone()
