@@ -57,6 +57,10 @@ MP_API int mp_device_info(int* sm_count, int* cc_major, int* cc_minor); /* host 
  * demand_counts (src/planner.py:27-33). assign values must lie in [0,E).
  */
 MP_API int mp_histogram(const int32_t* assign, int L, int T, int E, int32_t* demand, void* stream);
+/* Allocation-free form (CUDA-graph capturable). */
+MP_API size_t mp_histogram_workspace_bytes(int L, int T, int E);
+MP_API int mp_histogram_ws(const int32_t* assign, int L, int T, int E, int32_t* demand, void* ws, size_t ws_bytes,
+                           void* stream);
 
 /* Capped replica plan per layer, bit-exact with cap_replicas
  * (src/planner.py:36-72) via its closed-form water-fill; plan_all_layers
@@ -181,11 +185,23 @@ MP_API size_t mp_ffn_workspace_bytes(int T, int dp, int Fp);
 MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,
                       const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                       const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
+/* The same layer as three launches (gather | GEMM1 | GEMM2) sharing `ws`, for callers that
+ * time or overlap the grouped GEMMs separately. */
+MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
+                         size_t ws_bytes, void* stream);
+MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
+                     const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
+MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
+                       const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
+                       size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ K9
  * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):
  * dst <- src, `bytes` long, device-to-device (or peer) on `stream`. */
 MP_API int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+/* Operand staging: y[i] = bf16(x[i]) (round to nearest even), n % 4 == 0. */
+MP_API int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream);
 
 #ifdef __cplusplus
 }

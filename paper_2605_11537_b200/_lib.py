@@ -38,6 +38,8 @@ SIGNATURES: dict[str, tuple] = {
     "mp_last_error": (ctypes.c_char_p, []),
     "mp_device_info": (_I, [_P, _P, _P]),
     "mp_histogram": (_I, [_P, _I, _I, _I, _P, _P]),
+    "mp_histogram_workspace_bytes": (_Z, [_I, _I, _I]),
+    "mp_histogram_ws": (_I, [_P, _I, _I, _I, _P, _P, _Z, _P]),
     "mp_cap_replicas": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "mp_place_workspace_bytes": (_Z, [_I, _I, _I]),
     "mp_place": (_I, [_P, _I, _I, _I, _P, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
@@ -56,7 +58,11 @@ SIGNATURES: dict[str, tuple] = {
     "mp_route_top1_ex": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
     "mp_ffn_workspace_bytes": (_Z, [_I, _I, _I]),
     "mp_moe_ffn": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_ffn_gather": (_I, [_P, _I, _I, _I, _I, _P, _P, _Z, _P]),
+    "mp_ffn_up": (_I, [_I, _I, _I, _I, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_ffn_down": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
+    "mp_f32_to_bf16": (_I, [_P, _P, _Z, _P]),
 }
 
 _ERRORS = {

@@ -3,6 +3,7 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "epilogues.cuh"
@@ -105,6 +106,25 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
     if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, grid, st);
     return launch_gemm<64, 8>(ta, tb, s, e, grid, st);
   }
+}
+
+namespace mp {
+__global__ void k_f32_to_bf16(const float4* __restrict__ x, uint2* __restrict__ y, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = x[i];
+    y[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+  }
+}
+}  // namespace mp
+
+extern "C" int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream) {
+  MP_REQUIRE(n % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, MP_ERR_CONFIG,
+             "mp_f32_to_bf16: n %% 4 != 0 or misaligned");
+  const size_t n4 = n / 4;
+  const int grid = (int)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
+  if (n4) k_f32_to_bf16<<<grid, 256, 0, (cudaStream_t)stream>>>((const float4*)x, (uint2*)y, n4);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
 }
 
 extern "C" int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream) {

@@ -42,47 +42,76 @@ extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
   return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp);
 }
 
+static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
+                  const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, cudaStream_t st) {
+  // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&tb, u, (uint64_t)E * Fp, dp, dp, 256);
+  if (rc) return rc;
+  SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64};
+  EpiStoreBf16 e{hid, Fp, nullptr, 1, 0};
+  return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
+}
+
+static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
+                    const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
+                    const __nv_bfloat16* hid, cudaStream_t st) {
+  // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
+  const int bn = (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64);
+  CUtensorMap ta, tb;
+  int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&tb, v, (uint64_t)E * dp, Fp, Fp, bn);
+  if (rc) return rc;
+  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64};
+  EpiScatterAdd e{y, dp, tok_of_row};
+  if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
+  if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, num_sms(), st);
+  return launch_gemm<64, 8>(ta, tb, s, e, num_sms(), st);
+}
+
+#define FFN_CHECKS()                                                                                            \
+  MP_REQUIRE(T >= 1 && E >= 1, MP_ERR_CONFIG, "ffn: bad T/E");                                                  \
+  MP_REQUIRE(dp % 64 == 0 && Fp % 256 == 0, MP_ERR_CONFIG, "ffn: need dp%%64==0 and Fp%%256==0 (dp=%d Fp=%d)", dp, \
+             Fp);                                                                                               \
+  MP_REQUIRE(ws_bytes >= mp_ffn_workspace_bytes(T, dp, Fp), MP_ERR_CONFIG, "ffn: workspace too small");          \
+  __nv_bfloat16* xperm = (__nv_bfloat16*)ws;                                                                    \
+  __nv_bfloat16* hid = (__nv_bfloat16*)((char*)ws + al(sizeof(__nv_bfloat16) * (size_t)T * dp));                \
+  (void)xperm;                                                                                                  \
+  (void)hid;
+
+extern "C" int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
+                             size_t ws_bytes, void* stream) {
+  FFN_CHECKS();
+  k_gather_rows<<<cdiv(T * 32, 256), 256, 0, (cudaStream_t)stream>>>(x, T, dp, tok_of_row, xperm);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row,
+                         const int32_t* piece_rows, const int32_t* exp_begin, void* ws, size_t ws_bytes,
+                         void* stream) {
+  FFN_CHECKS();
+  return ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, (cudaStream_t)stream);
+}
+
+extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
+                           const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
+                           size_t ws_bytes, void* stream) {
+  FFN_CHECKS();
+  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, (cudaStream_t)stream);
+}
+
 extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,
                           const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                           const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
-  MP_REQUIRE(T >= 1 && E >= 1, MP_ERR_CONFIG, "mp_moe_ffn: bad T/E");
-  MP_REQUIRE(dp % 64 == 0 && Fp % 256 == 0, MP_ERR_CONFIG, "mp_moe_ffn: need dp%%64==0 and Fp%%256==0 (dp=%d Fp=%d)",
-             dp, Fp);
-  MP_REQUIRE(ws_bytes >= mp_ffn_workspace_bytes(T, dp, Fp), MP_ERR_CONFIG, "mp_moe_ffn: workspace too small");
+  FFN_CHECKS();
   cudaStream_t st = (cudaStream_t)stream;
-  __nv_bfloat16* xperm = (__nv_bfloat16*)ws;
-  __nv_bfloat16* hid = (__nv_bfloat16*)((char*)ws + al(sizeof(__nv_bfloat16) * (size_t)T * dp));
-
   k_gather_rows<<<cdiv(T * 32, 256), 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
   MP_CUDA_TRY(cudaGetLastError());
-
-  const int grid = num_sms();
-  // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
-  {
-    CUtensorMap ta, tb;
-    int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
-    if (rc) return rc;
-    rc = make_tmap_bf16(&tb, u, (uint64_t)E * Fp, dp, dp, 256);
-    if (rc) return rc;
-    SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64};
-    EpiStoreBf16 e{hid, Fp, nullptr, 1, 0};
-    rc = launch_gemm<256, 4>(ta, tb, s, e, grid, st);
-    if (rc) return rc;
-  }
-  // GEMM2: x[tok] += hid . V_e^T   [rows x dp]
-  {
-    const int bn = (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64);
-    CUtensorMap ta, tb;
-    int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
-    if (rc) return rc;
-    rc = make_tmap_bf16(&tb, v, (uint64_t)E * dp, Fp, Fp, bn);
-    if (rc) return rc;
-    SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64};
-    EpiScatterAdd e{y, dp, tok_of_row};
-    if (bn == 256) rc = launch_gemm<256, 4>(ta, tb, s, e, grid, st);
-    else if (bn == 128) rc = launch_gemm<128, 6>(ta, tb, s, e, grid, st);
-    else rc = launch_gemm<64, 8>(ta, tb, s, e, grid, st);
-    if (rc) return rc;
-  }
-  return MP_OK;
+  int rc = ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, st);
+  if (rc) return rc;
+  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, st);
 }

@@ -382,6 +382,26 @@ extern "C" int mp_histogram(const int32_t* assign, int L, int T, int E, int32_t*
   return MP_OK;
 }
 
+extern "C" size_t mp_histogram_workspace_bytes(int L, int T, int E) {
+  return (size_t)L * cdiv(T > 0 ? T : 1, kChunk) * E * sizeof(int32_t);
+}
+
+// Same as mp_histogram with a caller-provided workspace (graph-capturable, no allocation).
+extern "C" int mp_histogram_ws(const int32_t* assign, int L, int T, int E, int32_t* demand, void* ws, size_t ws_bytes,
+                               void* stream) {
+  MP_REQUIRE(L >= 1 && T >= 1 && E >= 1, MP_ERR_CONFIG, "mp_histogram_ws: bad sizes L=%d T=%d E=%d", L, T, E);
+  MP_REQUIRE(ws_bytes >= mp_histogram_workspace_bytes(L, T, E), MP_ERR_CONFIG, "mp_histogram_ws: workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nch = cdiv(T, kChunk);
+  const size_t sm = sizeof(int) * (size_t)E;
+  MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_histogram_ws: E=%d too large", E);
+  MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm));
+  k_chunk_hist<<<dim3(nch, L), kChunk, sm, st>>>(assign, T, E, nch, (int32_t*)ws);
+  k_chunk_prefix<<<L, 256, 0, st>>>((int32_t*)ws, nch, E, demand);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
 extern "C" int mp_cap_replicas(const int32_t* demand, int L, int E, int capacity, int unit_rows, int32_t* caps,
                                int32_t* infeasible, void* stream) {
   MP_REQUIRE(capacity >= 1, MP_ERR_CONFIG, "capacity must be >= 1, got %d", capacity);

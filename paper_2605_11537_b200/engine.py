@@ -1,0 +1,305 @@
+"""Device-resident MoE-MPMC inference pipeline (the benchmarked hot path).
+
+One batch ("step") = the paper's Alg. 2 + Alg. 1 + the MoE forward, all on the
+GPU with no host synchronisation (reference call stack: src/simulator.py:127-208
+driving src/predictor.py:212-223, src/planner.py:27-85, src/placement.py:109-180,
+src/router_oracle.py:119-135):
+
+  1. predict    S SRU layers over the batch token sequence + per-layer head argmax
+                (mp_sru_layer x S, mp_heads_argmax)                -> pred (L, T)
+  2. plan+place histogram -> capped replica plan -> residency update / token walk
+                for all L layers (mp_histogram_ws, mp_cap_replicas, mp_place)
+  3. forward    per MoE layer: true top-1 routing (mp_route_top1_ex), execution
+                map onto the resident replicas + corrective loads + replica-segment
+                permutation (mp_exec_map), gather, grouped expert GEMM1 (+ReLU),
+                grouped GEMM2 with scatter + residual combine (mp_ffn_*).
+
+Replication modes (SURVEY.md §7 baselines):
+  "off"   distinct-only caps (one replica per demanded expert), each replica's
+          rows are one serial work unit  -> the non-replicated GPU baseline (ii)
+  "on"    capped replica plan (demand in M-tiles by default),
+          each replica one work unit                                     (iii)
+  "split" like "on" but every 128-row M-tile is its own work unit (upper bound)
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import asdict, dataclass
+
+import torch
+
+from . import _lib
+from ._dev import ptr, require_device, round_up, stream_ptr
+from .predictor import DeviceSru
+from .router_oracle import DeviceMoeLayer, router_eg
+
+DISTINCT_ONLY_UNIT = 1 << 30  # ceil(n / unit) == 1 for every demanded expert
+
+
+@dataclass
+class PipelineConfig:
+    num_layers: int = 12          # Switch-base MoE layers
+    num_experts: int = 128        # Switch-base-128
+    d_model: int = 768
+    d_ff: int = 3072
+    tokens: int = 16384           # tokens per batch (per GPU)
+    sru_layers: int = 10          # src/predictor.py:19
+    capacity: int = 296           # replica slots per layer (2 x 148 SMs)
+    demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
+    replication: str = "on"       # on | off | split
+    predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
+    skew: float = 1.2
+    noise: float = 0.1
+    seed: int = 0
+
+    def as_dict(self):
+        return asdict(self)
+
+
+class SyntheticSwitch:
+    """Device-side synthetic Switch-base workload with the reference's distributions
+    (src/workload.py:123-313): unit expert centroids in the first d/2 "routing"
+    dimensions, Zipf(skew) popularity over a seeded permutation, a seeded expert
+    permutation per layer, embeddings = centroid + N(0, noise^2) resampled until
+    the router margin is >= 0.02, router rows = permuted centroids, U ~ N(0, 1/d),
+    V ~ N(0, 1/F) with the routing rows of V zeroed (so routing is reproducible)."""
+
+    MARGIN = 0.02
+
+    def __init__(self, cfg: PipelineConfig, device: torch.device):
+        self.cfg = cfg
+        self.dev = device
+        g = torch.Generator(device=device).manual_seed(cfg.seed)
+        self.g = g
+        E, d, L = cfg.num_experts, cfg.d_model, cfg.num_layers
+        self.k = max(1, d // 2)
+        c = torch.randn(E, self.k, device=device, generator=g, dtype=torch.float64)
+        c = c / c.norm(dim=1, keepdim=True)
+        self.centroids = torch.zeros(E, d, device=device)
+        self.centroids[:, : self.k] = c.float()
+        rank = torch.empty(E, dtype=torch.long, device=device)
+        rank[torch.randperm(E, device=device, generator=g)] = torch.arange(E, device=device)
+        w = 1.0 / (rank.double() + 1.0) ** cfg.skew
+        self.probs = (w / w.sum()).float()
+        perms = [torch.arange(E, device=device)]
+        for _ in range(1, L):
+            perms.append(torch.randperm(E, device=device, generator=g))
+        self.perms = torch.stack(perms)  # (L, E): expert at layer l of layer-0 expert e
+
+    def router(self, l: int) -> torch.Tensor:
+        r = torch.empty_like(self.centroids)
+        r[self.perms[l]] = self.centroids
+        return r
+
+    def expert_weights(self, l: int):
+        cfg = self.cfg
+        E, d, F = cfg.num_experts, cfg.d_model, cfg.d_ff
+        u = torch.empty(E, F, d, device=self.dev, dtype=torch.bfloat16)
+        v = torch.empty(E, d, F, device=self.dev, dtype=torch.bfloat16)
+        for e in range(E):  # per expert to bound the fp32 temporaries
+            u[e] = (torch.randn(F, d, device=self.dev, generator=self.g) / math.sqrt(d)).to(torch.bfloat16)
+            ve = torch.randn(d, F, device=self.dev, generator=self.g) / math.sqrt(F)
+            ve[: self.k] = 0.0
+            v[e] = ve.to(torch.bfloat16)
+        return u, v
+
+    def batch(self, T: int):
+        """(embeddings (T, d) fp32, layer-0 experts (T,), oracle routing (L, T))."""
+        e0 = torch.multinomial(self.probs, T, replacement=True, generator=self.g)
+        base = self.centroids[e0]
+        emb = torch.empty_like(base)
+        pending = torch.arange(T, device=self.dev)
+        rout = self.centroids[:, : self.k].double()
+        for _ in range(100):
+            cand = base[pending] + self.cfg.noise * torch.randn(len(pending), self.cfg.d_model, device=self.dev,
+                                                                generator=self.g)
+            logits = cand[:, : self.k].double() @ rout.T
+            own = logits.gather(1, e0[pending, None]).squeeze(1)
+            logits.scatter_(1, e0[pending, None], -math.inf)
+            ok = own - logits.max(dim=1).values >= self.MARGIN
+            emb[pending[ok]] = cand[ok]
+            pending = pending[~ok]
+            if len(pending) == 0:
+                break
+        return emb, e0, self.perms[:, e0]
+
+
+class MoEPipeline:
+    """Weights + buffers resident in HBM; ``step`` runs one batch with zero host syncs."""
+
+    def __init__(self, cfg: PipelineConfig, device: torch.device | None = None, workload: SyntheticSwitch | None = None):
+        self.cfg = cfg
+        self.dev = device or require_device()
+        dev = self.dev
+        L, E, d, F, T = cfg.num_layers, cfg.num_experts, cfg.d_model, cfg.d_ff, cfg.tokens
+        assert d % 64 == 0 and F % 256 == 0, "engine expects Switch-base-like padded sizes"
+        self.wl = workload or SyntheticSwitch(cfg, dev)
+        self.dp, self.Fp = d, F
+        # ---- MoE layers (bf16 expert weights, split-bf16 router)
+        self.layers = []
+        for l in range(L):
+            u, v = self.wl.expert_weights(l)
+            self.layers.append(DeviceMoeLayer.from_device(self.wl.router(l), u, v))
+        # ---- predictor (S SRU layers + heads)
+        g = torch.Generator(device=dev).manual_seed(cfg.seed + 1)
+        bound = 1.0 / math.sqrt(d)
+
+        def draw(*shape):
+            return (torch.rand(*shape, device=dev, generator=g, dtype=torch.float64) * 2 - 1) * bound
+
+        sru = []
+        for _ in range(cfg.sru_layers):
+            w, w_f, w_r, b_f, b_r = draw(d, d), draw(d, d), draw(d, d), draw(d), draw(d)
+            if cfg.predictor == "constructed":
+                b_r = b_r - 8.0  # highway-open: h ~= x, so heads = router rows forecast the routing
+            sru.append((w, w_f, w_r, b_f, b_r))
+        if cfg.predictor == "constructed":
+            heads = torch.stack([self.wl.router(l) for l in range(L)]).double()
+        else:
+            heads = draw(L, E, d)
+        self.sru = DeviceSru([tuple(t.cpu().numpy() for t in lay) for lay in sru], heads.cpu().numpy(), dev)
+        # ---- buffers
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.assign = torch.empty(L, T, **i32)
+        self.demand = torch.empty(L, E, **i32)
+        self.caps = torch.empty(L, E, **i32)
+        self.infeasible = torch.empty(L, **i32)
+        self.res = torch.zeros(L, E, **i32)
+        self.pred_slot = torch.empty(L, T, **i32)
+        self.pred_event = torch.empty(L, T, **i32)
+        self.offloads = torch.empty(L, E, **i32)
+        self.fallback = torch.empty(L, **i32)
+        self.num_slots = torch.empty(L, **i32)
+        self.route = torch.empty(L, T, **i32)
+        self.max_slots = max(cfg.capacity, E) + E
+        self.exec_slot = torch.empty(L, T, **i32)
+        self.corrective = torch.empty(L, E, **i32)
+        self.exec_slots = torch.empty(L, **i32)
+        self.tok_of_row = torch.empty(L, T, **i32)
+        pstride = self.max_slots + (T + 127) // 128
+        self.piece_row = torch.empty(L, pstride, **i32)
+        self.piece_rows = torch.empty(L, pstride, **i32)
+        self.exp_begin = torch.empty(L, E + 1, **i32)
+        self.nonfinite = torch.zeros(1, **i32)
+        self.h32 = [torch.empty(T, d, device=dev) for _ in range(2)]
+        self.h16 = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+        self.x16 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+
+        def ws(n):
+            return torch.empty(max(int(n), 256), dtype=torch.uint8, device=dev)
+
+        self.ws_sru_n = _lib.size_query("mp_sru_workspace_bytes", T, d)
+        self.ws_sru = ws(self.ws_sru_n)
+        self.ws_hist_n = _lib.size_query("mp_histogram_workspace_bytes", L, T, E)
+        self.ws_hist = ws(self.ws_hist_n)
+        self.ws_place_n = _lib.size_query("mp_place_workspace_bytes", L, T, E)
+        self.ws_place = ws(self.ws_place_n)
+        self.ws_exec_n = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, self.max_slots)
+        self.ws_exec = ws(self.ws_exec_n)
+        self.ws_router_n = _lib.size_query("mp_router_workspace_bytes", T, d)
+        self.ws_router = ws(self.ws_router_n)
+        self.ws_ffn_n = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+        self.ws_ffn = ws(self.ws_ffn_n)
+        self.launches_per_step = None
+
+    # ------------------------------------------------------------------ pieces of a step
+    def predict(self, x: torch.Tensor, sp: int) -> int:
+        """Alg. 2: SRU stack over the batch sequence, head argmax -> self.assign. Returns #launches."""
+        cfg, T, d = self.cfg, self.cfg.tokens, self.dp
+        n = 0
+        _lib.call("mp_f32_to_bf16", ptr(x), ptr(self.x16), T * d, sp)
+        n += 1
+        cur32, cur16 = x, self.x16
+        for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
+            h32, h16 = self.h32[i % 2], self.h16[i % 2]
+            _lib.call("mp_sru_layer", ptr(cur16), ptr(cur32), ptr(W), ptr(B), T, d, None, ptr(h32), ptr(h16), None,
+                      ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
+            n += 4
+            cur32, cur16 = h32, h16
+        _lib.call("mp_heads_argmax", ptr(cur16), ptr(self.sru.heads), T, d, cfg.num_layers, cfg.num_experts,
+                  self.sru.Eg, ptr(self.assign), sp)
+        return n + 1
+
+    def plan_and_place(self, sp: int) -> int:
+        """Alg. 1: demand histogram -> capped plan -> residency + token walk for all layers."""
+        cfg, L, T, E = self.cfg, self.cfg.num_layers, self.cfg.tokens, self.cfg.num_experts
+        unit = DISTINCT_ONLY_UNIT if cfg.replication == "off" else cfg.demand_unit
+        _lib.call("mp_histogram_ws", ptr(self.assign), L, T, E, ptr(self.demand), ptr(self.ws_hist), self.ws_hist_n,
+                  sp)
+        _lib.call("mp_cap_replicas", ptr(self.demand), L, E, cfg.capacity, unit, ptr(self.caps),
+                  ptr(self.infeasible), sp)
+        _lib.call("mp_place", ptr(self.assign), L, T, E, ptr(self.caps), cfg.capacity, cfg.capacity, ptr(self.res),
+                  ptr(self.pred_slot), ptr(self.pred_event), ptr(self.offloads), ptr(self.fallback),
+                  ptr(self.num_slots), ptr(self.ws_place), self.ws_place_n, sp)
+        return 2 + 1 + 4
+
+    def layer(self, l: int, x: torch.Tensor, sp: int, ev=None) -> int:
+        """One MoE layer in place on the residual stream x."""
+        cfg, T, E, d, F = self.cfg, self.cfg.tokens, self.cfg.num_experts, self.dp, self.Fp
+        lay = self.layers[l]
+        split = 1 if cfg.replication == "split" else 0
+        _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
+                  ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
+        _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
+                  ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
+                  ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]),
+                  ptr(self.ws_exec), self.ws_exec_n, sp)
+        _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
+        if ev is not None:
+            ev[0].record()
+        _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
+                  ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
+        if ev is not None:
+            ev[1].record()
+        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
+                  ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
+        if ev is not None:
+            ev[2].record()
+        return 3 + 4 + 1 + 1 + 1
+
+    def step(self, x: torch.Tensor, events=None) -> int:
+        """Run one batch on the current stream; x (T, d) fp32 is the residual stream (in/out).
+
+        events: optional list (per layer) of 3 CUDA events bracketing GEMM1 / GEMM2.
+        Returns the number of kernel launches issued."""
+        sp = stream_ptr()
+        n = self.predict(x, sp)
+        n += self.plan_and_place(sp)
+        for l in range(self.cfg.num_layers):
+            n += self.layer(l, x, sp, events[l] if events is not None else None)
+        self.launches_per_step = n
+        return n
+
+    # ------------------------------------------------------------------ accounting
+    def expert_weight_bytes(self) -> int:
+        """bf16 bytes of one expert's U + V (4 d F)."""
+        return 4 * self.cfg.d_model * self.cfg.d_ff
+
+    def touched_experts(self) -> torch.Tensor:
+        """(L,) experts that received tokens in the last step (device)."""
+        return (self.exp_begin[:, 1:] > self.exp_begin[:, :-1]).sum(dim=1)
+
+
+def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor) -> DeviceMoeLayer:
+    """DeviceMoeLayer from device tensors already in kernel layout (d % 64 == 0, F % 256 == 0)."""
+    lay = DeviceMoeLayer.__new__(DeviceMoeLayer)
+    E, d = router.shape
+    F = u.shape[1]
+    lay.E, lay.d, lay.F, lay.dp, lay.Fp = E, d, F, d, F
+    lay.Eg = router_eg(E)
+    w32 = router.float().contiguous()
+    hi = w32.to(torch.bfloat16)
+    lo = (w32 - hi.float()).to(torch.bfloat16)
+    lay.w_hl = torch.zeros(lay.Eg, 2 * d, device=router.device, dtype=torch.bfloat16)
+    lay.w_hl[:E, :d] = hi
+    lay.w_hl[:E, d:] = lo
+    lay.w32 = w32
+    lay.w_abs = torch.empty(d, device=router.device)
+    _lib.call("mp_router_weight_absmax", ptr(w32), E, d, ptr(lay.w_abs), stream_ptr())
+    lay.U = u.reshape(E * F, d).contiguous()
+    lay.V = v.reshape(E * d, F).contiguous()
+    return lay
+
+
+DeviceMoeLayer.from_device = staticmethod(_layer_from_device)
