@@ -186,14 +186,20 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
                       const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                       const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 /* The same layer as three launches (gather | GEMM1 | GEMM2) sharing `ws`, for callers that
- * time or overlap the grouped GEMMs separately. */
+ * time or overlap the grouped GEMMs separately. tiled != 0: u / v are in the pre-tiled layout
+ * of mp_tile_kmajor (BN 256 for u, mp_ffn_down_bn(dp) for v), so every weight TMA box is one
+ * contiguous HBM burst instead of BN strided 128-byte rows. */
 MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                          size_t ws_bytes, void* stream);
-MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
-                     const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
-MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
+MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int tiled, const int32_t* piece_row,
+                     const int32_t* piece_rows, const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
+MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, int tiled, const int32_t* tok_of_row,
                        const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
                        size_t ws_bytes, void* stream);
+MP_API int mp_ffn_down_bn(int dp);
+/* Weight layout transform for the grouped GEMM B operand:
+ * dst[g][n / BN][k / 64][n % BN][k % 64] = src[g * N + n][k]   (bf16, G groups of N x K). */
+MP_API int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int BN, void* stream);
 
 /* ------------------------------------------------------------------ K9
  * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):

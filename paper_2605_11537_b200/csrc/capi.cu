@@ -84,7 +84,7 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
                             const float* bias, int act, int sig_from, void* stream) {
   MP_REQUIRE(M >= 1 && N >= 64 && K >= 64 && K % 64 == 0 && N % 64 == 0, MP_ERR_CONFIG,
              "mp_gemm_bf16: need K%%64==0, N%%64==0 (M=%d N=%d K=%d)", M, N, K);
-  MP_REQUIRE(ldc >= N, MP_ERR_CONFIG, "mp_gemm_bf16: ldc < N");
+  MP_REQUIRE(ldc >= N || ldc == 0, MP_ERR_CONFIG, "mp_gemm_bf16: ldc < N");
   cudaStream_t st = (cudaStream_t)stream;
   const int bn = (N % 256 == 0) ? 256 : (N % 128 == 0 ? 128 : 64);
   CUtensorMap ta, tb;

@@ -12,6 +12,10 @@
 #include "epilogues.cuh"
 #include "launch.cuh"
 
+#include <algorithm>
+
+extern "C" int mp_ffn_down_bn(int dp);
+
 namespace mp {
 
 // xperm[row] = bf16(x[tok_of_row[row]]); one warp per row, 8-byte lanes.
@@ -34,38 +38,70 @@ __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const 
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+// dst[g][nt][kb][r][c] = src[g*N + nt*BN + r][kb*64 + c], 16-byte granules.
+__global__ void k_tile_kmajor(const uint4* __restrict__ src, uint4* __restrict__ dst, int G, int N, int K, int BN) {
+  const size_t total = (size_t)G * N * K / 8;
+  const int kq = K / 8;  // 16-byte granules per source row
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i / kq;
+    const int gk = (int)(i - row * kq);  // granule within the row
+    const int g = (int)(row / N), n = (int)(row - (size_t)g * N);
+    const int nt = n / BN, r = n - nt * BN, kb = gk / 8, c = gk - kb * 8;
+    const size_t o = ((((size_t)g * (N / BN) + nt) * (K / 64) + kb) * BN + r) * 8 + c;
+    dst[o] = src[i];
+  }
+}
+
 }  // namespace mp
 
 using namespace mp;
+
+extern "C" int mp_ffn_down_bn(int dp) { return (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64); }
+
+extern "C" int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int BN, void* stream) {
+  MP_REQUIRE(G >= 1 && N % BN == 0 && K % 64 == 0 && (BN == 64 || BN == 128 || BN == 256), MP_ERR_CONFIG,
+             "mp_tile_kmajor: need N %% BN == 0, K %% 64 == 0 (N=%d K=%d BN=%d)", N, K, BN);
+  const size_t total = (size_t)G * N * K / 8;
+  const int grid = (int)std::min<size_t>((total + 255) / 256, (size_t)num_sms() * 16);
+  k_tile_kmajor<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, G, N, K, BN);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
 
 extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
   return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp);
 }
 
+static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, int tiled) {
+  if (tiled) return make_tmap_bf16(tb, w, (uint64_t)E * N * (K / 64), 64, 64, bn);
+  return make_tmap_bf16(tb, w, (uint64_t)E * N, K, K, bn);
+}
+
 static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
-                  const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, cudaStream_t st) {
+                  const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, int tiled,
+                  cudaStream_t st) {
   // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
   if (rc) return rc;
-  rc = make_tmap_bf16(&tb, u, (uint64_t)E * Fp, dp, dp, 256);
+  rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled);
   if (rc) return rc;
-  SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64};
+  SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
   EpiStoreBf16 e{hid, Fp, nullptr, 1, 0};
   return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
 }
 
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
-                    const __nv_bfloat16* hid, cudaStream_t st) {
+                    const __nv_bfloat16* hid, int tiled, cudaStream_t st) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
-  const int bn = (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64);
+  const int bn = mp_ffn_down_bn(dp);
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
   if (rc) return rc;
-  rc = make_tmap_bf16(&tb, v, (uint64_t)E * dp, Fp, Fp, bn);
+  rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled);
   if (rc) return rc;
-  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64};
+  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
   EpiScatterAdd e{y, dp, tok_of_row};
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, num_sms(), st);
@@ -90,18 +126,19 @@ extern "C" int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const
   return MP_OK;
 }
 
-extern "C" int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row,
+extern "C" int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int tiled, const int32_t* piece_row,
                          const int32_t* piece_rows, const int32_t* exp_begin, void* ws, size_t ws_bytes,
                          void* stream) {
   FFN_CHECKS();
-  return ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, (cudaStream_t)stream);
+  return ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, tiled, (cudaStream_t)stream);
 }
 
-extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
-                           const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
-                           size_t ws_bytes, void* stream) {
+extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, int tiled,
+                           const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                           const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
   FFN_CHECKS();
-  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, (cudaStream_t)stream);
+  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, tiled,
+                  (cudaStream_t)stream);
 }
 
 extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,
@@ -111,7 +148,7 @@ extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E
   cudaStream_t st = (cudaStream_t)stream;
   k_gather_rows<<<cdiv(T * 32, 256), 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
   MP_CUDA_TRY(cudaGetLastError());
-  int rc = ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, st);
+  int rc = ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, 0, st);
   if (rc) return rc;
-  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, st);
+  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, 0, st);
 }

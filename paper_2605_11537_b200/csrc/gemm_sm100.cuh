@@ -2,11 +2,13 @@
 //
 //   D[128 x BN] = A[128 x K] * B[BN x K]^T      (bf16 in, fp32 accumulate in TMEM)
 //
-// Roles (256 threads, one CTA per SM):
+// Roles (384 threads, one CTA per SM):
 //   warp 0 lane 0 : TMA producer  (A and B k-blocks of 64 bf16 = one 128 B swizzle atom)
 //   warp 1 lane 0 : MMA issuer    (4 x tcgen05.mma 128xBNx16 per k-block)
 //   warp 2        : TMEM allocator (2 accumulator stages x BN columns)
-//   warps 4..7    : epilogue       (tcgen05.ld -> registers -> caller's Epilogue)
+//   warps 4..11   : epilogue, two warpgroups (tcgen05.ld -> registers -> caller's
+//                   Epilogue); warpgroup h owns accumulator columns [h*BN/2, (h+1)*BN/2)
+//                   when the epilogue is column-separable, else warpgroup 0 does all.
 // Pipelines: smem ring full/empty (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue).
 //
 // Work is expressed as "units": a unit is a run of rows [a_row, a_row+rows) of A
@@ -23,7 +25,8 @@ namespace mp {
 
 constexpr int kBlockM = 128;
 constexpr int kBlockK = 64;  // 64 bf16 = 128 B = one SWIZZLE_128B atom row
-constexpr int kGemmThreads = 256;
+constexpr int kEpiWarps = 8;
+constexpr int kGemmThreads = 128 + 32 * kEpiWarps;
 
 struct Unit {
   int a_row;  // first row of A (and of the row-indexed output)
@@ -38,16 +41,20 @@ struct GemmSmem {
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
-  static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16 + 1024;  // +1024 alignment slack
+  static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kBytes = kVecOffset + 2 * BN * 4 + 1024;  // + column-vector staging, alignment slack
 };
 
 // Scheduler concept:
 //   int num_units() const; Unit unit(int u) const; int num_kb() const;
 //   int a_kcol(int kb) const; int b_kcol(int kb) const;
 // Epilogue concept:
-//   template<int BN> void run(const Unit&, int mt, int r, uint32_t taddr) const
+//   static constexpr bool kSplitCols;   // columns independent -> two warpgroups split them
+//   const float* colvec() const;        // per-column vector (bias) or null; staged in smem per tile
+//   template<int NC> void run(const Unit&, int mt, int r, uint32_t taddr, int c0, const float* svec) const
 //   (r = row inside the 128-row tile owned by this thread; taddr = TMEM address of
-//    (lane quadrant, accumulator stage, column 0)).
+//    (lane quadrant, accumulator stage, column c0); the thread handles tile columns
+//    [c0, c0 + NC)).
 
 template <int BN, int STAGES, class Sched, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -62,6 +69,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* svec = reinterpret_cast<float*>(smem + L::kVecOffset);  // [2][BN]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -75,7 +83,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[s], kEpiWarps);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -91,6 +99,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
+      const uint64_t pol_stream = policy_evict_first();
       uint32_t stage = 0, phase = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const Unit U = sched.unit(u);
@@ -102,7 +111,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint8_t* sb = sa + L::kABytes;
             mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
             tma_load_2d(sa, &tmA, &full[stage], sched.a_kcol(kb), U.a_row + mt * kBlockM);
-            tma_load_2d(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row);
+            if constexpr (Sched::kStreamB)  // weights are read once per step: do not let them evict reused tiles
+              tma_load_2d_hint(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb), pol_stream);
+            else
+              tma_load_2d(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb));
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -147,18 +159,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // -------------------------------------------------------------- epilogue
-    const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int r = q * 32 + lane;     // row of the tile owned by this thread
+    const int q = warp & 3;            // TMEM lane quadrant this warp may access
+    const int half = (warp - 4) >> 2;  // warpgroup index
+    const int r = q * 32 + lane;       // row of the tile owned by this thread
+    constexpr bool split = Epi::kSplitCols;
+    constexpr int NC = split ? BN / 2 : BN;
+    const bool active = split || half == 0;
+    const int c0 = split ? half * (BN / 2) : 0;
     uint32_t tile = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const Unit U = sched.unit(u);
       const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
       for (int mt = 0; mt < mtiles; ++mt, ++tile) {
         const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
+        const float* vec = epi.colvec();
+        if (vec != nullptr) {  // stage this tile's column vector once (all epilogue threads, named barrier 1)
+          const int et = threadIdx.x - 128;
+          for (int i = et; i < BN; i += 32 * kEpiWarps) svec[(tile & 1) * BN + i] = __ldg(&vec[U.n0 + i]);
+          named_bar_sync(1, 32 * kEpiWarps);
+        }
         mbar_wait(&tfull[as], aph);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
-        epi.template run<BN>(U, mt, r, taddr);
+        if (active) {
+          const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c0;
+          epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0);
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[as]);
@@ -178,6 +203,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // Dense C[M x N] = A[M x K] B[N x K]^T, units = (m block, n block), n fastest.
 struct DenseSched {
+  static constexpr bool kStreamB = false;
   int M, n_tiles, kb, bn;
   __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
   __device__ Unit unit(int u) const {
@@ -192,10 +218,12 @@ struct DenseSched {
   __device__ int num_kb() const { return kb; }
   __device__ int a_kcol(int k) const { return k * kBlockK; }
   __device__ int b_kcol(int k) const { return k * kBlockK; }
+  __device__ int b_krow(int) const { return 0; }
 };
 
 // Device-built unit list (grouped GEMM over replica segments).
 struct ListSched {
+  static constexpr bool kStreamB = false;
   const int4* units;      // {a_row, rows, b_row, n0}
   const int* num_units_p;  // device scalar, written by the planner
   int kb;
@@ -207,6 +235,7 @@ struct ListSched {
   __device__ int num_kb() const { return kb; }
   __device__ int a_kcol(int k) const { return k * kBlockK; }
   __device__ int b_kcol(int k) const { return k * kBlockK; }
+  __device__ int b_krow(int) const { return 0; }
 };
 
 // Grouped GEMM over replica-segment pieces (built on device by mp_exec_map):
@@ -214,10 +243,12 @@ struct ListSched {
 // expert-major, then BN slice, then piece, so consecutive units (running on
 // neighbouring SMs at the same time) share one weight tile through L2.
 struct SegSched {
+  static constexpr bool kStreamB = true;
   const int32_t* piece_row;
   const int32_t* piece_rows;
   const int32_t* exp_begin;  // E + 1 entries
   int E, n_tiles, bn, n_per_expert, kb;
+  int b_tiled;  // B pre-tiled as [E][n_tiles][kb][bn rows][64 cols]: every TMA box is one contiguous burst
   __device__ int num_units() const { return exp_begin[E] * n_tiles; }
   __device__ Unit unit(int u) const {
     int lo = 0, hi = E;  // exp_begin[lo]*n_tiles <= u < exp_begin[hi]*n_tiles
@@ -229,11 +260,13 @@ struct SegSched {
     const int local = u - b * n_tiles;
     const int nt = local / cnt;
     const int p = b + (local - nt * cnt);
-    return Unit{piece_row[p], piece_rows[p], lo * n_per_expert + nt * bn, nt * bn};
+    const int brow = b_tiled ? (lo * n_tiles + nt) * kb * bn : lo * n_per_expert + nt * bn;
+    return Unit{piece_row[p], piece_rows[p], brow, nt * bn};
   }
   __device__ int num_kb() const { return kb; }
   __device__ int a_kcol(int k) const { return k * kBlockK; }
-  __device__ int b_kcol(int k) const { return k * kBlockK; }
+  __device__ int b_kcol(int k) const { return b_tiled ? 0 : k * kBlockK; }
+  __device__ int b_krow(int k) const { return b_tiled ? k * bn : 0; }
 };
 
 // Split-bf16 "3-pass" product for fp32-faithful dot products on the tensor
@@ -241,6 +274,7 @@ struct SegSched {
 //   acc = x_hi.w_hi + x_hi.w_lo + x_lo.w_hi
 // expressed as 3*nk k-blocks with remapped k coordinates.
 struct Split3Sched {
+  static constexpr bool kStreamB = false;
   int M, n_tiles, nk, bn, kd;  // kd = padded real K (multiple of 64)
   __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
   __device__ Unit unit(int u) const {
@@ -259,6 +293,7 @@ struct Split3Sched {
   __device__ int b_kcol(int k) const {
     return k < nk ? k * kBlockK : (k < 2 * nk ? kd + (k - nk) * kBlockK : (k - 2 * nk) * kBlockK);
   }
+  __device__ int b_krow(int) const { return 0; }
 };
 
 }  // namespace mp

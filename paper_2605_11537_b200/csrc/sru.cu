@@ -33,7 +33,7 @@ __global__ void k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, i
   const int t0 = ch * kScanChunk, t1 = min(T, t0 + kScanChunk);
   float a0 = 1.f, a1 = 1.f, b0 = 0.f, b1 = 0.f;
   const __nv_bfloat16* p = ufr + (size_t)t0 * 3 * d + 2 * cp;
-#pragma unroll 4
+#pragma unroll 8
   for (int t = t0; t < t1; ++t, p += 3 * d) {
     const float2 u = ld_bf16x2(p), f = ld_bf16x2(p + d);
     b0 = f.x * b0 + (1.f - f.x) * u.x;
@@ -46,17 +46,39 @@ __global__ void k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, i
   *reinterpret_cast<float2*>(aggB + o) = make_float2(b0, b1);
 }
 
-// pass B: carry_in[ch] per channel (c_0 = 0 at the start of every batch).
+// pass B: carry_in[ch] per channel (c_0 = 0 at the start of every batch, or the
+// carry of a preceding shard). Loads are hoisted 16 chunks at a time so the
+// serial chain only pays FMA latency, not memory latency.
 __global__ void k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
                              const float* __restrict__ c0, float* __restrict__ carry) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d) return;
   float run = c0 ? c0[c] : 0.f;
-  for (int ch = 0; ch < nch; ++ch) {
+  int ch = 0;
+  for (; ch + 16 <= nch; ch += 16) {
+    float a[16], b[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      a[i] = __ldg(&aggA[(size_t)(ch + i) * d + c]);
+      b[i] = __ldg(&aggB[(size_t)(ch + i) * d + c]);
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      carry[(size_t)(ch + i) * d + c] = run;
+      run = fmaf(a[i], run, b[i]);
+    }
+  }
+  for (; ch < nch; ++ch) {
     const size_t o = (size_t)ch * d + c;
     carry[o] = run;
-    run = aggA[o] * run + aggB[o];
+    run = fmaf(aggA[o], run, aggB[o]);
   }
+}
+
+// tanh via one exp + one reciprocal (|abs err| ~1e-7; the reference uses np.tanh in f64)
+__device__ __forceinline__ float fast_tanh(float x) {
+  const float e = __expf(2.f * x);
+  return 1.f - 2.f * __frcp_rn(1.f + e);
 }
 
 // pass C: replay each chunk from its carry; h = r tanh(c) + (1 - r) x.
@@ -72,14 +94,14 @@ __global__ void k_scan_output(const __nv_bfloat16* __restrict__ ufr, const float
   float c0 = cin.x, c1 = cin.y;
   bool bad = false;
   const __nv_bfloat16* p = ufr + (size_t)t0 * 3 * d + 2 * cp;
-#pragma unroll 4
+#pragma unroll 8
   for (int t = t0; t < t1; ++t, p += 3 * d) {
     const float2 u = ld_bf16x2(p), f = ld_bf16x2(p + d), r = ld_bf16x2(p + 2 * d);
     const float2 xv = *reinterpret_cast<const float2*>(x + (size_t)t * d + 2 * cp);
     c0 = f.x * c0 + (1.f - f.x) * u.x;
     c1 = f.y * c1 + (1.f - f.y) * u.y;
-    const float h0 = r.x * tanhf(c0) + (1.f - r.x) * xv.x;
-    const float h1 = r.y * tanhf(c1) + (1.f - r.y) * xv.y;
+    const float h0 = r.x * fast_tanh(c0) + (1.f - r.x) * xv.x;
+    const float h1 = r.y * fast_tanh(c1) + (1.f - r.y) * xv.y;
     bad |= !(isfinite(h0) && isfinite(h1) && isfinite(c0) && isfinite(c1));
     *reinterpret_cast<float2*>(h32 + (size_t)t * d + 2 * cp) = make_float2(h0, h1);
     *reinterpret_cast<__nv_bfloat162*>(h16 + (size_t)t * d + 2 * cp) = __floats2bfloat162_rn(h0, h1);

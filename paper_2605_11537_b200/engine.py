@@ -248,11 +248,11 @@ class MoEPipeline:
         _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[0].record()
-        _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
+        _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), lay.tiled, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[1].record()
-        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
+        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), lay.tiled, ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
                   ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[2].record()
@@ -297,8 +297,13 @@ def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor) -
     lay.w32 = w32
     lay.w_abs = torch.empty(d, device=router.device)
     _lib.call("mp_router_weight_absmax", ptr(w32), E, d, ptr(lay.w_abs), stream_ptr())
-    lay.U = u.reshape(E * F, d).contiguous()
-    lay.V = v.reshape(E * d, F).contiguous()
+    # pre-tiled B operands: each TMA box of the grouped GEMMs is one contiguous 32 KB burst
+    u2, v2 = u.reshape(E * F, d).contiguous(), v.reshape(E * d, F).contiguous()
+    lay.U, lay.V = torch.empty_like(u2), torch.empty_like(v2)
+    _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, 256, stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, _lib.size_query("mp_ffn_down_bn", d), stream_ptr())
+    lay.tiled = 1
+    del u2, v2
     return lay
 
 

@@ -133,6 +133,7 @@ class DeviceMoeLayer:
         V[:, :d, :F] = v.to(torch.bfloat16)
         self.U = U.view(E * Fp, dp)
         self.V = V.view(E * dp, Fp)
+        self.tiled = 0
 
 
 class DeviceMoe:

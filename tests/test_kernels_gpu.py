@@ -190,3 +190,37 @@ def test_exec_map_and_ffn(dev):
             hid = (xb[m] @ Ub[e].float().T).relu().bfloat16().float()
             ref[m] += hid @ Vb[e].float().T
         assert _rel(x - x0, ref - x0) < 1e-3
+
+
+def test_tiled_weight_layout_is_bitwise_identical(dev):
+    """Pre-tiled B operands (mp_tile_kmajor) give the same bits as the reference layout."""
+    rng = np.random.default_rng(11)
+    T, E, d, F = 900, 6, 256, 512
+    route = torch.from_numpy(rng.integers(0, E, size=T).astype(np.int32)).to(dev)
+    slot_expert = torch.arange(E, dtype=torch.int32, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    tor = torch.empty(T, **i32)
+    pn = E + (T + 127) // 128
+    prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
+    nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
+    sws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    _lib.call("mp_segments_from_slots", ptr(route), ptr(slot_expert), T, E, E, 1, ptr(tor), ptr(prow), ptr(prows),
+              ptr(eb), ptr(sws), nb, stream_ptr())
+    U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
+    V = (torch.randn(E * d, F, device=dev) / 16).bfloat16()
+    Ut, Vt = torch.empty_like(U), torch.empty_like(V)
+    _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, _lib.size_query("mp_ffn_down_bn", d), stream_ptr())
+    x = torch.randn(T, d, device=dev)
+    fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+    ws = torch.empty(fb, dtype=torch.uint8, device=dev)
+    y_ref = x.clone()
+    _lib.call("mp_moe_ffn", ptr(x), ptr(y_ref), T, d, F, E, ptr(U), ptr(V), ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+              ptr(ws), fb, stream_ptr())
+    y = x.clone()
+    _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
+    _lib.call("mp_ffn_up", T, d, F, E, ptr(Ut), 1, ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb, stream_ptr())
+    _lib.call("mp_ffn_down", ptr(y), T, d, F, E, ptr(Vt), 1, ptr(tor), ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb,
+              stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(y, y_ref)

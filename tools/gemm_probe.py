@@ -1,0 +1,66 @@
+"""GEMM micro-probe: libmoempmc dense tcgen05 GEMM vs cuBLAS on the hot-path shapes."""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2605_11537_b200 import _lib  # noqa: E402
+from paper_2605_11537_b200._dev import ptr, require_device, stream_ptr  # noqa: E402
+
+
+def timeit(fn, iters=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3  # us
+
+
+def main():
+    dev = require_device()
+    for (M, N, K) in [(16384, 2304, 768), (16384, 3072, 768), (16384, 768, 3072), (16384, 1536, 768)]:
+        A = torch.randn(M, K, device=dev).bfloat16()
+        B = torch.randn(N, K, device=dev).bfloat16()
+        C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        bias = torch.randn(N, device=dev)
+        fl = 2 * M * N * K
+        res = {}
+        res["ours_plain"] = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, N, None, 0, 0,
+                                                     stream_ptr()))
+        res["ours_bias_sig"] = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, N, ptr(bias),
+                                                        2, K, stream_ptr()))
+        res["ours_nostore"] = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, 0, None, 0, 0,
+                                                       stream_ptr()))
+        res["cublas"] = timeit(lambda: torch.matmul(A, B.T, out=C))
+        print(f"M={M} N={N} K={K}: " + "  ".join(f"{k}={v:.1f}us ({fl / v / 1e6:.0f} TF)" for k, v in res.items()))
+
+
+if __name__ == "__main__":
+    main()
+
+
+def stream_probe():
+    """Pure weight streaming: one 128-row M tile against every expert's weights (B >> L2)."""
+    dev = require_device()
+    for (N, K) in [(128 * 3072, 768), (128 * 768, 3072)]:
+        A = torch.randn(128, K, device=dev).bfloat16()
+        B = (torch.randn(N, K, device=dev) / 8).bfloat16()
+        C = torch.empty(128, N, device=dev, dtype=torch.bfloat16)
+        us = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), 128, N, K, 0, N, None, 0, 0,
+                                      stream_ptr()), iters=10)
+        us0 = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), 128, N, K, 0, 0, None, 0, 0,
+                                       stream_ptr()), iters=10)
+        X = torch.empty_like(B)
+        usc = timeit(lambda: X.copy_(B), iters=10)
+        print(f"stream N={N} K={K}: gemm {us:.1f}us = {B.numel() * 2 / us / 1e3:.0f} GB/s of B; nostore {us0:.1f}us "
+              f"= {B.numel() * 2 / us0 / 1e3:.0f} GB/s; torch copy {usc:.1f}us = {2 * B.numel() * 2 / usc / 1e3:.0f} GB/s r+w")
+
+
+if __name__ == "__main__" and "--stream" in sys.argv:
+    stream_probe()
