@@ -63,6 +63,35 @@ __device__ __forceinline__ void apply_act(float* v, const float* svec, int act, 
   }
 }
 
+// Coalesced bf16 store of one 32-column chunk of the warp's 32 rows: lane = row
+// writes its 64 B to warp-private smem (row stride 80 B: conflict-free 16 B
+// stores), then each store instruction writes 8 rows x 64 B contiguous
+// segments. row_ptr(i) gives the destination of tile row i of this warp (or
+// null for rows outside the unit).
+template <class RowPtr>
+__device__ __forceinline__ void store_chunk_bf16(const float* v, uint32_t* scratch, RowPtr&& row_ptr) {
+  const int lane = threadIdx.x & 31;
+  uint4* srow = reinterpret_cast<uint4*>(scratch + lane * 20);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 w;
+    w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+    w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+    w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+    w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+    srow[q] = w;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int row = it * 8 + (lane >> 2), part = lane & 3;
+    const uint4 w = *reinterpret_cast<const uint4*>(scratch + row * 20 + part * 4);
+    __nv_bfloat16* dst = row_ptr(row);
+    if (dst) reinterpret_cast<uint4*>(dst)[part] = w;
+  }
+  __syncwarp();
+}
+
 // out[row, n0 + c] = act(acc + bias) -> bf16 (act: 0 none, 1 relu, 2 sigmoid for cols >= sig_from)
 struct EpiStoreBf16 {
   static constexpr bool kSplitCols = true;
@@ -73,24 +102,17 @@ struct EpiStoreBf16 {
   int sig_from;
   __device__ __forceinline__ const float* colvec() const { return bias; }
   template <int NC>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec) const {
-    const int rr = mt * kBlockM + r;
-    const bool ok = rr < U.rows;
-    __nv_bfloat16* dst = out + (size_t)(U.a_row + rr) * ldo + U.n0 + c0;
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec,
+                                      uint32_t* scratch) const {
+    const int row0 = mt * kBlockM + (r & ~31);  // first unit row of this warp
+    __nv_bfloat16* base = out + (size_t)(U.a_row + row0) * ldo + U.n0 + c0;
+    const int nvalid = U.rows - row0;
     tmem_chunks<NC>(taddr, [&](int c, float* v) {
       apply_act(v, bias ? svec + c : nullptr, act, U.n0 + c0 + c >= sig_from);
-      if (ok && ldo) {  // ldo == 0: diagnostic mode, no stores
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 w;
-          w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-          w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-          w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-          w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-          d4[q] = w;
-        }
-      }
+      if (ldo)  // ldo == 0: diagnostic mode, no stores
+        store_chunk_bf16(v, scratch, [&](int i) -> __nv_bfloat16* {
+          return i < nvalid ? base + (size_t)i * ldo + c : nullptr;
+        });
     });
   }
 };
@@ -105,7 +127,8 @@ struct EpiStoreF32 {
   int sig_from;
   __device__ __forceinline__ const float* colvec() const { return bias; }
   template <int NC>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec) const {
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec,
+                                      uint32_t*) const {
     const int rr = mt * kBlockM + r;
     const bool ok = rr < U.rows;
     float* dst = out + (size_t)(U.a_row + rr) * ldo + U.n0 + c0;
@@ -130,24 +153,38 @@ struct EpiScatterAdd {
   const int32_t* tok_of_row;
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
   template <int NC>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float*) const {
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float*,
+                                      uint32_t* scratch) const {
+    const int lane = threadIdx.x & 31;
     const int rr = mt * kBlockM + r;
     const bool ok = rr < U.rows;
-    const int tok = ok ? __ldg(&tok_of_row[U.a_row + rr]) : 0;
-    float4* dst = reinterpret_cast<float4*>(x + (size_t)tok * ldx + U.n0 + c0);
+    const int tok = ok ? __ldg(&tok_of_row[U.a_row + rr]) : -1;
+    float* base = x + U.n0 + c0;
+    float4* srow = reinterpret_cast<float4*>(scratch + lane * 20);
     tmem_chunks<NC>(taddr, [&](int c, float* v) {
-      if (ok) {
-        float4 o[8];
+      // two 16-column halves: lane = row -> smem, then 8 rows x 64 B per instruction
 #pragma unroll
-        for (int q = 0; q < 8; ++q) o[q] = dst[c / 4 + q];
+      for (int h = 0; h < 2; ++h) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          o[q].x += v[4 * q + 0];
-          o[q].y += v[4 * q + 1];
-          o[q].z += v[4 * q + 2];
-          o[q].w += v[4 * q + 3];
-          dst[c / 4 + q] = o[q];
+        for (int q = 0; q < 4; ++q)
+          srow[q] = make_float4(v[16 * h + 4 * q], v[16 * h + 4 * q + 1], v[16 * h + 4 * q + 2], v[16 * h + 4 * q + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int row = it * 8 + (lane >> 2), part = lane & 3;
+          const int t = __shfl_sync(0xffffffffu, tok, row);
+          const float4 a = *reinterpret_cast<const float4*>(scratch + row * 20 + part * 4);
+          if (t >= 0) {
+            float4* dst = reinterpret_cast<float4*>(base + (size_t)t * ldx + c + 16 * h) + part;
+            float4 o = *dst;
+            o.x += a.x;
+            o.y += a.y;
+            o.z += a.z;
+            o.w += a.w;
+            *dst = o;
+          }
         }
+        __syncwarp();
       }
     });
   }
@@ -165,7 +202,8 @@ struct EpiGroupArgmax {
   int ngroups;
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
   template <int BN>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int, const float*) const {
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int, const float*,
+                                      uint32_t*) const {
     const int rr = mt * kBlockM + r;
     const bool ok = rr < U.rows;
     float best = -INFINITY;
@@ -206,7 +244,8 @@ struct EpiRouterTop1 {
   int32_t* recheck_list;
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
   template <int BN>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int, const float*) const {
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int, const float*,
+                                      uint32_t*) const {
     const int rr = mt * kBlockM + r;
     const bool ok = rr < U.rows;
     float b1 = -INFINITY, b2 = -INFINITY;

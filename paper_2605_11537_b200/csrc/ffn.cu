@@ -13,6 +13,7 @@
 #include "launch.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 extern "C" int mp_ffn_down_bn(int dp);
 
@@ -87,7 +88,8 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
   rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled);
   if (rc) return rc;
   SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
-  EpiStoreBf16 e{hid, Fp, nullptr, 1, 0};
+  static const bool diag_nostore = getenv("MP_DIAG_NOSTORE") != nullptr;  // profiling switch only
+  EpiStoreBf16 e{hid, diag_nostore ? 0 : Fp, nullptr, 1, 0};
   return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
 }
 

@@ -42,7 +42,9 @@ struct GemmSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
   static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
-  static constexpr int kBytes = kVecOffset + 2 * BN * 4 + 1024;  // + column-vector staging, alignment slack
+  static constexpr int kScratchOffset = kVecOffset + 2 * BN * 4;
+  static constexpr int kScratchWordsPerWarp = 32 * 20;  // 32 rows x (16 + 4 pad) words: store transpose
+  static constexpr int kBytes = kScratchOffset + 8 * kScratchWordsPerWarp * 4 + 1024;  // + alignment slack
 };
 
 // Scheduler concept:
@@ -51,7 +53,8 @@ struct GemmSmem {
 // Epilogue concept:
 //   static constexpr bool kSplitCols;   // columns independent -> two warpgroups split them
 //   const float* colvec() const;        // per-column vector (bias) or null; staged in smem per tile
-//   template<int NC> void run(const Unit&, int mt, int r, uint32_t taddr, int c0, const float* svec) const
+//   template<int NC> void run(const Unit&, int mt, int r, uint32_t taddr, int c0, const float* svec,
+//                             uint32_t* scratch) const   (scratch: warp-private smem, 640 words)
 //   (r = row inside the 128-row tile owned by this thread; taddr = TMEM address of
 //    (lane quadrant, accumulator stage, column c0); the thread handles tile columns
 //    [c0, c0 + NC)).
@@ -70,6 +73,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* svec = reinterpret_cast<float*>(smem + L::kVecOffset);  // [2][BN]
+  uint32_t* scratch_all = reinterpret_cast<uint32_t*>(smem + L::kScratchOffset);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -182,7 +186,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         if (active) {
           const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c0;
-          epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0);
+          epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
+                               scratch_all + (warp - 4) * L::kScratchWordsPerWarp);
         }
         tc_fence_before();
         __syncwarp();

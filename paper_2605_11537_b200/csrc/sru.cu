@@ -16,7 +16,7 @@
 
 namespace mp {
 
-constexpr int kScanChunk = 64;   // tokens per scan chunk
+constexpr int kScanChunk = 32;   // tokens per scan chunk
 constexpr int kScanThreads = 128;  // channel pairs per block
 
 __device__ __forceinline__ float2 ld_bf16x2(const __nv_bfloat16* p) {
@@ -24,54 +24,87 @@ __device__ __forceinline__ float2 ld_bf16x2(const __nv_bfloat16* p) {
   return __bfloat1622float2(v);
 }
 
-// pass A: grid (cdiv(d/2, 128), nch). ufr row = [u | f | r], 3d bf16.
-__global__ void k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, int d, float* __restrict__ aggA,
-                                 float* __restrict__ aggB) {
-  const int cp = blockIdx.x * kScanThreads + threadIdx.x;  // channel pair
-  if (2 * cp >= d) return;
+// pass A: chunk aggregates (A = prod f, B = chunk scan from c = 0) per channel,
+// 4 channels per thread, u/f loads software-pipelined 8 tokens deep.
+struct bf16x4 {
+  __nv_bfloat162 a, b;
+};
+__global__ void __launch_bounds__(64) k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, int d,
+                                                       float* __restrict__ aggA, float* __restrict__ aggB) {
+  const int cq = blockIdx.x * blockDim.x + threadIdx.x;
+  if (4 * cq >= d) return;
   const int ch = blockIdx.y;
   const int t0 = ch * kScanChunk, t1 = min(T, t0 + kScanChunk);
-  float a0 = 1.f, a1 = 1.f, b0 = 0.f, b1 = 0.f;
-  const __nv_bfloat16* p = ufr + (size_t)t0 * 3 * d + 2 * cp;
-#pragma unroll 8
-  for (int t = t0; t < t1; ++t, p += 3 * d) {
-    const float2 u = ld_bf16x2(p), f = ld_bf16x2(p + d);
-    b0 = f.x * b0 + (1.f - f.x) * u.x;
-    b1 = f.y * b1 + (1.f - f.y) * u.y;
-    a0 *= f.x;
-    a1 *= f.y;
+  float a[4] = {1.f, 1.f, 1.f, 1.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+  const size_t ld3 = (size_t)3 * d;
+#pragma unroll 1
+  for (int tb = t0; tb < t1; tb += 8) {
+    bf16x4 u[8], f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int t = min(tb + i, t1 - 1);
+      const __nv_bfloat16* p = ufr + (size_t)t * ld3 + 4 * cq;
+      u[i] = *reinterpret_cast<const bf16x4*>(p);
+      f[i] = *reinterpret_cast<const bf16x4*>(p + d);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (tb + i < t1) {
+        const float2 ua = __bfloat1622float2(u[i].a), ub = __bfloat1622float2(u[i].b);
+        const float2 fa = __bfloat1622float2(f[i].a), fb = __bfloat1622float2(f[i].b);
+        const float uu[4] = {ua.x, ua.y, ub.x, ub.y}, ff[4] = {fa.x, fa.y, fb.x, fb.y};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          b[j] = fmaf(ff[j], b[j] - uu[j], uu[j]);
+          a[j] *= ff[j];
+        }
+      }
+    }
   }
-  const size_t o = (size_t)ch * d + 2 * cp;
-  *reinterpret_cast<float2*>(aggA + o) = make_float2(a0, a1);
-  *reinterpret_cast<float2*>(aggB + o) = make_float2(b0, b1);
+  const size_t o = (size_t)ch * d + 4 * cq;
+  *reinterpret_cast<float4*>(aggA + o) = make_float4(a[0], a[1], a[2], a[3]);
+  *reinterpret_cast<float4*>(aggB + o) = make_float4(b[0], b[1], b[2], b[3]);
 }
 
 // pass B: carry_in[ch] per channel (c_0 = 0 at the start of every batch, or the
-// carry of a preceding shard). Loads are hoisted 16 chunks at a time so the
-// serial chain only pays FMA latency, not memory latency.
+// carry of a preceding shard). Hierarchical so the serial depth is
+// 3 * sqrt(nch) instead of nch: block = 32 channels x G chunk groups; each
+// (group, channel) composes its chunks' affine maps, one thread per channel
+// scans the G group maps, then every group replays its chunks from its carry.
+constexpr int kCarryGroups = 16;
 __global__ void k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
                              const float* __restrict__ c0, float* __restrict__ carry) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
-  float run = c0 ? c0[c] : 0.f;
-  int ch = 0;
-  for (; ch + 16 <= nch; ch += 16) {
-    float a[16], b[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      a[i] = __ldg(&aggA[(size_t)(ch + i) * d + c]);
-      b[i] = __ldg(&aggB[(size_t)(ch + i) * d + c]);
+  __shared__ float sA[kCarryGroups][32], sB[kCarryGroups][32], sC[kCarryGroups][32];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  const int per = cdiv(nch, kCarryGroups);
+  const int ch0 = g * per, ch1 = min(nch, ch0 + per);
+  float A = 1.f, B = 0.f;
+  if (c < d)
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const size_t o = (size_t)ch * d + c;
+      const float a = __ldg(&aggA[o]), b = __ldg(&aggB[o]);
+      B = fmaf(a, B, b);  // compose: apply (A,B) first, then (a,b)
+      A *= a;
     }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      carry[(size_t)(ch + i) * d + c] = run;
-      run = fmaf(a[i], run, b[i]);
+  sA[g][cl] = A;
+  sB[g][cl] = B;
+  __syncthreads();
+  if (g == 0) {
+    float run = (c < d && c0) ? c0[c] : 0.f;
+    for (int h = 0; h < kCarryGroups; ++h) {
+      sC[h][cl] = run;
+      run = fmaf(sA[h][cl], run, sB[h][cl]);
     }
   }
-  for (; ch < nch; ++ch) {
-    const size_t o = (size_t)ch * d + c;
-    carry[o] = run;
-    run = fmaf(aggA[o], run, aggB[o]);
+  __syncthreads();
+  if (c < d) {
+    float run = sC[g][cl];
+    for (int ch = ch0; ch < ch1; ++ch) {
+      const size_t o = (size_t)ch * d + c;
+      carry[o] = run;
+      run = fmaf(__ldg(&aggA[o]), run, __ldg(&aggB[o]));
+    }
   }
 }
 
@@ -82,31 +115,79 @@ __device__ __forceinline__ float fast_tanh(float x) {
 }
 
 // pass C: replay each chunk from its carry; h = r tanh(c) + (1 - r) x.
-__global__ void k_scan_output(const __nv_bfloat16* __restrict__ ufr, const float* __restrict__ x, int T, int d,
-                              const float* __restrict__ carry, float* __restrict__ h32,
-                              __nv_bfloat16* __restrict__ h16, float* __restrict__ c_last,
-                              int32_t* __restrict__ nonfinite) {
-  const int cp = blockIdx.x * kScanThreads + threadIdx.x;
-  if (2 * cp >= d) return;
+// 4 channels per thread: 8-byte bf16x4 loads of u/f/r, 16-byte x loads/h stores.
+__device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
+  const bf16x4 v = *reinterpret_cast<const bf16x4*>(p);
+  const float2 lo = __bfloat1622float2(v.a), hi = __bfloat1622float2(v.b);
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
+}
+
+__device__ __forceinline__ float sru_step(float& c, float u, float f, float r, float x) {
+  c = fmaf(f, c - u, u);  // f c + (1 - f) u
+  return fmaf(r, fast_tanh(c) - x, x);  // r tanh(c) + (1 - r) x
+}
+
+// Loads are software-pipelined kPF tokens deep (raw bf16x4 / float4 kept in
+// registers) so each thread keeps ~kPF * 40 B in flight across the serial chain.
+constexpr int kPF = 4;
+__global__ void __launch_bounds__(64) k_scan_output(const __nv_bfloat16* __restrict__ ufr,
+                                                    const float* __restrict__ x, int T, int d,
+                                                    const float* __restrict__ carry, float* __restrict__ h32,
+                                                    __nv_bfloat16* __restrict__ h16, float* __restrict__ c_last,
+                                                    int32_t* __restrict__ nonfinite) {
+  const int cq = blockIdx.x * blockDim.x + threadIdx.x;  // channel quad
+  if (4 * cq >= d) return;
   const int ch = blockIdx.y;
   const int t0 = ch * kScanChunk, t1 = min(T, t0 + kScanChunk);
-  const float2 cin = *reinterpret_cast<const float2*>(carry + (size_t)ch * d + 2 * cp);
-  float c0 = cin.x, c1 = cin.y;
+  const float4 cin = *reinterpret_cast<const float4*>(carry + (size_t)ch * d + 4 * cq);
+  float c0 = cin.x, c1 = cin.y, c2 = cin.z, c3 = cin.w;
   bool bad = false;
-  const __nv_bfloat16* p = ufr + (size_t)t0 * 3 * d + 2 * cp;
-#pragma unroll 8
-  for (int t = t0; t < t1; ++t, p += 3 * d) {
-    const float2 u = ld_bf16x2(p), f = ld_bf16x2(p + d), r = ld_bf16x2(p + 2 * d);
-    const float2 xv = *reinterpret_cast<const float2*>(x + (size_t)t * d + 2 * cp);
-    c0 = f.x * c0 + (1.f - f.x) * u.x;
-    c1 = f.y * c1 + (1.f - f.y) * u.y;
-    const float h0 = r.x * fast_tanh(c0) + (1.f - r.x) * xv.x;
-    const float h1 = r.y * fast_tanh(c1) + (1.f - r.y) * xv.y;
-    bad |= !(isfinite(h0) && isfinite(h1) && isfinite(c0) && isfinite(c1));
-    *reinterpret_cast<float2*>(h32 + (size_t)t * d + 2 * cp) = make_float2(h0, h1);
-    *reinterpret_cast<__nv_bfloat162*>(h16 + (size_t)t * d + 2 * cp) = __floats2bfloat162_rn(h0, h1);
+  const size_t ld3 = (size_t)3 * d;
+  bf16x4 bu[2][kPF], bfv[2][kPF], br[2][kPF];
+  float4 bx[2][kPF];
+  auto fetch = [&](int buf, int tb) {
+#pragma unroll
+    for (int i = 0; i < kPF; ++i) {
+      const int t = min(tb + i, t1 - 1);
+      const __nv_bfloat16* p = ufr + (size_t)t * ld3 + 4 * cq;
+      bu[buf][i] = *reinterpret_cast<const bf16x4*>(p);
+      bfv[buf][i] = *reinterpret_cast<const bf16x4*>(p + d);
+      br[buf][i] = *reinterpret_cast<const bf16x4*>(p + 2 * d);
+      bx[buf][i] = *reinterpret_cast<const float4*>(x + (size_t)t * d + 4 * cq);
+    }
+  };
+  fetch(0, t0);
+#pragma unroll 1
+  for (int tb = t0; tb < t1; tb += 2 * kPF) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int tc = tb + half * kPF;
+      if (tc >= t1) break;
+      if (tc + kPF < t1) fetch(half ^ 1, tc + kPF);
+#pragma unroll
+      for (int i = 0; i < kPF; ++i) {
+        const int t = tc + i;
+        if (t < t1) {
+          const float2 ua = __bfloat1622float2(bu[half][i].a), ub = __bfloat1622float2(bu[half][i].b);
+          const float2 fa = __bfloat1622float2(bfv[half][i].a), fb = __bfloat1622float2(bfv[half][i].b);
+          const float2 ra = __bfloat1622float2(br[half][i].a), rb = __bfloat1622float2(br[half][i].b);
+          const float4 xv = bx[half][i];
+          float4 h;
+          h.x = sru_step(c0, ua.x, fa.x, ra.x, xv.x);
+          h.y = sru_step(c1, ua.y, fa.y, ra.y, xv.y);
+          h.z = sru_step(c2, ub.x, fb.x, rb.x, xv.z);
+          h.w = sru_step(c3, ub.y, fb.y, rb.y, xv.w);
+          bad |= !(isfinite(h.x) && isfinite(h.y) && isfinite(h.z) && isfinite(h.w) && isfinite(c0 + c1 + c2 + c3));
+          *reinterpret_cast<float4*>(h32 + (size_t)t * d + 4 * cq) = h;
+          bf16x4 hb;
+          hb.a = __floats2bfloat162_rn(h.x, h.y);
+          hb.b = __floats2bfloat162_rn(h.z, h.w);
+          *reinterpret_cast<bf16x4*>(h16 + (size_t)t * d + 4 * cq) = hb;
+        }
+      }
+    }
   }
-  if (c_last && t1 == T) *reinterpret_cast<float2*>(c_last + 2 * cp) = make_float2(c0, c1);
+  if (c_last && t1 == T) *reinterpret_cast<float4*>(c_last + 4 * cq) = make_float4(c0, c1, c2, c3);
   if (bad) atomicOr(nonfinite, 1);  // reference raises NumericError (src/predictor.py:170-171)
 }
 
@@ -178,11 +259,10 @@ extern "C" int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* 
   int rc = mp_gemm_bf16(x_bf16, w_cat, ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, stream);
   if (rc) return rc;
   // K2
-  const dim3 g(cdiv(d / 2, kScanThreads), nch);
-  k_scan_aggregate<<<g, kScanThreads, 0, st>>>(ufr, T, d, aggA, aggB);
-  k_scan_carry<<<cdiv(d, 128), 128, 0, st>>>(aggA, aggB, nch, d, c0, carry);
-  k_scan_output<<<g, kScanThreads, 0, st>>>(ufr, x_f32, T, d, carry, h_f32, (__nv_bfloat16*)h_bf16, c_last,
-                                            nonfinite);
+  const dim3 gq(cdiv(d / 4, 64), nch);
+  k_scan_aggregate<<<gq, 64, 0, st>>>(ufr, T, d, aggA, aggB);
+  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(aggA, aggB, nch, d, c0, carry);
+  k_scan_output<<<gq, 64, 0, st>>>(ufr, x_f32, T, d, carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
