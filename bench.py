@@ -34,7 +34,7 @@ METRIC = "Switch-base-128 MoE tokens/s at 1/2/4/8 B200; grouped-GEMM tensor-pipe
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--replication", choices=["on", "off", "split"], default="on")
@@ -49,6 +49,8 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
+    p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
     return p.parse_args()
 
 
@@ -219,12 +221,27 @@ def run_ours(args):
         x.copy_(emb)
         return pipe.step(x, events)
 
+    if args.l2_persist > 0:
+        from paper_2605_11537_b200 import _lib as mplib
+        from paper_2605_11537_b200._dev import stream_ptr
+
+        mplib.call("mp_l2_persist", x.data_ptr(), x.numel() * 4, float(args.l2_persist), stream_ptr())
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
+
+    from paper_2605_11537_b200.engine import DeviceEvent
+
+    ev = [[DeviceEvent() for _ in range(3)] for _ in range(L)]
+    graph = None
+    if not args.no_graph:
+        graph = pipe.capture(x, ev)  # one CUDA graph per step, GEMM timing events inside it
+        for k in range(2):
+            x.copy_(batches[k % len(batches)][0])
+            graph.replay()
+        torch.cuda.synchronize()
     barrier(world)
 
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(L)] for _ in range(args.steps)]
     clocks = ClockSampler(torch.cuda.current_device() if world == 1 else local)
     clocks.start()
     time.sleep(0.3)
@@ -233,21 +250,28 @@ def run_ours(args):
     barrier(world)
     start.record()
     launches = 0
+    up, down = [], []
     for k in range(args.steps):
-        launches += step(k, ev[k]) + 1  # + the input staging copy
+        if graph is not None:
+            x.copy_(batches[k % len(batches)][0])
+            graph.replay()
+            launches += graph.launches + 1
+        else:
+            launches += step(k, ev) + 1  # + the input staging copy
     end.record()
     torch.cuda.synchronize()
     elapsed_ms = start.elapsed_time(end)
     clk = clocks.stop()
     elapsed_ms = max_over_ranks(elapsed_ms, world)
+    # GEMM launch durations of the last timed step (events recorded inside the step / graph)
+    up = [ev[l][0].elapsed_ms(ev[l][1]) for l in range(L)]
+    down = [ev[l][1].elapsed_ms(ev[l][2]) for l in range(L)]
 
     # correctness spot checks on the last step (not timed)
     last = batches[(args.steps - 1) % len(batches)]
     routing_exact = bool((pipe.route.long() == last[2]).all().item())
     pred_acc = float((pipe.assign.long() == last[2]).float().mean().item())
 
-    up = [ev[k][l][0].elapsed_time(ev[k][l][1]) for k in range(args.steps) for l in range(L)]
-    down = [ev[k][l][1].elapsed_time(ev[k][l][2]) for k in range(args.steps) for l in range(L)]
     t_up, t_down = sum(up) / len(up), sum(down) / len(down)
     touched = pipe.touched_experts().float().mean().item()
     w_bytes = touched * pipe.expert_weight_bytes()
@@ -299,6 +323,7 @@ def run_ours(args):
             "tensor_frac": flops / ((t_up + t_down) * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"],
         },
         "checks": {"routing_exact_last_step": routing_exact, "predictor_accuracy_last_step": pred_acc},
+        "cuda_graph": graph is not None,
     }
 
     if not args.no_e2e:
@@ -331,6 +356,8 @@ def run_e2e(args, pipe, batches, world):
     comp_done = [torch.cuda.Event() for _ in range(2)]
     d2h_done = [torch.cuda.Event() for _ in range(2)]
 
+    graphs = [pipe.capture(dev[j]) for j in range(2)] if not args.no_graph else None
+
     def run(n, timed):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if timed:
@@ -343,7 +370,10 @@ def run_e2e(args, pipe, batches, world):
                 dev[j].copy_(host_in[k % len(host_in)], non_blocking=True)
                 h2d_done[j].record(h2d)
             comp.wait_event(h2d_done[j])
-            pipe.step(dev[j])
+            if graphs is not None:
+                graphs[j].replay()
+            else:
+                pipe.step(dev[j])
             comp_done[j].record(comp)
             d2h.wait_event(comp_done[j])
             with torch.cuda.stream(d2h):
@@ -367,7 +397,12 @@ def main():
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    import torch
+
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    with torch.cuda.stream(torch.cuda.Stream()):  # capturable (non-legacy) compute stream
+        return run_ours(args)
 
 
 if __name__ == "__main__":

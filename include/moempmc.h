@@ -94,7 +94,8 @@ MP_API int mp_place(const int32_t* assign, int L, int T, int E, const int32_t* c
  * res). Also emits the replica-segment permutation consumed by the grouped
  * GEMM: rows are grouped by slot (expert-major, replica-minor), a slot's rows
  * in token order; pieces are the GEMM work units (one per slot, or per 128-row
- * M-tile of a slot when split_m != 0).
+ * M-tile of a slot when split_m bit 0 is set). split_m bit 1: pad every expert to an
+ * even piece count (empty pieces have 0 rows) for the CTA-pair grouped GEMM.
  *   max_slots  >= max over layers of resident slots + corrective loads
  *   per layer l (strides): token_to_slot/row_of_token/tok_of_row: T;
  *   piece_row/piece_rows: max_slots + ceil(T/128); exp_begin: E + 1.
@@ -186,14 +187,15 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
                       const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                       const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 /* The same layer as three launches (gather | GEMM1 | GEMM2) sharing `ws`, for callers that
- * time or overlap the grouped GEMMs separately. tiled != 0: u / v are in the pre-tiled layout
- * of mp_tile_kmajor (BN 256 for u, mp_ffn_down_bn(dp) for v), so every weight TMA box is one
- * contiguous HBM burst instead of BN strided 128-byte rows. */
+ * time or overlap the grouped GEMMs separately. flags bit 0: u / v are in the pre-tiled
+ * layout of mp_tile_kmajor (BN 256 for u, mp_ffn_down_bn(dp) for v); bit 1: CTA-pair
+ * (tcgen05 cta_group::2, M = 256) kernels over piece pairs -- pieces must come from a
+ * builder called with split_m bit 1 (even piece count per expert), dp % 256 == 0. */
 MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                          size_t ws_bytes, void* stream);
-MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int tiled, const int32_t* piece_row,
+MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int flags, const int32_t* piece_row,
                      const int32_t* piece_rows, const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
-MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, int tiled, const int32_t* tok_of_row,
+MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, int flags, const int32_t* tok_of_row,
                        const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
                        size_t ws_bytes, void* stream);
 MP_API int mp_ffn_down_bn(int dp);
@@ -205,6 +207,21 @@ MP_API int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int B
  * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):
  * dst <- src, `bytes` long, device-to-device (or peer) on `stream`. */
 MP_API int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+/* Whole-step CUDA graphs (capture on `stream`, replay) and timing events that remain
+ * valid inside a captured graph (recorded as external event nodes). Host plumbing. */
+MP_API int mp_graph_begin(void* stream);
+MP_API int mp_graph_end(void* stream, void** graph_exec);
+MP_API int mp_graph_launch(void* graph_exec, void* stream);
+MP_API int mp_graph_destroy(void* graph_exec);
+MP_API int mp_event_create(void** ev);
+MP_API int mp_event_record(void* ev, void* stream);
+MP_API int mp_event_elapsed_ms(void* a, void* b, float* ms); /* host out-param */
+MP_API int mp_event_destroy(void* ev);
+
+/* L2 residency hint: persisting access-policy window over [ptr, ptr + bytes) for kernels
+ * launched on `stream` (bytes = 0 clears). Host plumbing. */
+MP_API int mp_l2_persist(void* ptr, size_t bytes, float hit_ratio, void* stream);
 
 /* Operand staging: y[i] = bf16(x[i]) (round to nearest even), n % 4 == 0. */
 MP_API int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream);

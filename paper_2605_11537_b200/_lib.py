@@ -65,6 +65,15 @@ SIGNATURES: dict[str, tuple] = {
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
     "mp_f32_to_bf16": (_I, [_P, _P, _Z, _P]),
+    "mp_l2_persist": (_I, [_P, _Z, _F, _P]),
+    "mp_graph_begin": (_I, [_P]),
+    "mp_graph_end": (_I, [_P, _P]),
+    "mp_graph_launch": (_I, [_P, _P]),
+    "mp_graph_destroy": (_I, [_P]),
+    "mp_event_create": (_I, [_P]),
+    "mp_event_record": (_I, [_P, _P]),
+    "mp_event_elapsed_ms": (_I, [_P, _P, _P]),
+    "mp_event_destroy": (_I, [_P]),
 }
 
 _ERRORS = {

@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "epilogues.cuh"
@@ -95,6 +96,16 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
   DenseSched s{M, N / bn, K / 64, bn};
   const int units = cdiv(M, kBlockM) * (N / bn);
   const int grid = units < num_sms() ? units : num_sms();
+  static const bool pair = getenv("MP_GEMM_PAIR") != nullptr;  // experiment switch: CTA-pair kernel
+  if (pair && bn == 256 && c_dtype == 0 && M >= 256) {
+    CUtensorMap tb2;
+    rc = make_tmap_bf16(&tb2, B, N, K, K, bn / 2);
+    if (rc) return rc;
+    Dense2Sched s2{M, N / bn, K / 64, bn};
+    EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
+    const int cu = cdiv(M, 2 * kBlockM) * (N / bn);
+    return launch_gemm2<256, 6>(ta, tb2, s2, e, std::min(2 * cu, num_sms()), st);
+  }
   if (c_dtype == 0) {
     EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
     if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, grid, st);
@@ -129,5 +140,82 @@ extern "C" int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream) {
 
 extern "C" int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream) {
   MP_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return MP_OK;
+}
+
+// ---------------------------------------------------------------- graphs and events
+// Stream capture / replay of a whole pipeline step, and timing events that stay
+// valid inside captured graphs (recorded as external event nodes).
+extern "C" int mp_graph_begin(void* stream) {
+  MP_CUDA_TRY(cudaStreamBeginCapture((cudaStream_t)stream, cudaStreamCaptureModeThreadLocal));
+  return MP_OK;
+}
+
+extern "C" int mp_graph_end(void* stream, void** graph_exec) {
+  cudaGraph_t g = nullptr;
+  MP_CUDA_TRY(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  cudaGraphExec_t ex = nullptr;
+  const cudaError_t e = cudaGraphInstantiateWithFlags(&ex, g, 0);
+  cudaGraphDestroy(g);
+  MP_CUDA_TRY(e);
+  *graph_exec = (void*)ex;
+  return MP_OK;
+}
+
+extern "C" int mp_graph_launch(void* graph_exec, void* stream) {
+  MP_CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream));
+  return MP_OK;
+}
+
+extern "C" int mp_graph_destroy(void* graph_exec) {
+  MP_CUDA_TRY(cudaGraphExecDestroy((cudaGraphExec_t)graph_exec));
+  return MP_OK;
+}
+
+extern "C" int mp_event_create(void** ev) {
+  cudaEvent_t e;
+  MP_CUDA_TRY(cudaEventCreate(&e));
+  *ev = (void*)e;
+  return MP_OK;
+}
+
+extern "C" int mp_event_record(void* ev, void* stream) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  MP_CUDA_TRY(cudaStreamIsCapturing((cudaStream_t)stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    MP_CUDA_TRY(cudaEventRecordWithFlags((cudaEvent_t)ev, (cudaStream_t)stream, cudaEventRecordExternal));
+  else
+    MP_CUDA_TRY(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)stream));
+  return MP_OK;
+}
+
+extern "C" int mp_event_elapsed_ms(void* a, void* b, float* ms) {
+  MP_CUDA_TRY(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b));
+  return MP_OK;
+}
+
+extern "C" int mp_event_destroy(void* ev) {
+  MP_CUDA_TRY(cudaEventDestroy((cudaEvent_t)ev));
+  return MP_OK;
+}
+
+// Keep [ptr, ptr + bytes) resident in L2 for kernels launched on `stream` (persisting
+// access-policy window; bytes = 0 clears it). Used for the residual stream, which is
+// re-read by every layer's router, gather and combine while 1.2 GB of weights stream by.
+extern "C" int mp_l2_persist(void* ptr, size_t bytes, float hit_ratio, void* stream) {
+  int dev = 0;
+  MP_CUDA_TRY(cudaGetDevice(&dev));
+  int max_win = 0, max_persist = 0;
+  MP_CUDA_TRY(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  MP_CUDA_TRY(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  const size_t win = std::min(bytes, (size_t)max_win);
+  MP_CUDA_TRY(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(win, (size_t)max_persist)));
+  cudaStreamAttrValue attr = {};
+  attr.accessPolicyWindow.base_ptr = ptr;
+  attr.accessPolicyWindow.num_bytes = win;
+  attr.accessPolicyWindow.hitRatio = win ? hit_ratio : 0.f;
+  attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  MP_CUDA_TRY(cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &attr));
   return MP_OK;
 }

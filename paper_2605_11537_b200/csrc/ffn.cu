@@ -10,6 +10,7 @@
 // segment is a contiguous run of A rows; replicas of one expert alias the same
 // weight rows (no copies on one GPU).
 #include "epilogues.cuh"
+#include "gemm2_sm100.cuh"
 #include "launch.cuh"
 
 #include <algorithm>
@@ -73,38 +74,50 @@ extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
   return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp);
 }
 
-static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, int tiled) {
-  if (tiled) return make_tmap_bf16(tb, w, (uint64_t)E * N * (K / 64), 64, 64, bn);
-  return make_tmap_bf16(tb, w, (uint64_t)E * N, K, K, bn);
+static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, int tiled, int box_rows) {
+  if (tiled) return make_tmap_bf16(tb, w, (uint64_t)E * N * (K / 64), 64, 64, box_rows);
+  return make_tmap_bf16(tb, w, (uint64_t)E * N, K, K, box_rows);
 }
 
+// flags: bit 0 = pre-tiled weights, bit 1 = CTA-pair (cta_group::2) kernel over paired pieces
 static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
-                  const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, int tiled,
+                  const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, int flags,
                   cudaStream_t st) {
   // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
+  const int tiled = flags & 1, pair = (flags >> 1) & 1;
+  static const bool diag_nostore = getenv("MP_DIAG_NOSTORE") != nullptr;  // profiling switch only
+  EpiStoreBf16 e{hid, diag_nostore ? 0 : Fp, nullptr, 1, 0};
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
   if (rc) return rc;
-  rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled);
+  rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled, pair ? 128 : 256);
   if (rc) return rc;
+  if (pair) {
+    Seg2Sched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
+    return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
+  }
   SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
-  static const bool diag_nostore = getenv("MP_DIAG_NOSTORE") != nullptr;  // profiling switch only
-  EpiStoreBf16 e{hid, diag_nostore ? 0 : Fp, nullptr, 1, 0};
   return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
 }
 
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
-                    const __nv_bfloat16* hid, int tiled, cudaStream_t st) {
+                    const __nv_bfloat16* hid, int flags, cudaStream_t st) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
+  const int tiled = flags & 1, pair = (flags >> 1) & 1;
   const int bn = mp_ffn_down_bn(dp);
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
   if (rc) return rc;
-  rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled);
+  rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
   if (rc) return rc;
-  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
   EpiScatterAdd e{y, dp, tok_of_row};
+  if (pair) {
+    MP_REQUIRE(bn == 256, MP_ERR_CONFIG, "ffn pair mode needs dp %% 256 == 0");
+    Seg2Sched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
+    return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
+  }
+  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, num_sms(), st);
   return launch_gemm<64, 8>(ta, tb, s, e, num_sms(), st);
@@ -128,18 +141,18 @@ extern "C" int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const
   return MP_OK;
 }
 
-extern "C" int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int tiled, const int32_t* piece_row,
+extern "C" int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int flags, const int32_t* piece_row,
                          const int32_t* piece_rows, const int32_t* exp_begin, void* ws, size_t ws_bytes,
                          void* stream) {
   FFN_CHECKS();
-  return ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, tiled, (cudaStream_t)stream);
+  return ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, flags, (cudaStream_t)stream);
 }
 
-extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, int tiled,
+extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, int flags,
                            const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                            const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
   FFN_CHECKS();
-  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, tiled,
+  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags,
                   (cudaStream_t)stream);
 }
 

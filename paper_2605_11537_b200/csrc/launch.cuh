@@ -4,6 +4,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "gemm2_sm100.cuh"
 #include "gemm_sm100.cuh"
 
 namespace mp {
@@ -25,6 +26,23 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched
     configured = true;
   }
   if (grid < 1) grid = 1;
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+template <int BN, int STAGES, class Sched, class Epi>
+int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched, const Epi& epi, int grid,
+                 cudaStream_t st) {
+  auto kern = k_umma_gemm2<BN, STAGES, Sched, Epi>;
+  const int smem = Gemm2Smem<BN, STAGES>::kBytes;
+  static bool configured = false;
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  if (grid < 2) grid = 2;
+  grid &= ~1;  // whole clusters
   kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;

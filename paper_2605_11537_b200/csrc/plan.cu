@@ -229,6 +229,36 @@ __global__ void k_place_rank(const int32_t* __restrict__ assign, int T, int E, i
   token_event[(size_t)l * T + t] = ev;
 }
 
+__device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// Pad each expert's piece count to even (the CTA-pair GEMM computes pieces 2p, 2p+1
+// of one expert per cluster). s_off: exclusive slot offsets (E + 1), s_pc: pieces per slot.
+__device__ inline void pad_pieces_even(const int* s_off, int E, int* s_pc) {
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int tot = 0;
+    for (int s = s_off[e]; s < s_off[e + 1]; ++s) tot += s_pc[s];
+    if (tot & 1) s_pc[s_off[e + 1] - 1] += 1;
+  }
+  __syncthreads();
+}
+
+// Pieces of one slot: M-tiles (split) or the whole slot; extra pieces beyond the
+// real ones are empty padding (0 rows, a valid row address).
+__device__ inline void emit_pieces(int32_t* pr, int32_t* pn, int p0, int np, int row0, int size, int split) {
+  for (int p = 0; p < np; ++p) {
+    const int rows = split ? min(kBlockMRows, size - p * kBlockMRows) : (p == 0 ? size : 0);
+    pr[p0 + p] = (split && rows > 0) ? row0 + p * kBlockMRows : row0;
+    pn[p0 + p] = max(rows, 0);
+  }
+}
+
 // Execution map per layer (src/simulator.py:185-203) + slot rows + GEMM pieces.
 // grid L, block 1024. smem: s_off[E+1] s_n[E] s_row[MS+1] s_pc[MS+1]
 __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_slots, int split_m,
@@ -274,9 +304,10 @@ __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_
     const int j = s - s_off[lo], c = s_off[lo + 1] - s_off[lo], n = s_n[lo];
     const int size = n > j ? (n - j + c - 1) / c : 0;
     s_row[s] = size;
-    s_pc[s] = split_m ? cdiv(size, kBlockMRows) : (size > 0 ? 1 : 0);
+    s_pc[s] = (split_m & 1) ? cdiv(size, kBlockMRows) : (size > 0 ? 1 : 0);
   }
   __syncthreads();
+  if (split_m & 2) pad_pieces_even(s_off, E, s_pc);  // CTA-pair GEMM: even piece count per expert
   block_exclusive_scan(s_row, ns, red);
   const int P = block_exclusive_scan(s_pc, ns, red);
   if (threadIdx.x == 0) {
@@ -294,10 +325,7 @@ __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_
     const int row0 = s_row[s];
     const int size = (s + 1 < ns ? s_row[s + 1] : total_rows) - row0;
     const int p0 = s_pc[s], np = s_pc[s + 1] - p0;
-    for (int p = 0; p < np; ++p) {
-      pr[p0 + p] = split_m ? row0 + p * kBlockMRows : row0;
-      pn[p0 + p] = split_m ? min(kBlockMRows, size - p * kBlockMRows) : size;
-    }
+    emit_pieces(pr, pn, p0, np, row0, size, split_m & 1);
   }
   for (int e = threadIdx.x; e <= E; e += blockDim.x) {
     off_g[(size_t)l * (E + 1) + e] = s_off[e];
@@ -337,9 +365,18 @@ __global__ void k_seg_layer(const int32_t* __restrict__ size, const int32_t* __r
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
     const int n = size[s];
     s_row[s] = n;
-    s_pc[s] = split_m ? cdiv(n, kBlockMRows) : (n > 0 ? 1 : 0);
+    s_pc[s] = (split_m & 1) ? cdiv(n, kBlockMRows) : (n > 0 ? 1 : 0);
   }
   __syncthreads();
+  if (split_m & 2) {  // even piece count per expert (slots grouped by expert)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+      const int a = lower_bound_i32(slot_expert, S, e), b = lower_bound_i32(slot_expert, S, e + 1);
+      int tot = 0;
+      for (int s = a; s < b; ++s) tot += s_pc[s];
+      if (tot & 1) s_pc[b - 1] += 1;
+    }
+    __syncthreads();
+  }
   const int total = block_exclusive_scan(s_row, S, red);
   const int P = block_exclusive_scan(s_pc, S, red);
   if (threadIdx.x == 0) {
@@ -351,10 +388,7 @@ __global__ void k_seg_layer(const int32_t* __restrict__ size, const int32_t* __r
     slot_row_g[s] = s_row[s];
     const int row0 = s_row[s], n = s_row[s + 1] - row0;
     const int p0 = s_pc[s], np = s_pc[s + 1] - p0;
-    for (int p = 0; p < np; ++p) {
-      piece_row[p0 + p] = split_m ? row0 + p * kBlockMRows : row0;
-      piece_rows[p0 + p] = split_m ? min(kBlockMRows, n - p * kBlockMRows) : n;
-    }
+    emit_pieces(piece_row, piece_rows, p0, np, row0, n, split_m & 1);
   }
   for (int e = threadIdx.x; e <= E; e += blockDim.x) {
     int lo = 0, hi = S;  // first slot with slot_expert >= e

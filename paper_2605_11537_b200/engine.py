@@ -24,6 +24,7 @@ Replication modes (SURVEY.md §7 baselines):
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import asdict, dataclass
 
@@ -247,15 +248,15 @@ class MoEPipeline:
                   ptr(self.ws_exec), self.ws_exec_n, sp)
         _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
-            ev[0].record()
+            ev[0].record(sp)
         _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), lay.tiled, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
-            ev[1].record()
+            ev[1].record(sp)
         _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), lay.tiled, ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
                   ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
-            ev[2].record()
+            ev[2].record(sp)
         return 3 + 4 + 1 + 1 + 1
 
     def step(self, x: torch.Tensor, events=None) -> int:
@@ -271,6 +272,22 @@ class MoEPipeline:
         self.launches_per_step = n
         return n
 
+    # ------------------------------------------------------------------ CUDA graph
+    def capture(self, x: torch.Tensor, events=None) -> "StepGraph":
+        """Capture one step over the fixed residual-stream buffer ``x`` (run ``step`` once
+        first so every kernel attribute is configured). Replays need no host work."""
+        sp = stream_ptr()
+        _lib.call("mp_graph_begin", sp)
+        try:
+            n = self.step(x, events)
+        except Exception:
+            ex = ctypes.c_void_p()
+            _lib.load_library().mp_graph_end(sp, ctypes.byref(ex))
+            raise
+        ex = ctypes.c_void_p()
+        _lib.call("mp_graph_end", sp, ctypes.byref(ex))
+        return StepGraph(ex, n)
+
     # ------------------------------------------------------------------ accounting
     def expert_weight_bytes(self) -> int:
         """bf16 bytes of one expert's U + V (4 d F)."""
@@ -279,6 +296,45 @@ class MoEPipeline:
     def touched_experts(self) -> torch.Tensor:
         """(L,) experts that received tokens in the last step (device)."""
         return (self.exp_begin[:, 1:] > self.exp_begin[:, :-1]).sum(dim=1)
+
+
+class DeviceEvent:
+    """CUDA event owned by libmoempmc (valid inside captured graphs)."""
+
+    def __init__(self):
+        self.h = ctypes.c_void_p()
+        _lib.call("mp_event_create", ctypes.byref(self.h))
+
+    def record(self, sp: int):
+        _lib.call("mp_event_record", self.h, sp)
+
+    def elapsed_ms(self, end: "DeviceEvent") -> float:
+        ms = ctypes.c_float()
+        _lib.call("mp_event_elapsed_ms", self.h, end.h, ctypes.byref(ms))
+        return float(ms.value)
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.load_library().mp_event_destroy(self.h)
+        except Exception:
+            pass
+
+
+class StepGraph:
+    def __init__(self, exec_handle: ctypes.c_void_p, launches: int):
+        self.h = exec_handle
+        self.launches = launches
+
+    def replay(self):
+        _lib.call("mp_graph_launch", self.h, stream_ptr())
+
+    def __del__(self):
+        try:
+            if self.h:
+                _lib.load_library().mp_graph_destroy(self.h)
+        except Exception:
+            pass
 
 
 def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor) -> DeviceMoeLayer:

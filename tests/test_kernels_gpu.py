@@ -224,3 +224,49 @@ def test_tiled_weight_layout_is_bitwise_identical(dev):
               stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(y, y_ref)
+
+
+@pytest.mark.parametrize("split", [1, 0])
+def test_cta_pair_ffn_matches_single_cta(dev, split):
+    """cta_group::2 grouped GEMMs over paired pieces == the 1-CTA kernels, bit for bit."""
+    rng = np.random.default_rng(5 + split)
+    T, E, d, F = 3000, 9, 256, 512
+    p = 1.0 / (np.arange(E) + 1.0) ** 1.3
+    route = torch.from_numpy(rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)).to(dev)
+    slot_expert = torch.arange(E, dtype=torch.int32, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
+    sws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    pn = 2 * (E + (T + 127) // 128)
+
+    def segments(flags):
+        tor = torch.empty(T, **i32)
+        prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
+        _lib.call("mp_segments_from_slots", ptr(route), ptr(slot_expert), T, E, E, flags, ptr(tor), ptr(prow),
+                  ptr(prows), ptr(eb), ptr(sws), nb, stream_ptr())
+        return tor, prow, prows, eb
+
+    U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
+    V = (torch.randn(E * d, F, device=dev) / 22).bfloat16()
+    Ut, Vt = torch.empty_like(U), torch.empty_like(V)
+    _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, 256, stream_ptr())
+    x = torch.randn(T, d, device=dev)
+    fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+    ws = torch.empty(fb, dtype=torch.uint8, device=dev)
+
+    def run(flags_seg, flags_ffn, u, v):
+        tor, prow, prows, eb = segments(flags_seg)
+        y = x.clone()
+        _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
+        _lib.call("mp_ffn_up", T, d, F, E, ptr(u), flags_ffn, ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb,
+                  stream_ptr())
+        _lib.call("mp_ffn_down", ptr(y), T, d, F, E, ptr(v), flags_ffn, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+                  ptr(ws), fb, stream_ptr())
+        torch.cuda.synchronize()
+        return y, eb
+
+    y1, _ = run(split, 0, U, V)
+    y2, eb = run(split | 2, 3, Ut, Vt)
+    assert (eb.cpu().numpy() % 2 == 0).all()
+    assert torch.equal(y1, y2)

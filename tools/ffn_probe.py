@@ -38,10 +38,12 @@ def main():
         prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
         nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
         sws = torch.empty(nb, dtype=torch.uint8, device=dev)
-        _lib.call("mp_segments_from_slots", ptr(r), ptr(se), T, E, E, split, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
-                  ptr(sws), nb, stream_ptr())
-        _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
-        for tiled, (u, v) in ((0, (U, V)), (1, (Ut, Vt))):
+        for tiled, (u, v) in ((1, (Ut, Vt)), (3, (Ut, Vt))):
+            pn = 2 * (E + T // 128 + 1)
+            prow, prows = torch.empty(pn, **i32), torch.empty(pn, **i32)
+            _lib.call("mp_segments_from_slots", ptr(r), ptr(se), T, E, E, split | (tiled & 2), ptr(tor), ptr(prow),
+                      ptr(prows), ptr(eb), ptr(sws), nb, stream_ptr())
+            _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
             t1 = timeit(lambda: _lib.call("mp_ffn_up", T, d, F, E, ptr(u), tiled, ptr(prow), ptr(prows), ptr(eb),
                                           ptr(ws), fb, stream_ptr()), iters=10)
             y = x.clone()
