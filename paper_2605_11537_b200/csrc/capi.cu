@@ -77,6 +77,24 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
   return MP_OK;
 }
 
+// 2-D fp32 row-major tensor map, box = [box_rows x 32 cols] (128 B), SWIZZLE_128B (TF32 operands).
+int make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                  uint32_t box_rows) {
+  auto enc = get_encode();
+  MP_REQUIRE(enc != nullptr, MP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  MP_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (row_stride_elems * 4) % 16 == 0, MP_ERR_CONFIG,
+             "tensor map: base and row stride must be 16-byte aligned");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MP_REQUIRE(r == CUDA_SUCCESS, MP_ERR_CUDA, "cuTensorMapEncodeTiled(f32) failed (%d)", (int)r);
+  return MP_OK;
+}
+
 }  // namespace mp
 
 using namespace mp;

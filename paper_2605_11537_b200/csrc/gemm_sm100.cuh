@@ -59,7 +59,7 @@ struct GemmSmem {
 //    (lane quadrant, accumulator stage, column c0); the thread handles tile columns
 //    [c0, c0 + NC)).
 
-template <int BN, int STAGES, class Sched, class Epi>
+template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched,
                 Epi epi) {
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_bf16_f32(kBlockM, BN);
+      constexpr uint32_t idesc = Kind::idesc(kBlockM, BN);
       uint32_t stage = 0, phase = 0, tile = 0;
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const Unit U = sched.unit(u);
@@ -147,9 +147,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t adesc = sw128_kmajor_desc(smem_u32(sa));
             const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sa + L::kABytes));
 #pragma unroll
-            for (int k = 0; k < kBlockK / 16; ++k) {
-              // advance 16 bf16 = 32 B inside the swizzle atom: +2 in the >>4 address field
-              umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < 4; ++k) {
+              // advance 32 B of K inside the swizzle atom: +2 in the >>4 address field
+              Kind::mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
             }
             umma_commit(&empty[stage]);
             if (++stage == STAGES) {
@@ -272,6 +272,21 @@ struct SegSched {
   __device__ int a_kcol(int k) const { return k * kBlockK; }
   __device__ int b_kcol(int k) const { return b_tiled ? 0 : k * kBlockK; }
   __device__ int b_krow(int k) const { return b_tiled ? k * bn : 0; }
+};
+
+// Dense fp32/TF32 GEMM: k-blocks of 32 fp32 (128 B).
+struct DenseTf32Sched {
+  static constexpr bool kStreamB = false;
+  int M, n_tiles, kb, bn;
+  __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
+  __device__ Unit unit(int u) const {
+    const int mb = u / n_tiles, nb = u - mb * n_tiles;
+    return Unit{mb * kBlockM, min(kBlockM, M - mb * kBlockM), nb * bn, nb * bn};
+  }
+  __device__ int num_kb() const { return kb; }
+  __device__ int a_kcol(int k) const { return k * 32; }
+  __device__ int b_kcol(int k) const { return k * 32; }
+  __device__ int b_krow(int) const { return 0; }
 };
 
 // Split-bf16 "3-pass" product for fp32-faithful dot products on the tensor

@@ -15,10 +15,13 @@ int num_sms();
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                    uint32_t box_rows);
 
-template <int BN, int STAGES, class Sched, class Epi>
+int make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+                  uint32_t box_rows);
+
+template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched, const Epi& epi, int grid,
                 cudaStream_t st) {
-  auto kern = k_umma_gemm<BN, STAGES, Sched, Epi>;
+  auto kern = k_umma_gemm<BN, STAGES, Sched, Epi, Kind>;
   const int smem = GemmSmem<BN, STAGES>::kBytes;
   static bool configured = false;  // one attribute call per instantiation
   if (!configured) {
