@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
+    p.add_argument("--ffn", choices=["fused", "two"], default="two")
     return p.parse_args()
 
 
@@ -210,7 +211,7 @@ def run_ours(args):
 
     cfg = PipelineConfig(num_layers=args.layers, num_experts=args.experts, tokens=args.tokens,
                          capacity=args.capacity, demand_unit=args.demand_unit, replication=args.replication,
-                         predictor=args.predictor, seed=args.seed + rank)
+                         predictor=args.predictor, ffn=args.ffn, seed=args.seed + rank)
     pipe = MoEPipeline(cfg)
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]
@@ -275,9 +276,11 @@ def run_ours(args):
     t_up, t_down = sum(up) / len(up), sum(down) / len(down)
     touched = pipe.touched_experts().float().mean().item()
     w_bytes = touched * pipe.expert_weight_bytes()
-    act_up = T * (2 * d + 2 * cfg.d_ff)
-    act_down = T * (2 * cfg.d_ff + 8 * d)
-    alg_bytes = w_bytes + act_up + act_down
+    # algorithmic bytes of one MoE layer's FFN: every touched expert's U and V once (bf16)
+    # plus the token activations it must move: gather (read fp32 x, write bf16 rows), GEMM1
+    # reads the bf16 rows, the combine reads and writes fp32 x. The hidden H is an
+    # intermediate (kept in an L2 ring by the fused kernel) and is not counted.
+    alg_bytes = w_bytes + T * (4 * d + 2 * d + 2 * d + 8 * d)
     flops = 4.0 * T * d * cfg.d_ff
     peaks, peak_kind = load_peaks()
     achieved = alg_bytes / ((t_up + t_down) * 1e-3) / 1e9
@@ -307,7 +310,8 @@ def run_ours(args):
         "clocks": clk,
         "gpu_launches": launches,
         "roofline": {
-            "kernel": "grouped expert GEMM pair (k_umma_gemm SegSched: GEMM1 relu + GEMM2 scatter-combine), per layer",
+            "kernel": ("fused grouped expert FFN (k_ffn_fused: GEMM1 relu + GEMM2 scatter-combine, H in L2 ring)"
+                       if args.ffn == "fused" else "grouped expert GEMM pair (GEMM1 relu + GEMM2 scatter-combine)"),
             "bound": "hbm",
             "achieved": achieved,
             "peak": peaks["hbm_gbs"],

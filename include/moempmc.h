@@ -199,6 +199,16 @@ MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, in
                        const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
                        size_t ws_bytes, void* stream);
 MP_API int mp_ffn_down_bn(int dp);
+/* One MoE layer's FFN as ONE persistent launch (after a gather): GEMM1 and GEMM2 units
+ * of every piece interleaved, the hidden activations living in an L2-resident ring of
+ * 128-row slots (never a T x F HBM buffer), device-side completion counters ordering
+ * GEMM2 after GEMM1 and slot reuse after GEMM2. Needs pre-tiled weights (BN 256 for both),
+ * pieces of <= 128 rows (split_m bit 0), dp % 256 == 0, Fp % 256 == 0; x updated in place.
+ * max_pieces >= the piece-array capacity used by the builder. */
+MP_API size_t mp_ffn_fused_workspace_bytes(int T, int dp, int Fp, int max_pieces);
+MP_API int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* u_tiled, const void* v_tiled,
+                        const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                        const int32_t* exp_begin, int max_pieces, void* ws, size_t ws_bytes, void* stream);
 /* Weight layout transform for the grouped GEMM B operand:
  * dst[g][n / BN][k / 64][n % BN][k % 64] = src[g * N + n][k]   (bf16, G groups of N x K). */
 MP_API int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int BN, void* stream);

@@ -167,3 +167,289 @@ extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E
   if (rc) return rc;
   return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, 0, st);
 }
+
+// ============================================================================
+// Fused, interleaved expert FFN: GEMM1 (relu) and GEMM2 (scatter + residual) of
+// every piece in ONE persistent launch, with the hidden activations H kept in
+// an L2-resident ring of 128-row slots instead of a T x F HBM buffer.
+//
+// Unit order (static round-robin over CTAs, every role walks the same list):
+//   group q = [12 GEMM1 units of piece q (BN slices of F)] +
+//             [ 3 GEMM2 units of piece q - kLag (BN slices of d)]
+// Piece p's H rows live in ring slot p % kSlots (kSlots > kLag). Dependencies
+// both point to EARLIER groups, so the persistent schedule cannot deadlock:
+//   GEMM2(p) waits done1[p] == n_tiles1   (H of piece p complete)  -- group p + kLag
+//   GEMM1(p) waits done2[p - kSlots] == n_tiles2 (slot free again)  -- group p - kSlots + kLag
+// Writers publish with __threadfence + atomicAdd after a named barrier of the
+// epilogue warps; readers acquire, then fence.proxy.async before TMA reads.
+// ============================================================================
+namespace mp {
+
+constexpr int kFfnLag = 16;
+constexpr int kFfnSlots = 48;
+
+struct FfnFused {
+  const int32_t* piece_row;
+  const int32_t* piece_rows;
+  const int32_t* exp_begin;
+  const int32_t* tok_of_row;
+  int E, nt1, nt2, kb1, kb2;  // F/256, d/256, d/64, F/64
+  int F;
+  __nv_bfloat16* ring;        // kSlots x 128 x F
+  float* x;                   // residual stream (T x ldx)
+  int ldx;
+  int32_t* done1;
+  int32_t* done2;
+  int P_unused;
+};
+
+struct FUnit {
+  int kind;  // 0 = GEMM1, 1 = GEMM2, -1 = empty
+  int p, e, nt, rows, a_row, b_row;
+};
+
+__device__ __forceinline__ int ffn_num_pieces(const FfnFused& f) { return f.exp_begin[f.E]; }
+
+__device__ __forceinline__ FUnit ffn_unit(const FfnFused& f, int u) {
+  const int per = f.nt1 + f.nt2;
+  const int q = u / per, local = u - q * per;
+  const int P = ffn_num_pieces(f);
+  FUnit U;
+  U.kind = -1;
+  int p, nt;
+  if (local < f.nt1) {
+    p = q;
+    nt = local;
+    if (p >= P) return U;
+    U.kind = 0;
+  } else {
+    p = q - kFfnLag;
+    nt = local - f.nt1;
+    if (p < 0 || p >= P) return U;
+    U.kind = 1;
+  }
+  U.rows = f.piece_rows[p];
+  if (U.rows <= 0) {
+    U.kind = -1;
+    return U;
+  }
+  int lo = 0, hi = f.E;  // expert of piece p: exp_begin[lo] <= p < exp_begin[lo + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (f.exp_begin[mid] <= p) lo = mid; else hi = mid;
+  }
+  U.p = p;
+  U.e = lo;
+  U.nt = nt;
+  if (U.kind == 0) {
+    U.a_row = f.piece_row[p];
+    U.b_row = (lo * f.nt1 + nt) * f.kb1 * 256;
+  } else {
+    U.a_row = (p % kFfnSlots) * kBlockM;
+    U.b_row = (lo * f.nt2 + nt) * f.kb2 * 256;
+  }
+  return U;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int32_t* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_ffn_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmU,
+                const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmV, FfnFused f) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  constexpr int BN = 256, STAGES = 4;
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* scratch_all = reinterpret_cast<uint32_t*>(smem + L::kScratchOffset);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX);
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmH);
+    tma_prefetch(&tmV);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int nunits = (ffn_num_pieces(f) + kFfnLag) * (f.nt1 + f.nt2);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      const uint64_t pol_w = policy_evict_first();
+      uint32_t stage = 0, phase = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const FUnit U = ffn_unit(f, u);
+        if (U.kind < 0) continue;
+        const CUtensorMap* ta = U.kind == 0 ? &tmX : &tmH;
+        const CUtensorMap* tb = U.kind == 0 ? &tmU : &tmV;
+        const int nkb = U.kind == 0 ? f.kb1 : f.kb2;
+        if (U.kind == 0) {
+          const int prev = U.p - kFfnSlots;  // ring slot must be drained by the previous occupant
+          if (prev >= 0 && f.piece_rows[prev] > 0)
+            while (ld_acquire_gpu(&f.done2[prev]) < f.nt2) __nanosleep(64);
+        } else {
+          while (ld_acquire_gpu(&f.done1[U.p]) < f.nt1) __nanosleep(64);
+          fence_proxy_async_global();  // H was written through the generic proxy
+        }
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+          tma_load_2d(sa, ta, &full[stage], kb * kBlockK, U.a_row);
+          tma_load_2d_hint(sb, tb, &full[stage], 0, U.b_row + kb * BN, pol_w);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(kBlockM, BN);
+      uint32_t stage = 0, phase = 0, tile = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const FUnit U = ffn_unit(f, u);
+        if (U.kind < 0) continue;
+        const int nkb = U.kind == 0 ? f.kb1 : f.kb2;
+        const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
+        mbar_wait(&tempty[as], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint8_t* sa = smem + stage * L::kStageBytes;
+          const uint64_t adesc = sw128_kmajor_desc(smem_u32(sa));
+          const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sa + L::kABytes));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[as]);
+        ++tile;
+      }
+    }
+  } else if (warp >= 4) {
+    // -------------------------------------------------------------- epilogue (2 warpgroups)
+    const int q = warp & 3, half = (warp - 4) >> 2;
+    const int r = q * 32 + lane;
+    const int c0 = half * (BN / 2);
+    uint32_t* scratch = scratch_all + (warp - 4) * L::kScratchWordsPerWarp;
+    uint32_t tile = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const FUnit U = ffn_unit(f, u);
+      if (U.kind < 0) continue;
+      const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
+      mbar_wait(&tfull[as], aph);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c0;
+      if (U.kind == 0) {
+        const Unit V{(U.p % kFfnSlots) * kBlockM, U.rows, U.b_row, U.nt * BN};  // H rows -> ring slot
+        EpiStoreBf16 e{f.ring, f.F, nullptr, 1, 0};
+        e.template run<BN / 2>(V, 0, r, taddr, c0, nullptr, scratch);
+      } else {
+        // rows of this piece map to tokens through the piece's permuted rows
+        const Unit V{U.a_row, U.rows, U.b_row, U.nt * BN};
+        EpiScatterAdd e{f.x, f.ldx, f.tok_of_row + (f.piece_row[U.p] - U.a_row)};
+        e.template run<BN / 2>(V, 0, r, taddr, c0, nullptr, scratch);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[as]);
+      named_bar_sync(2, 32 * kEpiWarps);  // every epilogue warp finished its stores for this unit
+      if (threadIdx.x == 128) {
+        __threadfence();
+        if (U.kind == 0) {
+          fence_proxy_async_global();
+          atomicAdd(&f.done1[U.p], 1);
+        } else {
+          atomicAdd(&f.done2[U.p], 1);
+        }
+      }
+      ++tile;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+#endif
+}
+
+}  // namespace mp
+
+extern "C" size_t mp_ffn_fused_workspace_bytes(int T, int dp, int Fp, int max_pieces) {
+  return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)kFfnSlots * kBlockM * Fp) +
+         al(sizeof(int32_t) * 2 * (size_t)max_pieces);
+}
+
+extern "C" int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* u_tiled, const void* v_tiled,
+                            const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                            const int32_t* exp_begin, int max_pieces, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(T >= 1 && E >= 1 && dp % 256 == 0 && Fp % 256 == 0, MP_ERR_CONFIG,
+             "mp_ffn_fused: need dp %% 256 == 0 and Fp %% 256 == 0");
+  MP_REQUIRE(ws_bytes >= mp_ffn_fused_workspace_bytes(T, dp, Fp, max_pieces), MP_ERR_CONFIG,
+             "mp_ffn_fused: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* p = (char*)ws;
+  __nv_bfloat16* xperm = (__nv_bfloat16*)p;
+  p += al(sizeof(__nv_bfloat16) * (size_t)T * dp);
+  __nv_bfloat16* ring = (__nv_bfloat16*)p;
+  p += al(sizeof(__nv_bfloat16) * (size_t)kFfnSlots * kBlockM * Fp);
+  int32_t* done = (int32_t*)p;
+  MP_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(int32_t) * 2 * (size_t)max_pieces, st));
+  k_gather_rows<<<cdiv(T * 32, 256), 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+  MP_CUDA_TRY(cudaGetLastError());
+  CUtensorMap tx, tu, th, tv;
+  int rc = make_tmap_bf16(&tx, xperm, T, dp, dp, kBlockM);
+  if (!rc) rc = make_tmap_bf16(&tu, u_tiled, (uint64_t)E * Fp * (dp / 64), 64, 64, 256);
+  if (!rc) rc = make_tmap_bf16(&th, ring, (uint64_t)kFfnSlots * kBlockM, Fp, Fp, kBlockM);
+  if (!rc) rc = make_tmap_bf16(&tv, v_tiled, (uint64_t)E * dp * (Fp / 64), 64, 64, 256);
+  if (rc) return rc;
+  FfnFused f{piece_row, piece_rows, exp_begin, tok_of_row, E, Fp / 256, dp / 256, dp / 64, Fp / 64, Fp, ring,
+             x, dp, done, done + max_pieces, 0};
+  const int smem = GemmSmem<256, 4>::kBytes;
+  static bool configured = false;
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(k_ffn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  k_ffn_fused<<<num_sms(), kGemmThreads, smem, st>>>(tx, tu, th, tv, f);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}

@@ -50,6 +50,7 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
+    ffn: str = "two"              # two (GEMM1 + GEMM2 launches) | fused (experimental: one launch, H in an L2 ring)
     skew: float = 1.2
     noise: float = 0.1
     seed: int = 0
@@ -202,6 +203,9 @@ class MoEPipeline:
         self.ws_router = ws(self.ws_router_n)
         self.ws_ffn_n = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
         self.ws_ffn = ws(self.ws_ffn_n)
+        self.pstride = pstride
+        self.ws_fused_n = _lib.size_query("mp_ffn_fused_workspace_bytes", T, d, F, pstride)
+        self.ws_fused = ws(self.ws_fused_n) if cfg.ffn == "fused" else None
         self.launches_per_step = None
 
     # ------------------------------------------------------------------ pieces of a step
@@ -239,13 +243,25 @@ class MoEPipeline:
         """One MoE layer in place on the residual stream x."""
         cfg, T, E, d, F = self.cfg, self.cfg.tokens, self.cfg.num_experts, self.dp, self.Fp
         lay = self.layers[l]
-        split = 1 if cfg.replication == "split" else 0
+        # the fused FFN needs <= 128-row pieces: replicas longer than a tile are split into
+        # consecutive M tiles of the SAME replica (a replica is still one slot)
+        split = 1 if (cfg.replication == "split" or cfg.ffn == "fused") else 0
         _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
                   ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
         _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
                   ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
                   ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]),
                   ptr(self.ws_exec), self.ws_exec_n, sp)
+        if cfg.ffn == "fused":
+            if ev is not None:
+                ev[0].record(sp)
+            _lib.call("mp_ffn_fused", ptr(x), T, d, F, E, ptr(lay.U), ptr(lay.V), ptr(self.tok_of_row[l]),
+                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), self.pstride,
+                      ptr(self.ws_fused), self.ws_fused_n, sp)
+            if ev is not None:
+                ev[1].record(sp)
+                ev[2].record(sp)
+            return 3 + 4 + 1 + 1 + 1
         _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[0].record(sp)
