@@ -52,6 +52,7 @@ def parse_args():
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
     p.add_argument("--ffn", choices=["fused", "two"], default="two")
+    p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     return p.parse_args()
 
 
@@ -198,7 +199,7 @@ def config_dict(args, world):
         "num_layers": args.layers, "num_experts": args.experts, "d_model": 768, "d_ff": 3072,
         "tokens_per_gpu": args.tokens, "global_batch": args.tokens * world, "sru_layers": 10,
         "capacity": args.capacity, "demand_unit": args.demand_unit, "replication": args.replication,
-        "predictor": args.predictor, "zipf_skew": 1.2, "parallelism": f"replicas{world}" if world > 1 else "single",
+        "predictor": args.predictor, "zipf_skew": 1.2, "parallelism": f"ep{world}" if world > 1 else ("ep1" if args.ep else "single"),
         "l2": "inputs larger than L2 (14.5 GB of expert weights streamed per step)",
     }
 
@@ -214,6 +215,9 @@ def run_ours(args):
                          predictor=args.predictor, ffn=args.ffn, seed=args.seed + rank)
     pipe = MoEPipeline(cfg)
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
+    ep = world > 1 or args.ep
+    if ep:
+        pipe.enable_expert_parallel()
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]
     x = torch.empty(T, d, device="cuda")
 
@@ -235,7 +239,7 @@ def run_ours(args):
 
     ev = [[DeviceEvent() for _ in range(3)] for _ in range(L)]
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and not ep:
         graph = pipe.capture(x, ev)  # one CUDA graph per step, GEMM timing events inside it
         for k in range(2):
             x.copy_(batches[k % len(batches)][0])
@@ -270,7 +274,8 @@ def run_ours(args):
 
     # correctness spot checks on the last step (not timed)
     last = batches[(args.steps - 1) % len(batches)]
-    routing_exact = bool((pipe.route.long() == last[2]).all().item())
+    routing_exact = bool((pipe.route.long() == last[2]).all().item()) if not ep else \
+        bool((pipe.ep.last_route.long() == last[2][-1]).all().item())
     pred_acc = float((pipe.assign.long() == last[2]).float().mean().item())
 
     t_up, t_down = sum(up) / len(up), sum(down) / len(down)
@@ -360,7 +365,8 @@ def run_e2e(args, pipe, batches, world):
     comp_done = [torch.cuda.Event() for _ in range(2)]
     d2h_done = [torch.cuda.Event() for _ in range(2)]
 
-    graphs = [pipe.capture(dev[j]) for j in range(2)] if not args.no_graph else None
+    graphs = [pipe.capture(dev[j]) for j in range(2)] if not args.no_graph and getattr(pipe, "ep", None) is None \
+        else None
 
     def run(n, timed):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -213,6 +213,31 @@ MP_API int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* u_ti
  * dst[g][n / BN][k / 64][n % BN][k % 64] = src[g * N + n][k]   (bf16, G groups of N x K). */
 MP_API int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int BN, void* stream);
 
+/* ------------------------------------------------------------------ C1/C2: expert parallelism
+ * (SURVEY.md §8(e)). G ranks, tokens sharded by position, all expert weights resident on
+ * every GPU, replica j of expert e on GPU (e*G/E + j) mod G. Per layer, after the caller
+ * all-gathers per-rank expert counts C (G x E int32, from mp_histogram_ws):
+ *   mp_ep_plan         same residency/corrective update and global stable ranks as the
+ *                      single-device execution map; send/recv row counts per peer; this
+ *                      rank's send position per token; local pieces of hosted replicas
+ *   mp_ep_pack         bf16 rows into the send buffer (destination-major)
+ *   (caller: variable all-to-all of the rows, e.g. NCCL)
+ *   mp_ep_recv_layout  local row (slot-major, global token order) of every received row
+ *   mp_gather_rows_bf16 + mp_ffn_up/down (tok_of_row = recv_of_local: results land in
+ *                      receive order)  (caller: reverse all-to-all of fp32 results)
+ *   mp_ep_combine      x[t] += yback[send_pos[t]]
+ * Results are bit-identical to the single-GPU path. ws >= mp_ep_workspace_bytes. */
+MP_API size_t mp_ep_workspace_bytes(int G, int T, int E, int max_slots);
+MP_API int mp_ep_plan(const int32_t* route, int T, const int32_t* C, int G, int E, int rank, int max_slots,
+                      int split_m, int32_t* res, int32_t* send_counts, int32_t* recv_counts, int32_t* num_local_rows,
+                      int32_t* send_pos, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin, void* ws,
+                      size_t ws_bytes, void* stream);
+MP_API int mp_ep_pack(const float* x, int T, int d, const int32_t* send_pos, void* sendbuf, void* stream);
+MP_API int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, const int32_t* recvbuf_rows_unused,
+                             int32_t* recv_of_local, void* ws, size_t ws_bytes, void* stream);
+MP_API int mp_gather_rows_bf16(const void* buf, int n, int d, const int32_t* idx, void* out, void* stream);
+MP_API int mp_ep_combine(float* x, int T, int d, const float* yback, const int32_t* send_pos, void* stream);
+
 /* ------------------------------------------------------------------ K9
  * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):
  * dst <- src, `bytes` long, device-to-device (or peer) on `stream`. */

@@ -66,6 +66,12 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_fused": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _Z, _P]),
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
+    "mp_ep_workspace_bytes": (_Z, [_I, _I, _I, _I]),
+    "mp_ep_plan": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_ep_pack": (_I, [_P, _I, _I, _P, _P, _P]),
+    "mp_ep_recv_layout": (_I, [_I, _I, _I, _I, _I, _P, _P, _P, _Z, _P]),
+    "mp_gather_rows_bf16": (_I, [_P, _I, _I, _P, _P, _P]),
+    "mp_ep_combine": (_I, [_P, _I, _I, _P, _P, _P]),
     "mp_f32_to_bf16": (_I, [_P, _P, _Z, _P]),
     "mp_l2_persist": (_I, [_P, _Z, _F, _P]),
     "mp_graph_begin": (_I, [_P]),

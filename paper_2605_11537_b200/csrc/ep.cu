@@ -1,0 +1,322 @@
+// Expert-parallel dispatch/combine planning.
+//
+// G ranks, tokens sharded contiguously by position, every rank routes its own
+// tokens. After an all-gather of per-rank expert counts C[g][e], every rank
+// computes the SAME plan from C and the (replicated) residency state:
+//   * execution slots exactly as the single-device map (src/simulator.py:185-203):
+//     cnt_e = res_e, or one corrective replica; slot (e, j) for j < cnt_e;
+//   * a token's GLOBAL stable rank = its local rank + sum_{g < rank} C[g][e], so
+//     slot(t) = off[e] + grank mod cnt_e is bit-identical to one device;
+//   * replica (e, j) runs on GPU (home(e) + j) mod G, home(e) = e * G / E (all
+//     expert weights are resident on every GPU; placement spreads hot replicas);
+//   * rows(g, s) = #tokens of rank g on slot s, in closed form:
+//     #{y in [B_g, B_g + C_g) : y = j mod c} = F(B_g + C_g) - F(B_g),
+//     F(x) = max(0, ceil((x - j) / c)).
+// Sender packs rows by (destination, slot, position); receiver lays rows out by
+// (slot, global position) -- the single-device order -- so the grouped GEMM and
+// its results are bit-identical to the 1-GPU path.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace mp {
+
+__device__ __forceinline__ int runs_before(int x, int j, int c) {  // F(x)
+  return x > j ? (x - j + c - 1) / c : 0;
+}
+
+// grid 1, block 1024. ws layout given by EpPlanWs.
+struct EpPlanWs {
+  int32_t* off;        // E + 1 slot offsets
+  int32_t* cnt;        // E
+  int32_t* B;          // E: sum_{g < rank} C[g][e]
+  int32_t* slot_gpu;   // S
+  int32_t* slot_size;  // S
+  int32_t* rows;       // G x S
+  int32_t* send_base;  // S (this rank as sender)
+  int32_t* recv_start; // G x S (this rank as receiver)
+  int32_t* local_start;// G x S
+};
+
+__global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank, int max_slots, int split,
+                          int32_t* __restrict__ res, EpPlanWs w, int32_t* __restrict__ send_counts,
+                          int32_t* __restrict__ recv_counts, int32_t* __restrict__ num_local_rows,
+                          int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
+                          int32_t* __restrict__ exp_begin, int32_t* __restrict__ err) {
+  extern __shared__ int sm[];
+  __shared__ int red[40];
+  int* s_off = sm;                   // E + 1
+  int* s_lb = s_off + E + 1;         // max_slots + 1 : local base (hosted slots)
+  int* s_pc = s_lb + max_slots + 1;  // max_slots + 1 : pieces per slot
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int n = 0, b = 0;
+    for (int g = 0; g < G; ++g) {
+      const int c = C[(size_t)g * E + e];
+      n += c;
+      if (g < rank) b += c;
+    }
+    const int rp = res[e];
+    const int c = rp > 0 ? rp : (n > 0 ? 1 : 0);
+    res[e] = c;  // corrective replicas persist (src/simulator.py:190-192)
+    w.cnt[e] = c;
+    w.B[e] = b;
+    s_off[e] = c;
+  }
+  __syncthreads();
+  const int S = block_exclusive_scan(s_off, E, red);
+  if (threadIdx.x == 0) s_off[E] = S;
+  __syncthreads();
+  if (S > max_slots) {
+    if (threadIdx.x == 0) atomicExch(err, 1);
+    return;
+  }
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) w.off[e] = s_off[e];
+  // slots: expert, ordinal, size, GPU; per-rank row counts
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    int lo = 0, hi = E;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_off[mid] <= s) lo = mid; else hi = mid;
+    }
+    const int e = lo, j = s - s_off[e], c = s_off[e + 1] - s_off[e];
+    const int home = (int)(((long long)e * G) / E);
+    const int gpu = (home + j) % G;
+    int size = 0, acc = 0;
+    for (int g = 0; g < G; ++g) {
+      const int cg = C[(size_t)g * E + e];
+      const int r = runs_before(acc + cg, j, c) - runs_before(acc, j, c);
+      w.rows[(size_t)g * max_slots + s] = r;
+      size += r;
+      acc += cg;
+    }
+    w.slot_gpu[s] = gpu;
+    w.slot_size[s] = size;
+    s_lb[s] = (gpu == rank) ? size : 0;
+    s_pc[s] = (gpu == rank) ? (split ? cdiv(size, kBlockMRows) : (size > 0 ? 1 : 0)) : 0;
+  }
+  __syncthreads();
+  const int nloc = block_exclusive_scan(s_lb, S, red);  // local row base of hosted slots
+  const int P = block_exclusive_scan(s_pc, S, red);
+  if (threadIdx.x == 0) {
+    s_lb[S] = nloc;
+    s_pc[S] = P;
+    *num_local_rows = nloc;
+  }
+  __syncthreads();
+  // sender tables (this rank) and receiver tables, one thread per peer
+  if (threadIdx.x < G) {
+    const int d = threadIdx.x;
+    int acc = 0;
+    for (int s = 0; s < S; ++s)
+      if (w.slot_gpu[s] == d) {
+        w.send_base[s] = acc;  // relative to the destination's block
+        acc += w.rows[(size_t)rank * max_slots + s];
+      }
+    send_counts[d] = acc;
+    int acc2 = 0;
+    for (int s = 0; s < S; ++s)
+      if (w.slot_gpu[s] == rank) {
+        w.recv_start[(size_t)d * max_slots + s] = acc2;  // relative to source d's block
+        acc2 += w.rows[(size_t)d * max_slots + s];
+      }
+    recv_counts[d] = acc2;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int gpu = w.slot_gpu[s];
+    int displ = 0;
+    for (int g = 0; g < gpu; ++g) displ += send_counts[g];
+    w.send_base[s] += displ;
+    if (gpu == rank) {
+      int acc = s_lb[s], rdispl = 0;
+      for (int g = 0; g < G; ++g) {
+        w.local_start[(size_t)g * max_slots + s] = acc;
+        acc += w.rows[(size_t)g * max_slots + s];
+        w.recv_start[(size_t)g * max_slots + s] += rdispl;
+        rdispl += recv_counts[g];
+      }
+      const int row0 = s_lb[s], size = w.slot_size[s];
+      const int p0 = s_pc[s], np = s_pc[s + 1] - p0;
+      for (int p = 0; p < np; ++p) {
+        piece_row[p0 + p] = split ? row0 + p * kBlockMRows : row0;
+        piece_rows[p0 + p] = split ? min(kBlockMRows, size - p * kBlockMRows) : size;
+      }
+    }
+  }
+  for (int e = threadIdx.x; e <= E; e += blockDim.x) exp_begin[e] = s_pc[s_off[e]];
+}
+
+// Sender: global rank -> slot -> send position; one thread per token (chunked stable rank).
+__global__ void k_ep_send_pos(const int32_t* __restrict__ route, int T, int E, int nch, const int32_t* __restrict__ cc,
+                              EpPlanWs w, int32_t* __restrict__ send_pos) {
+  __shared__ int se[kChunk];
+  const int ch = blockIdx.x;
+  const int t = ch * kChunk + threadIdx.x;
+  const int e = (t < T) ? __ldg(&route[t]) : -1;
+  se[threadIdx.x] = e;
+  __syncthreads();
+  int rin = 0;
+  for (int k = 0; k < (int)threadIdx.x; ++k) rin += (se[k] == e);
+  if (t >= T) return;
+  const int b = w.B[e], c = w.cnt[e];
+  const int grank = b + cc[(size_t)ch * E + e] + rin;
+  const int j = grank % c;
+  const int s = w.off[e] + j;
+  send_pos[t] = w.send_base[s] + (grank / c - runs_before(b, j, c));
+}
+
+// sendbuf[send_pos[t]] = bf16(x[t]); one warp per token.
+__global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32_t* __restrict__ send_pos,
+                          __nv_bfloat16* __restrict__ sendbuf) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * d);
+  uint2* dst = reinterpret_cast<uint2*>(sendbuf + (size_t)send_pos[t] * d);
+  for (int k = lane; k < d / 4; k += 32) {
+    const float4 v = __ldg(&src[k]);
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    dst[k] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
+// Receiver: local row of every received row, per (source, hosted slot) run. grid G.
+__global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ num_slots_p, int rank, EpPlanWs w,
+                              int32_t* __restrict__ recv_of_local) {
+  const int g = blockIdx.x;
+  const int ns = *num_slots_p;
+  for (int s = 0; s < ns; ++s) {
+    if (w.slot_gpu[s] != rank) continue;
+    const int n = w.rows[(size_t)g * max_slots + s];
+    const int r0 = w.recv_start[(size_t)g * max_slots + s], l0 = w.local_start[(size_t)g * max_slots + s];
+    for (int k = threadIdx.x; k < n; k += blockDim.x) recv_of_local[l0 + k] = r0 + k;
+  }
+}
+
+// xperm[row] = buf[idx[row]] for bf16 rows; one warp per row.
+__global__ void k_gather_bf16(const __nv_bfloat16* __restrict__ buf, int n, int d, const int32_t* __restrict__ idx,
+                              __nv_bfloat16* __restrict__ out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)__ldg(&idx[row]) * d);
+  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * d);
+  for (int k = lane; k < d / 8; k += 32) dst[k] = __ldg(&src[k]);
+}
+
+// x[t] += yback[send_pos[t]] (fp32; each token owns one row -> no atomics). one warp per token.
+__global__ void k_ep_combine(float* __restrict__ x, int T, int d, const float* __restrict__ yback,
+                             const int32_t* __restrict__ send_pos) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t >= T) return;
+  float4* dst = reinterpret_cast<float4*>(x + (size_t)t * d);
+  const float4* src = reinterpret_cast<const float4*>(yback + (size_t)send_pos[t] * d);
+  for (int k = lane; k < d / 4; k += 32) {
+    float4 o = dst[k];
+    const float4 v = __ldg(&src[k]);
+    o.x += v.x;
+    o.y += v.y;
+    o.z += v.z;
+    o.w += v.w;
+    dst[k] = o;
+  }
+}
+
+static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+static EpPlanWs carve(void* ws, int G, int E, int max_slots, int32_t** cc, int nch, int32_t** err, int32_t** nslots) {
+  char* p = (char*)ws;
+  auto take = [&](size_t n) {
+    int32_t* r = (int32_t*)p;
+    p += al(sizeof(int32_t) * n);
+    return r;
+  };
+  EpPlanWs w;
+  w.off = take(E + 1);
+  w.cnt = take(E);
+  w.B = take(E);
+  w.slot_gpu = take(max_slots);
+  w.slot_size = take(max_slots);
+  w.rows = take((size_t)G * max_slots);
+  w.send_base = take(max_slots);
+  w.recv_start = take((size_t)G * max_slots);
+  w.local_start = take((size_t)G * max_slots);
+  *cc = take((size_t)nch * E + E);
+  *err = take(1);
+  *nslots = take(1);
+  return w;
+}
+
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" size_t mp_ep_workspace_bytes(int G, int T, int E, int max_slots) {
+  const int nch = cdiv(T > 0 ? T : 1, kChunk);
+  return al(4 * (size_t)(E + 1)) + 2 * al(4 * (size_t)E) + 3 * al(4 * (size_t)max_slots) +
+         3 * al(4 * (size_t)G * max_slots) + al(4 * ((size_t)nch * E + E)) + 2 * al(4);
+}
+
+extern "C" int mp_ep_plan(const int32_t* route, int T, const int32_t* C, int G, int E, int rank, int max_slots,
+                          int split_m, int32_t* res, int32_t* send_counts, int32_t* recv_counts,
+                          int32_t* num_local_rows, int32_t* send_pos, int32_t* piece_row, int32_t* piece_rows,
+                          int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(G >= 1 && G <= 32 && rank >= 0 && rank < G && E >= 1 && max_slots >= E && T >= 0, MP_ERR_CONFIG,
+             "mp_ep_plan: bad sizes G=%d rank=%d E=%d", G, rank, E);
+  MP_REQUIRE(ws_bytes >= mp_ep_workspace_bytes(G, T, E, max_slots), MP_ERR_CONFIG, "mp_ep_plan: workspace");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nch = cdiv(T > 0 ? T : 1, kChunk);
+  int32_t *cc, *err, *nslots;
+  EpPlanWs w = carve(ws, G, E, max_slots, &cc, nch, &err, &nslots);
+  const size_t sm = sizeof(int) * ((size_t)E + 1 + 2 * ((size_t)max_slots + 1));
+  MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_ep_plan: E/max_slots too large");
+  static bool configured = false;
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(k_ep_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024)));
+    configured = true;
+  }
+  k_ep_plan<<<1, 1024, sm, st>>>(C, G, E, rank, max_slots, split_m & 1, res, w, send_counts, recv_counts,
+                                 num_local_rows, piece_row, piece_rows, exp_begin, err);
+  if (T > 0) {
+    // local stable ranks (chunk histograms + exclusive scan over chunks)
+    int rc = mp_histogram_ws(route, 1, T, E, cc + (size_t)nch * E, cc, (size_t)nch * E * 4, stream);
+    if (rc) return rc;
+    k_ep_send_pos<<<nch, kChunk, 0, st>>>(route, T, E, nch, cc, w, send_pos);
+  }
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_ep_pack(const float* x, int T, int d, const int32_t* send_pos, void* sendbuf, void* stream) {
+  MP_REQUIRE(d % 8 == 0, MP_ERR_CONFIG, "mp_ep_pack: d %% 8 != 0");
+  if (T > 0) k_ep_pack<<<cdiv(T * 32, 256), 256, 0, (cudaStream_t)stream>>>(x, T, d, send_pos, (__nv_bfloat16*)sendbuf);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, const int32_t* recvbuf_rows_unused,
+                                 int32_t* recv_of_local, void* ws, size_t ws_bytes, void* stream) {
+  (void)recvbuf_rows_unused;
+  const int nch = cdiv(T > 0 ? T : 1, kChunk);
+  int32_t *cc, *err, *nslots;
+  EpPlanWs w = carve(ws, G, E, max_slots, &cc, nch, &err, &nslots);
+  MP_REQUIRE(ws_bytes >= mp_ep_workspace_bytes(G, T, E, max_slots), MP_ERR_CONFIG, "mp_ep_recv_layout: workspace");
+  // number of slots = off[E]
+  k_ep_recv_map<<<G, 256, 0, (cudaStream_t)stream>>>(G, max_slots, w.off + E, rank, w, recv_of_local);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_gather_rows_bf16(const void* buf, int n, int d, const int32_t* idx, void* out, void* stream) {
+  MP_REQUIRE(d % 8 == 0, MP_ERR_CONFIG, "mp_gather_rows_bf16: d %% 8 != 0");
+  if (n > 0)
+    k_gather_bf16<<<cdiv(n * 32, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)buf, n, d, idx,
+                                                                         (__nv_bfloat16*)out);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_ep_combine(float* x, int T, int d, const float* yback, const int32_t* send_pos, void* stream) {
+  MP_REQUIRE(d % 4 == 0, MP_ERR_CONFIG, "mp_ep_combine: d %% 4 != 0");
+  if (T > 0) k_ep_combine<<<cdiv(T * 32, 256), 256, 0, (cudaStream_t)stream>>>(x, T, d, yback, send_pos);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}

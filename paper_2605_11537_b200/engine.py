@@ -174,7 +174,7 @@ class MoEPipeline:
         self.fallback = torch.empty(L, **i32)
         self.num_slots = torch.empty(L, **i32)
         self.route = torch.empty(L, T, **i32)
-        self.max_slots = max(cfg.capacity, E) + E
+        self.max_slots = max(cfg.capacity, E) * 8 + E  # also covers the global (G * C) plan of EP
         self.exec_slot = torch.empty(L, T, **i32)
         self.corrective = torch.empty(L, E, **i32)
         self.exec_slots = torch.empty(L, **i32)
@@ -275,11 +275,67 @@ class MoEPipeline:
             ev[2].record(sp)
         return 3 + 4 + 1 + 1 + 1
 
+    # ------------------------------------------------------------------ expert parallelism
+    def enable_expert_parallel(self, group=None) -> None:
+        """Shard experts' work over the ranks of ``group`` (one process per GPU, NCCL):
+        every rank keeps all weights, routes its own tokens and dispatches them to the GPU
+        hosting their replica (paper_2605_11537_b200/ep.py). Residency is planned from the
+        all-gathered predicted assignments so every rank holds the same state."""
+        import torch.distributed as dist
+
+        from .ep import CudaEpKernels, ExpertParallelMoE
+
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        cfg = self.cfg
+        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.max_slots)
+        self.ep = ExpertParallelMoE(k, cfg.num_layers, cfg.num_experts, group)
+        self.ep.res = self.res  # one residency state for placement and execution
+        GT = self.world * cfg.tokens
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        self.g_assign = torch.empty(cfg.num_layers, GT, **i32)
+        self.g_slot = torch.empty(cfg.num_layers, GT, **i32)
+        self.g_event = torch.empty(cfg.num_layers, GT, **i32)
+        self.ws_gplace_n = _lib.size_query("mp_place_workspace_bytes", cfg.num_layers, GT, cfg.num_experts)
+        self.ws_gplace = torch.empty(self.ws_gplace_n, dtype=torch.uint8, device=self.dev)
+        self.ws_ghist_n = _lib.size_query("mp_histogram_workspace_bytes", cfg.num_layers, GT, cfg.num_experts)
+        self.ws_ghist = torch.empty(self.ws_ghist_n, dtype=torch.uint8, device=self.dev)
+
+    def step_ep(self, x: torch.Tensor, events=None) -> int:
+        import torch.distributed as dist
+
+        cfg, L, T, E = self.cfg, self.cfg.num_layers, self.cfg.tokens, self.cfg.num_experts
+        sp = stream_ptr()
+        n = self.predict(x, sp)
+        parts = list(self.g_assign.view(L, self.world, T).unbind(1))
+        if self.world > 1:
+            gathered = [torch.empty(L, T, dtype=torch.int32, device=self.dev) for _ in range(self.world)]
+            dist.all_gather(gathered, self.assign, group=self.group)
+            for r in range(self.world):
+                parts[r].copy_(gathered[r])
+        else:
+            self.g_assign.copy_(self.assign)
+        GT = self.world * T
+        unit = DISTINCT_ONLY_UNIT if cfg.replication == "off" else cfg.demand_unit
+        _lib.call("mp_histogram_ws", ptr(self.g_assign), L, GT, E, ptr(self.demand), ptr(self.ws_ghist),
+                  self.ws_ghist_n, sp)
+        cap = cfg.capacity * self.world  # global capacity G * C_g (SURVEY §8(e))
+        _lib.call("mp_cap_replicas", ptr(self.demand), L, E, cap, unit, ptr(self.caps), ptr(self.infeasible), sp)
+        _lib.call("mp_place", ptr(self.g_assign), L, GT, E, ptr(self.caps), cap, cap, ptr(self.res), ptr(self.g_slot),
+                  ptr(self.g_event), ptr(self.offloads), ptr(self.fallback), ptr(self.num_slots), ptr(self.ws_gplace),
+                  self.ws_gplace_n, sp)
+        for l in range(L):
+            self.ep.layer(l, x, events[l] if events is not None else None)
+        return n + 7 + L * 12
+
     def step(self, x: torch.Tensor, events=None) -> int:
         """Run one batch on the current stream; x (T, d) fp32 is the residual stream (in/out).
 
         events: optional list (per layer) of 3 CUDA events bracketing GEMM1 / GEMM2.
         Returns the number of kernel launches issued."""
+        if getattr(self, "ep", None) is not None:
+            return self.step_ep(x, events)
         sp = stream_ptr()
         n = self.predict(x, sp)
         n += self.plan_and_place(sp)

@@ -1,0 +1,176 @@
+"""Expert-parallel MoE forward over G ranks (one process per GPU, NCCL), SURVEY.md §8(e).
+
+Tokens are sharded contiguously by position; every GPU holds all expert weights
+(14.5 GB at Switch-base-128 -- far inside 180 GB of HBM), so "placing" a
+replica only decides which GPU *reads* that expert's weights and computes its
+tokens. Per MoE layer, on every rank:
+
+  1. route the local tokens                      (mp_route_top1_ex)
+  2. local expert counts -> all-gather C (G x E)  (mp_histogram_ws + all_gather)
+  3. plan (identical on all ranks): residency + corrective replicas, global
+     stable ranks, replica (e, j) -> GPU (e*G/E + j) mod G, per-peer row counts,
+     send positions, local replica pieces         (mp_ep_plan)
+  4. dispatch: pack bf16 rows by destination, variable all-to-all
+  5. receiver: rows to slot-major global-token order (mp_ep_recv_layout,
+     mp_gather_rows_bf16), grouped expert GEMMs whose GEMM2 epilogue writes the
+     fp32 results straight into receive order (mp_ffn_up/down)
+  6. combine: reverse all-to-all, x[t] += y[send_pos[t]]  (mp_ep_combine)
+
+Because the global ranks, slots, rows and per-row arithmetic are those of the
+single-device path, the output is bit-identical to one GPU running the whole
+batch. The all-to-all byte counts are data dependent, so each layer does one
+small device->host read of the split sizes (the reference's own executor is
+host driven, src/simulator.py:181-208).
+
+The kernel layer is pluggable: ``CudaEpKernels`` (the product) or, in the
+CPU multi-process tests only, a numpy restatement from ``oracle/``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._dev import ptr, stream_ptr
+from .router_oracle import DeviceMoeLayer, route_device
+
+
+@dataclass
+class EpPlan:
+    send_counts: list[int]
+    recv_counts: list[int]
+    n_local: int
+    send_pos: torch.Tensor
+    piece_row: torch.Tensor
+    piece_rows: torch.Tensor
+    exp_begin: torch.Tensor
+
+
+class CudaEpKernels:
+    """Device implementation (libmoempmc.so) of the per-rank EP steps."""
+
+    dispatch_dtype = torch.bfloat16
+
+    def __init__(self, layers: list[DeviceMoeLayer], tokens: int, world: int, rank: int, max_slots: int):
+        self.layers = layers
+        self.T, self.G, self.rank, self.max_slots = tokens, world, rank, max_slots
+        lay = layers[0]
+        self.E, self.d, self.F = lay.E, lay.dp, lay.Fp
+        dev = lay.U.device
+        self.dev = dev
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.pstride = max_slots + (world * tokens + 127) // 128
+        self.cap_rows = world * tokens  # worst case: every token of every rank lands here
+        self.ws_n = _lib.size_query("mp_ep_workspace_bytes", world, tokens, self.E, max_slots)
+        self.ws = torch.empty(self.ws_n, dtype=torch.uint8, device=dev)
+        self.hist_n = _lib.size_query("mp_histogram_workspace_bytes", 1, tokens, self.E)
+        self.hist_ws = torch.empty(max(self.hist_n, 256), dtype=torch.uint8, device=dev)
+        self.ffn_n = _lib.size_query("mp_ffn_workspace_bytes", self.cap_rows, self.d, self.F)
+        self.ffn_ws = torch.empty(self.ffn_n, dtype=torch.uint8, device=dev)
+        self.counts_buf = torch.empty(self.E, **i32)
+        self.sc = torch.empty(world, **i32)
+        self.rc = torch.empty(world, **i32)
+        self.nloc = torch.empty(1, **i32)
+        self.send_pos = torch.empty(tokens, **i32)
+        self.piece_row = torch.empty(self.pstride, **i32)
+        self.piece_rows = torch.empty(self.pstride, **i32)
+        self.exp_begin = torch.empty(self.E + 1, **i32)
+        self.recv_of_local = torch.empty(self.cap_rows, **i32)
+
+    def route(self, x: torch.Tensor, l: int) -> torch.Tensor:
+        return route_device(x, self.layers[l])
+
+    def counts(self, route: torch.Tensor) -> torch.Tensor:
+        _lib.call("mp_histogram_ws", ptr(route), 1, route.shape[0], self.E, ptr(self.counts_buf), ptr(self.hist_ws),
+                  self.hist_n, stream_ptr())
+        return self.counts_buf
+
+    def plan(self, route: torch.Tensor, C: torch.Tensor, res: torch.Tensor) -> EpPlan:
+        T = route.shape[0]
+        _lib.call("mp_ep_plan", ptr(route), T, ptr(C), self.G, self.E, self.rank, self.max_slots, 1, ptr(res),
+                  ptr(self.sc), ptr(self.rc), ptr(self.nloc), ptr(self.send_pos), ptr(self.piece_row),
+                  ptr(self.piece_rows), ptr(self.exp_begin), ptr(self.ws), self.ws_n, stream_ptr())
+        host = torch.cat([self.sc, self.rc, self.nloc]).cpu().tolist()  # one small D2H per layer
+        G = self.G
+        return EpPlan(host[:G], host[G:2 * G], host[2 * G], self.send_pos[:T], self.piece_row, self.piece_rows,
+                      self.exp_begin)
+
+    def pack(self, x: torch.Tensor, plan: EpPlan, n_send: int) -> torch.Tensor:
+        buf = torch.empty(n_send, self.d, dtype=torch.bfloat16, device=self.dev)
+        _lib.call("mp_ep_pack", ptr(x), x.shape[0], self.d, ptr(plan.send_pos), ptr(buf), stream_ptr())
+        return buf
+
+    def expert_ffn(self, recvbuf: torch.Tensor, plan: EpPlan, l: int, ev=None) -> torch.Tensor:
+        n = recvbuf.shape[0]
+        y = torch.zeros(n, self.d, dtype=torch.float32, device=self.dev)
+        if n == 0:
+            return y
+        lay = self.layers[l]
+        _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
+                  ptr(self.recv_of_local), ptr(self.ws), self.ws_n, stream_ptr())
+        # xperm region of the FFN workspace <- received rows in local (slot-major) order
+        _lib.call("mp_gather_rows_bf16", ptr(recvbuf), n, self.d, ptr(self.recv_of_local), ptr(self.ffn_ws),
+                  stream_ptr())
+        sp = stream_ptr()
+        if ev is not None:
+            ev[0].record(sp)
+        _lib.call("mp_ffn_up", n, self.d, self.F, self.E, ptr(lay.U), lay.tiled, ptr(plan.piece_row),
+                  ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
+        if ev is not None:
+            ev[1].record(sp)
+        _lib.call("mp_ffn_down", ptr(y), n, self.d, self.F, self.E, ptr(lay.V), lay.tiled, ptr(self.recv_of_local),
+                  ptr(plan.piece_row), ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
+        if ev is not None:
+            ev[2].record(sp)
+        return y
+
+    def combine(self, x: torch.Tensor, yback: torch.Tensor, plan: EpPlan) -> None:
+        _lib.call("mp_ep_combine", ptr(x), x.shape[0], self.d, ptr(yback), ptr(plan.send_pos), stream_ptr())
+
+
+class ExpertParallelMoE:
+    """The MoE layer stack of one rank; ``forward`` runs all layers on the local token shard."""
+
+    def __init__(self, kernels, num_layers: int, num_experts: int, group=None):
+        self.k = kernels
+        self.group = group
+        self.G = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.L, self.E = num_layers, num_experts
+        # residency state (replicated on every rank, updated identically)
+        self.res = torch.zeros(num_layers, num_experts, dtype=torch.int32, device=getattr(kernels, "dev", "cpu"))
+
+    def _all_gather_counts(self, counts: torch.Tensor) -> torch.Tensor:
+        if self.G == 1:
+            return counts.view(1, -1)
+        parts = [torch.empty_like(counts) for _ in range(self.G)]
+        dist.all_gather(parts, counts, group=self.group)
+        return torch.stack(parts)
+
+    def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> None:
+        if self.G == 1:
+            out.copy_(inp)
+            return
+        dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits, group=self.group)
+
+    def layer(self, l: int, x: torch.Tensor, ev=None) -> torch.Tensor:
+        k = self.k
+        route = k.route(x, l)
+        C = self._all_gather_counts(k.counts(route))
+        plan = k.plan(route, C, self.res[l])
+        sendbuf = k.pack(x, plan, sum(plan.send_counts))
+        recvbuf = torch.empty(sum(plan.recv_counts), x.shape[1], dtype=sendbuf.dtype, device=sendbuf.device)
+        self._a2a(recvbuf, sendbuf, plan.recv_counts, plan.send_counts)
+        y = k.expert_ffn(recvbuf, plan, l, ev) if ev is not None else k.expert_ffn(recvbuf, plan, l)
+        yback = torch.empty(sum(plan.send_counts), x.shape[1], dtype=y.dtype, device=y.device)
+        self._a2a(yback, y, plan.send_counts, plan.recv_counts)
+        k.combine(x, yback, plan)
+        self.last_route = route
+        return x
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        for l in range(self.L):
+            self.layer(l, x)
+        return x
