@@ -360,6 +360,27 @@ class MoEPipeline:
         _lib.call("mp_graph_end", sp, ctypes.byref(ex))
         return StepGraph(ex, n)
 
+    def capture_call(self, fn) -> "StepGraph":
+        """Capture ``fn(sp) -> launches`` on the current stream into a replayable graph."""
+        sp = stream_ptr()
+        _lib.call("mp_graph_begin", sp)
+        try:
+            n = fn(sp)
+        except Exception:
+            ex = ctypes.c_void_p()
+            _lib.load_library().mp_graph_end(sp, ctypes.byref(ex))
+            raise
+        ex = ctypes.c_void_p()
+        _lib.call("mp_graph_end", sp, ctypes.byref(ex))
+        return StepGraph(ex, n)
+
+    def consume(self, x: torch.Tensor, sp: int, events=None) -> int:
+        """Consumer half of a step: plan + place the predicted table, then the MoE layers."""
+        n = self.plan_and_place(sp)
+        for l in range(self.cfg.num_layers):
+            n += self.layer(l, x, sp, events[l] if events is not None else None)
+        return n
+
     # ------------------------------------------------------------------ accounting
     def expert_weight_bytes(self) -> int:
         """bf16 bytes of one expert's U + V (4 d F)."""
@@ -368,6 +389,60 @@ class MoEPipeline:
     def touched_experts(self) -> torch.Tensor:
         """(L,) experts that received tokens in the last step (device)."""
         return (self.exp_begin[:, 1:] > self.exp_begin[:, :-1]).sum(dim=1)
+
+
+class OverlappedPipeline:
+    """The paper's two-actor schedule (Alg. 1 + Alg. 2; reference src/pipeline.py:70-139)
+    on two CUDA streams instead of a producer thread and a FIFO: the hash-table builder
+    (SRU predictor + heads) for batch i+1 runs on its own stream while batch i is planned,
+    placed and forwarded; double-buffered inputs/assignments, events in place of the queue
+    (queue capacity 1, the reference default src/pipeline.py:35-45). Each half is one
+    CUDA graph. Planning/placement stay in batch order on the consumer stream, so results
+    are identical to the sequential schedule (the reference's mode_equivalence_check)."""
+
+    def __init__(self, pipe: "MoEPipeline", events=None):
+        self.pipe = pipe
+        T, d = pipe.cfg.tokens, pipe.dp
+        dev = pipe.dev
+        self.xbuf = [torch.empty(T, d, device=dev) for _ in range(2)]
+        self.assign = [pipe.assign, torch.empty_like(pipe.assign)]
+        self.sp, self.sf = torch.cuda.Stream(), torch.cuda.Stream()
+        self.pred_ev = [torch.cuda.Event() for _ in range(2)]
+        self.cons_ev = [torch.cuda.Event() for _ in range(2)]
+        self.g_pred, self.g_cons = [], []
+        for j in range(2):  # warm (configures kernel attributes) then capture each half per slot
+            pipe.assign = self.assign[j]
+            with torch.cuda.stream(self.sp):
+                pipe.predict(self.xbuf[j], stream_ptr())
+                self.g_pred.append(pipe.capture_call(lambda sp, j=j: pipe.predict(self.xbuf[j], sp)))
+            with torch.cuda.stream(self.sf):
+                self.g_cons.append(pipe.capture_call(lambda sp, j=j: pipe.consume(self.xbuf[j], sp, events)))
+        pipe.assign = self.assign[0]
+        torch.cuda.synchronize()
+        self.launches = self.g_pred[0].launches + self.g_cons[0].launches
+
+    def run(self, batches, n: int, timer=None) -> None:
+        """Process ``n`` batches (cycled from ``batches`` (T, d) device tensors)."""
+        for i in range(n + 1):
+            if i < n:  # producer: batch i
+                j = i % 2
+                with torch.cuda.stream(self.sp):
+                    if i >= 2:
+                        self.sp.wait_event(self.cons_ev[j])
+                    elif i == 0 and timer is not None:
+                        timer[0].record(self.sp)
+                    self.xbuf[j].copy_(batches[i % len(batches)])
+                    self.g_pred[j].replay()
+                    self.pred_ev[j].record(self.sp)
+            if i >= 1:  # consumer: batch i - 1
+                j = (i - 1) % 2
+                with torch.cuda.stream(self.sf):
+                    self.sf.wait_event(self.pred_ev[j])
+                    self.g_cons[j].replay()
+                    self.cons_ev[j].record(self.sf)
+        if timer is not None:
+            with torch.cuda.stream(self.sf):
+                timer[1].record(self.sf)
 
 
 class DeviceEvent:
