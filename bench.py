@@ -51,7 +51,7 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
-    p.add_argument("--ffn", choices=["fused", "two"], default="two")
+    p.add_argument("--ffn", choices=["two", "mt", "fused"], default="two")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     p.add_argument("--overlap", choices=["on", "off"], default="off",
                    help="predictor of batch i+1 on its own stream during batch i (two-actor pipeline)")
@@ -329,7 +329,9 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {
             "kernel": ("fused grouped expert FFN (k_ffn_fused: GEMM1 relu + GEMM2 scatter-combine, H in L2 ring)"
-                       if args.ffn == "fused" else "grouped expert GEMM pair (GEMM1 relu + GEMM2 scatter-combine)"),
+                       if args.ffn == "fused" else
+                       "grouped expert GEMM pair (GEMM1 relu + GEMM2 scatter-combine"
+                       + (", multi-tile units k_ffn_mt)" if args.ffn == "mt" and args.replication != "off" else ")")),
             "bound": "hbm",
             "achieved": achieved,
             "peak": peaks["hbm_gbs"],

@@ -190,7 +190,11 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
  * time or overlap the grouped GEMMs separately. flags bit 0: u / v are in the pre-tiled
  * layout of mp_tile_kmajor (BN 256 for u, mp_ffn_down_bn(dp) for v); bit 1: CTA-pair
  * (tcgen05 cta_group::2, M = 256) kernels over piece pairs -- pieces must come from a
- * builder called with split_m bit 1 (even piece count per expert), dp % 256 == 0. */
+ * builder called with split_m bit 1 (even piece count per expert), dp % 256 == 0;
+ * bit 2: multi-tile units (two 128 x 256 accumulator tiles per unit: two pieces of one
+ * expert share each weight k-block, or one piece feeds two weight slices) -- pieces of
+ * <= 128 rows (split_m bit 0), Fp % 256 == 0 (up) / dp % 256 == 0 (down), E <= 1024.
+ * Every mode gives bitwise identical results. */
 MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                          size_t ws_bytes, void* stream);
 MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int flags, const int32_t* piece_row,

@@ -11,6 +11,7 @@
 // weight rows (no copies on one GPU).
 #include "epilogues.cuh"
 #include "gemm2_sm100.cuh"
+#include "gemm_mt_sm100.cuh"
 #include "launch.cuh"
 
 #include <algorithm>
@@ -79,17 +80,45 @@ static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, i
   return make_tmap_bf16(tb, w, (uint64_t)E * N, K, K, box_rows);
 }
 
-// flags: bit 0 = pre-tiled weights, bit 1 = CTA-pair (cta_group::2) kernel over paired pieces
+static int mt_single() {  // profiling switch: one tile per unit through the multi-tile kernel
+  static const int v = getenv("MP_MT_SINGLE") != nullptr;
+  return v;
+}
+
+template <class Epi>
+static int launch_ffn_mt(const CUtensorMap& ta, const CUtensorMap& tb, const FfnMtSched& s, const Epi& e,
+                         cudaStream_t st) {
+  auto kern = k_ffn_mt<Epi>;
+  const int smem = MtSmem::kBytes;
+  static bool configured = false;
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  kern<<<num_sms(), kGemmThreads, smem, st>>>(ta, tb, s, e);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+// flags: bit 0 = pre-tiled weights, bit 1 = CTA-pair (cta_group::2) kernel over paired pieces,
+//        bit 2 = multi-tile units (k_ffn_mt: two accumulator tiles per unit sharing A or B)
 static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
                   const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, int flags,
                   cudaStream_t st) {
   // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
-  const int tiled = flags & 1, pair = (flags >> 1) & 1;
+  const int tiled = flags & 1, pair = (flags >> 1) & 1, mt = (flags >> 2) & 1;
   static const bool diag_nostore = getenv("MP_DIAG_NOSTORE") != nullptr;  // profiling switch only
   EpiStoreBf16 e{hid, diag_nostore ? 0 : Fp, nullptr, 1, 0};
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
   if (rc) return rc;
+  if (mt) {
+    MP_REQUIRE(E <= kMtMaxE, MP_ERR_CONFIG, "ffn multi-tile mode: E <= %d", kMtMaxE);
+    rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled, 128);
+    if (rc) return rc;
+    FfnMtSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, dp / 64, Fp, tiled, mt_single()};
+    return launch_ffn_mt(ta, tb, s, e, st);
+  }
   rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled, pair ? 128 : 256);
   if (rc) return rc;
   if (pair) {
@@ -104,11 +133,20 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
                     const __nv_bfloat16* hid, int flags, cudaStream_t st) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
-  const int tiled = flags & 1, pair = (flags >> 1) & 1;
-  const int bn = mp_ffn_down_bn(dp);
+  const int tiled = flags & 1, pair = (flags >> 1) & 1, mt = (flags >> 2) & 1;
+  static const int bn_env = getenv("MP_FFN_DOWN_BN") ? atoi(getenv("MP_FFN_DOWN_BN")) : 0;  // profiling switch
+  const int bn = (bn_env && !tiled && dp % bn_env == 0) ? bn_env : mp_ffn_down_bn(dp);
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
   if (rc) return rc;
+  if (mt) {
+    MP_REQUIRE(bn == 256 && E <= kMtMaxE, MP_ERR_CONFIG, "ffn multi-tile mode: dp %% 256 == 0, E <= %d", kMtMaxE);
+    rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, 128);
+    if (rc) return rc;
+    EpiScatterAdd ea{y, dp, tok_of_row};
+    FfnMtSched s{piece_row, piece_rows, exp_begin, E, dp / 256, Fp / 64, dp, tiled, mt_single()};
+    return launch_ffn_mt(ta, tb, s, ea, st);
+  }
   rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
   if (rc) return rc;
   EpiScatterAdd e{y, dp, tok_of_row};

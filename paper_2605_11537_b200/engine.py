@@ -50,7 +50,8 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
-    ffn: str = "two"              # two (GEMM1 + GEMM2 launches) | fused (experimental: one launch, H in an L2 ring)
+    ffn: str = "two"              # two (single-tile units) | mt (multi-tile units, slower: see DESIGN) |
+                                  # fused (experimental: one launch, H in an L2 ring)
     skew: float = 1.2
     noise: float = 0.1
     seed: int = 0
@@ -245,7 +246,11 @@ class MoEPipeline:
         lay = self.layers[l]
         # the fused FFN needs <= 128-row pieces: replicas longer than a tile are split into
         # consecutive M tiles of the SAME replica (a replica is still one slot)
-        split = 1 if (cfg.replication == "split" or cfg.ffn == "fused") else 0
+        # replication "off" keeps one serial unit per expert (one server per expert, the
+        # paper's baseline); the multi-tile kernel pairs 128-row tiles, so it runs on split
+        # pieces (a replica is still one slot; its tiles are independent GEMM units)
+        use_mt = cfg.ffn == "mt" and cfg.replication != "off" and d % 256 == 0 and E <= 1024
+        split = 1 if (cfg.replication == "split" or cfg.ffn == "fused" or use_mt) else 0
         _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
                   ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
         _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
@@ -265,11 +270,12 @@ class MoEPipeline:
         _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[0].record(sp)
-        _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), lay.tiled, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
+        flags = lay.tiled | (4 if use_mt else 0)
+        _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), flags, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[1].record(sp)
-        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), lay.tiled, ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
+        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags, ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
                   ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[2].record(sp)

@@ -272,6 +272,53 @@ def test_cta_pair_ffn_matches_single_cta(dev, split):
     assert torch.equal(y1, y2)
 
 
+@pytest.mark.parametrize("skew,d,F,tiled", [(0.0, 256, 768, 1), (1.2, 512, 512, 1), (3.0, 768, 1280, 0),
+                                             (1.2, 256, 256, 0), (8.0, 512, 768, 1)])
+def test_multi_tile_ffn_matches_single_tile(dev, skew, d, F, tiled):
+    """Multi-tile units (two accumulator tiles sharing A or B) == the single-tile kernels, bit for bit:
+    odd and even piece counts per expert, odd slice counts, empty experts, both weight layouts."""
+    rng = np.random.default_rng(int(skew * 10) + d + F)
+    T, E = 5000, 21
+    p = 1.0 / (np.arange(E) + 1.0) ** skew
+    p[E // 2] = 0.0  # an expert with no tokens
+    route = torch.from_numpy(rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)).to(dev)
+    slot_expert = torch.arange(E, dtype=torch.int32, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
+    sws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    pn = E + (T + 127) // 128
+    tor = torch.empty(T, **i32)
+    prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
+    _lib.call("mp_segments_from_slots", ptr(route), ptr(slot_expert), T, E, E, 1, ptr(tor), ptr(prow), ptr(prows),
+              ptr(eb), ptr(sws), nb, stream_ptr())
+    U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
+    V = (torch.randn(E * d, F, device=dev) / 28).bfloat16()
+    if tiled:
+        Ut, Vt = torch.empty_like(U), torch.empty_like(V)
+        _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
+        _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, 256, stream_ptr())
+    else:
+        Ut, Vt = U, V
+    x = torch.randn(T, d, device=dev)
+    fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+    ws = torch.empty(fb, dtype=torch.uint8, device=dev)
+    y1 = x.clone()
+    _lib.call("mp_moe_ffn", ptr(x), ptr(y1), T, d, F, E, ptr(U), ptr(V), ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+              ptr(ws), fb, stream_ptr())
+    h0 = (T * d * 2 + 255) // 256 * 256  # hidden buffer offset in the FFN workspace
+    h1 = ws[h0:h0 + T * F * 2].clone()
+    y2 = x.clone()
+    ws.zero_()
+    _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
+    _lib.call("mp_ffn_up", T, d, F, E, ptr(Ut), tiled | 4, ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb, stream_ptr())
+    h2 = ws[h0:h0 + T * F * 2].clone()
+    _lib.call("mp_ffn_down", ptr(y2), T, d, F, E, ptr(Vt), tiled | 4, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+              ptr(ws), fb, stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h2)
+    assert torch.equal(y1, y2)
+
+
 @pytest.mark.parametrize("skew", [0.0, 1.2, 3.0])
 def test_fused_interleaved_ffn_matches_two_launch(dev, skew):
     """Fused GEMM1/GEMM2 launch with the L2 ring for H == the two-launch path, bit for bit."""

@@ -1,0 +1,57 @@
+"""A/B one grouped GEMM (up or down) between FFN kernel flags on a fixed routing -- for ncu captures.
+
+usage: python tools/ffn_ab.py {up|down} {balanced|zipf} FLAGS [FLAGS ...]
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2605_11537_b200 import _lib  # noqa: E402
+from paper_2605_11537_b200._dev import ptr, require_device, stream_ptr  # noqa: E402
+from tools.gemm_probe import timeit  # noqa: E402
+
+
+def main():
+    which, case, flags = sys.argv[1], sys.argv[2], [int(f) for f in sys.argv[3:] if not f.startswith("--")]
+    dev = require_device()
+    T, E, d, F = 16384, 128, 768, 3072
+    U = (torch.randn(E * F, d, device=dev) / 30).bfloat16()
+    V = (torch.randn(E * d, F, device=dev) / 55).bfloat16()
+    U0, V0 = U.clone(), V.clone()
+    _lib.call("mp_tile_kmajor", ptr(U0), ptr(U), E, F, d, 256, stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(V0), ptr(V), E, d, F, 256, stream_ptr())
+    x = torch.randn(T, d, device=dev)
+    rng = np.random.default_rng(0)
+    w = 1.0 / (rng.permutation(E) + 1.0) ** 1.2
+    route = np.repeat(np.arange(E), T // E) if case == "balanced" else rng.choice(E, size=T, p=w / w.sum())
+    r = torch.from_numpy(route.astype(np.int32)).to(dev)
+    se = torch.arange(E, dtype=torch.int32, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    tor = torch.empty(T, **i32)
+    pn = 2 * (E + T // 128 + 1)
+    prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
+    nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
+    sws = torch.empty(nb, dtype=torch.uint8, device=dev)
+    _lib.call("mp_segments_from_slots", ptr(r), ptr(se), T, E, E, 1, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+              ptr(sws), nb, stream_ptr())
+    fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+    ws = torch.empty(fb, dtype=torch.uint8, device=dev)
+    _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
+    y = x.clone()
+    for fl in flags:
+        def run():
+            if which == "up":
+                _lib.call("mp_ffn_up", T, d, F, E, ptr(U if fl & 1 else U0), fl, ptr(prow), ptr(prows), ptr(eb),
+                          ptr(ws), fb, stream_ptr())
+            else:
+                _lib.call("mp_ffn_down", ptr(y), T, d, F, E, ptr(V if fl & 1 else V0), fl, ptr(tor), ptr(prow),
+                          ptr(prows), ptr(eb), ptr(ws), fb, stream_ptr())
+        print(f"{which} {case} flags={fl}: {timeit(run, iters=10):.1f} us", flush=True)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()

@@ -38,7 +38,9 @@ def main():
         prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
         nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
         sws = torch.empty(nb, dtype=torch.uint8, device=dev)
-        for tiled, (u, v) in ((1, (Ut, Vt)), (3, (Ut, Vt))):
+        for tiled, (u, v) in ((1, (Ut, Vt)), (3, (Ut, Vt)), (5, (Ut, Vt))):
+            if tiled == 5 and not split:
+                continue
             pn = 2 * (E + T // 128 + 1)
             prow, prows = torch.empty(pn, **i32), torch.empty(pn, **i32)
             _lib.call("mp_segments_from_slots", ptr(r), ptr(se), T, E, E, split | (tiled & 2), ptr(tor), ptr(prow),
