@@ -82,6 +82,24 @@ __device__ inline int block_exclusive_scan(int* a, int n, int* red /* >= 33 ints
   return total;
 }
 
+// Router workspace (mp_router_workspace_bytes): [xhl: T x 2d bf16][xb: T f32][count + list: T+1 i32][wabs: d f32]
+struct RouterWs {
+  void* xhl;
+  float* xb;
+  int32_t* count;
+  int32_t* list;
+  static size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+  RouterWs(void* ws, int T, int d) {
+    char* p = (char*)ws;
+    xhl = p;
+    p += al((size_t)2 * T * 2 * d);
+    xb = (float*)p;
+    p += al(sizeof(float) * (size_t)T);
+    count = (int32_t*)p;
+    list = count + 1;
+  }
+};
+
 }  // namespace mp
 
 #define MP_CUDA_TRY(expr)                                                                  \

@@ -98,38 +98,50 @@ extern "C" int mp_router_weight_absmax(const float* w_f32, int E, int d, float* 
   return MP_OK;
 }
 
-extern "C" int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
-                                const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
-                                void* stream) {
-  MP_REQUIRE(T >= 1 && d % 64 == 0 && ldx >= d && ldx % 2 == 0, MP_ERR_CONFIG, "mp_route_top1: bad T/d/ldx");
-  MP_REQUIRE(E >= 1 && E <= Eg && (Eg == 64 || Eg == 128 || Eg == 256), MP_ERR_CONFIG,
-             "mp_route_top1: E=%d needs Eg in {64,128,256} >= E", E);
-  MP_REQUIRE(ws_bytes >= mp_router_workspace_bytes(T, d), MP_ERR_CONFIG, "mp_route_top1: workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
-  char* p = (char*)ws;
-  __nv_bfloat16* xhl = (__nv_bfloat16*)p;
-  p += al(sizeof(__nv_bfloat16) * (size_t)T * 2 * d);
-  float* xb = (float*)p;
-  p += al(sizeof(float) * (size_t)T);
-  int32_t* cnt = (int32_t*)p;
-  int32_t* list = cnt + 1;
-  k_router_prep<<<cdiv(T * 32, 256), 256, 0, st>>>(x, ldx, T, d, w_abs, xhl, xb, cnt);
+static int route_gemm(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32, int E, int Eg,
+                      int32_t* route, const RouterWs& rw, float eps, cudaStream_t st) {
   CUtensorMap ta, tb;
-  int rc = make_tmap_bf16(&ta, xhl, T, 2 * d, 2 * d, kBlockM);
+  int rc = make_tmap_bf16(&ta, rw.xhl, T, 2 * d, 2 * d, kBlockM);
   if (rc) return rc;
   rc = make_tmap_bf16(&tb, w_hl, Eg, 2 * d, 2 * d, Eg);
   if (rc) return rc;
   Split3Sched s{T, 1, d / 64, Eg, d};
-  EpiRouterTop1 e{route, xb, kRouterEps, E, cnt, list};
+  EpiRouterTop1 e{route, rw.xb, eps, E, rw.count, rw.list};
   const int units = cdiv(T, kBlockM);
   const int grid = units < num_sms() ? units : num_sms();
   if (Eg == 256) rc = launch_gemm<256, 4>(ta, tb, s, e, grid, st);
   else if (Eg == 128) rc = launch_gemm<128, 6>(ta, tb, s, e, grid, st);
   else rc = launch_gemm<64, 8>(ta, tb, s, e, grid, st);
   if (rc) return rc;
-  k_router_recheck<<<num_sms(), 256, 0, st>>>(x, ldx, d, w_f32, E, cnt, list, route);
+  k_router_recheck<<<num_sms(), 256, 0, st>>>(x, ldx, d, w_f32, E, rw.count, rw.list, route);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
+}
+
+#define ROUTER_CHECKS()                                                                                          \
+  MP_REQUIRE(T >= 1 && d % 64 == 0 && ldx >= d && ldx % 2 == 0, MP_ERR_CONFIG, "mp_route_top1: bad T/d/ldx");     \
+  MP_REQUIRE(E >= 1 && E <= Eg && (Eg == 64 || Eg == 128 || Eg == 256), MP_ERR_CONFIG,                          \
+             "mp_route_top1: E=%d needs Eg in {64,128,256} >= E", E);                                          \
+  MP_REQUIRE(ws_bytes >= mp_router_workspace_bytes(T, d), MP_ERR_CONFIG, "mp_route_top1: workspace too small");
+
+extern "C" int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
+                                const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
+                                void* stream) {
+  ROUTER_CHECKS();
+  cudaStream_t st = (cudaStream_t)stream;
+  const RouterWs rw(ws, T, d);
+  k_router_prep<<<cdiv(T * 32, 256), 256, 0, st>>>(x, ldx, T, d, w_abs, (__nv_bfloat16*)rw.xhl, rw.xb, rw.count);
+  return route_gemm(x, ldx, T, d, w_hl, w_f32, E, Eg, route, rw, kRouterEps, st);
+}
+
+extern "C" int mp_route_top1_prepared(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
+                                      int E, int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream) {
+  ROUTER_CHECKS();
+  // xhl / xb were produced by the previous layer's mp_ffn_down_router epilogue (xb summed
+  // by atomics in arbitrary order: 1e-4 relative slack on the bound); count was reset
+  // by mp_ffn_gather_split.
+  return route_gemm(x, ldx, T, d, w_hl, w_f32, E, Eg, route, RouterWs(ws, T, d), kRouterEps * 1.0001f,
+                    (cudaStream_t)stream);
 }
 
 extern "C" int mp_route_top1(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32, int E,
