@@ -52,7 +52,6 @@ def parse_args():
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
     p.add_argument("--ffn", choices=["two", "mt", "fused"], default="two")
-    p.add_argument("--chain-router", type=int, default=1, help="GEMM2 epilogue prepares the next router input")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     p.add_argument("--overlap", choices=["on", "off"], default="off",
                    help="predictor of batch i+1 on its own stream during batch i (two-actor pipeline)")
@@ -215,8 +214,7 @@ def run_ours(args):
 
     cfg = PipelineConfig(num_layers=args.layers, num_experts=args.experts, tokens=args.tokens,
                          capacity=args.capacity, demand_unit=args.demand_unit, replication=args.replication,
-                         predictor=args.predictor, ffn=args.ffn, chain_router=bool(args.chain_router),
-                         seed=args.seed + rank)
+                         predictor=args.predictor, ffn=args.ffn, seed=args.seed + rank)
     pipe = MoEPipeline(cfg)
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
     ep = world > 1 or args.ep

@@ -170,11 +170,6 @@ MP_API int mp_router_weight_absmax(const float* w_f32, int E, int d, float* w_ab
 MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
                             const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
                             void* stream);
-/* Layer-chained form (same result): the split operand and bound scale already sit in `ws`,
- * written by the previous layer's mp_ffn_down_router, and the recheck counter was reset by
- * mp_ffn_gather_split -- the split/scale pre-pass over x is skipped. */
-MP_API int mp_route_top1_prepared(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
-                                  int E, int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ K6 gather + K7 + K8
  * One MoE layer's expert FFNs over replica segments, fused with the ungated
@@ -208,17 +203,6 @@ MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, in
                        const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
                        size_t ws_bytes, void* stream);
 MP_API int mp_ffn_down_bn(int dp);
-/* Layer chaining with the router (d == dp): mp_ffn_gather_split gathers the bf16 rows from
- * the router workspace (its hi half is bf16(x)) and resets the router's accumulators;
- * mp_ffn_down_router is mp_ffn_down (flags bit 0 only) whose epilogue also writes the next
- * layer's router operand and bound scale (w_abs_next = that router's max_e |w_ek|) for
- * the rows it finalises. */
-MP_API int mp_ffn_gather_split(void* router_ws, size_t router_ws_bytes, int T, int dp, int Fp, int E,
-                               const int32_t* tok_of_row, void* ws, size_t ws_bytes, void* stream);
-MP_API int mp_ffn_down_router(float* y, int T, int dp, int Fp, int E, const void* v, int flags,
-                              const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
-                              const int32_t* exp_begin, void* ws, size_t ws_bytes, void* router_ws,
-                              size_t router_ws_bytes, const float* w_abs_next, void* stream);
 /* One MoE layer's FFN as ONE persistent launch (after a gather): GEMM1 and GEMM2 units
  * of every piece interleaved, the hidden activations living in an L2-resident ring of
  * 128-row slots (never a T x F HBM buffer), device-side completion counters ordering

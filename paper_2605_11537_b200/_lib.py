@@ -56,15 +56,12 @@ SIGNATURES: dict[str, tuple] = {
     "mp_route_top1": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _Z, _P]),
     "mp_router_weight_absmax": (_I, [_P, _I, _I, _P, _P]),
     "mp_route_top1_ex": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
-    "mp_route_top1_prepared": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _P, _P, _Z, _P]),
     "mp_ffn_workspace_bytes": (_Z, [_I, _I, _I]),
     "mp_moe_ffn": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_gather": (_I, [_P, _I, _I, _I, _I, _P, _P, _Z, _P]),
     "mp_ffn_up": (_I, [_I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down_bn": (_I, [_I]),
-    "mp_ffn_gather_split": (_I, [_P, _Z, _I, _I, _I, _I, _P, _P, _Z, _P]),
-    "mp_ffn_down_router": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P, _Z, _P, _P]),
     "mp_ffn_fused_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "mp_ffn_fused": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _Z, _P]),
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),

@@ -161,7 +161,19 @@ struct EpiScatterAdd {
     const int tok = ok ? __ldg(&tok_of_row[U.a_row + rr]) : -1;
     float* base = x + U.n0 + c0;
     float4* srow = reinterpret_cast<float4*>(scratch + lane * 20);
+    const int pq = lane & 3;
+    int tt[4];  // token of the row this lane updates in store step `it`
+#pragma unroll
+    for (int it = 0; it < 4; ++it) tt[it] = __shfl_sync(0xffffffffu, tok, it * 8 + (lane >> 2));
     tmem_chunks<NC>(taddr, [&](int c, float* v) {
+      // all 8 residual reads of the chunk are issued up front (independent rows): one
+      // memory latency per chunk instead of one per row group
+      float4 o[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int it = 0; it < 4; ++it)
+          if (tt[it] >= 0) o[h][it] = *(reinterpret_cast<const float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq);
       // two 16-column halves: lane = row -> smem, then 8 rows x 64 B per instruction
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -171,101 +183,20 @@ struct EpiScatterAdd {
         __syncwarp();
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
-          const int row = it * 8 + (lane >> 2), part = lane & 3;
-          const int t = __shfl_sync(0xffffffffu, tok, row);
-          const float4 a = *reinterpret_cast<const float4*>(scratch + row * 20 + part * 4);
-          if (t >= 0) {
-            float4* dst = reinterpret_cast<float4*>(base + (size_t)t * ldx + c + 16 * h) + part;
-            float4 o = *dst;
-            o.x += a.x;
-            o.y += a.y;
-            o.z += a.z;
-            o.w += a.w;
-            *dst = o;
-          }
-        }
-        __syncwarp();
-      }
-    });
-  }
-};
-
-// GEMM2 epilogue that also emits the NEXT layer's router inputs for the rows it
-// finalises (replaces k_router_prep for layers >= 1):
-//   xhl[t] = [bf16(x_t) | bf16(x_t - bf16(x_t))]        (split-bf16 router operand)
-//   xb[t] += sum_{k in tile} |x_tk| * wabs[k]            (certification scale)
-// xb is accumulated with fp32 atomics over the column slices (zeroed by
-// mp_ffn_gather_split); it only scales the router's error bound, which the
-// consumer inflates by 1e-4 relative, so the summation order cannot matter.
-struct EpiScatterAddSplit {
-  static constexpr bool kSplitCols = true;
-  float* x;  // T x ldx fp32 residual stream (updated in place)
-  int ldx;
-  const int32_t* tok_of_row;
-  __nv_bfloat16* xhl;  // T x 2d
-  int d;
-  float* xb;           // T
-  const float* wabs;   // d: max_e |w_ek| of the next layer's router
-  __device__ __forceinline__ const float* colvec() const { return nullptr; }
-  template <int NC>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float*,
-                                      uint32_t* scratch) const {
-    const int lane = threadIdx.x & 31;
-    const int rr = mt * kBlockM + r;
-    const bool ok = rr < U.rows;
-    const int tok = ok ? __ldg(&tok_of_row[U.a_row + rr]) : -1;
-    const int col0 = U.n0 + c0;
-    float* base = x + col0;
-    float4* srow = reinterpret_cast<float4*>(scratch + lane * 20);
-    float part[4] = {0.f, 0.f, 0.f, 0.f};
-    tmem_chunks<NC>(taddr, [&](int c, float* v) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          srow[q] = make_float4(v[16 * h + 4 * q], v[16 * h + 4 * q + 1], v[16 * h + 4 * q + 2], v[16 * h + 4 * q + 3]);
-        __syncwarp();
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int row = it * 8 + (lane >> 2), pq = lane & 3;
-          const int t = __shfl_sync(0xffffffffu, tok, row);
+          const int row = it * 8 + (lane >> 2);
           const float4 a = *reinterpret_cast<const float4*>(scratch + row * 20 + pq * 4);
-          if (t >= 0) {
-            const int col = c + 16 * h + 4 * pq;  // tile-relative column of this lane's 4 values
-            float4* dst = reinterpret_cast<float4*>(base + (size_t)t * ldx + col);
-            float4 o = *dst;
-            o.x += a.x;
-            o.y += a.y;
-            o.z += a.z;
-            o.w += a.w;
-            *dst = o;
-            const __nv_bfloat162 h01 = __floats2bfloat162_rn(o.x, o.y), h23 = __floats2bfloat162_rn(o.z, o.w);
-            const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
-            const __nv_bfloat162 l01 = __floats2bfloat162_rn(o.x - f01.x, o.y - f01.y);
-            const __nv_bfloat162 l23 = __floats2bfloat162_rn(o.z - f23.x, o.w - f23.y);
-            __nv_bfloat16* xr = xhl + (size_t)t * 2 * d + col0 + col;
-            uint2 hw, lw;
-            hw.x = *reinterpret_cast<const uint32_t*>(&h01);
-            hw.y = *reinterpret_cast<const uint32_t*>(&h23);
-            lw.x = *reinterpret_cast<const uint32_t*>(&l01);
-            lw.y = *reinterpret_cast<const uint32_t*>(&l23);
-            *reinterpret_cast<uint2*>(xr) = hw;
-            *reinterpret_cast<uint2*>(xr + d) = lw;
-            const float4 w = __ldg(reinterpret_cast<const float4*>(wabs + col0 + col));
-            part[it] += fabsf(o.x) * w.x + fabsf(o.y) * w.y + fabsf(o.z) * w.z + fabsf(o.w) * w.w;
+          if (tt[it] >= 0) {
+            float4 r = o[h][it];
+            r.x += a.x;
+            r.y += a.y;
+            r.z += a.z;
+            r.w += a.w;
+            *(reinterpret_cast<float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq) = r;
           }
         }
         __syncwarp();
       }
     });
-#pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      float s = part[it];
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      const int t = __shfl_sync(0xffffffffu, tok, it * 8 + (lane >> 2));
-      if ((lane & 3) == 0 && t >= 0) atomicAdd(&xb[t], s);
-    }
   }
 };
 

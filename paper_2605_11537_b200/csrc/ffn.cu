@@ -39,23 +39,6 @@ __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const 
   }
 }
 
-// xperm[row] = xhl[tok_of_row[row]][0:d) (the bf16 "hi" half IS bf16(x)); also zeroes the
-// router scale accumulators xb (by row index: covers all T) and the recheck count for
-// the next layer. One warp per row, 16-byte lanes.
-__global__ void k_gather_split(const __nv_bfloat16* __restrict__ xhl, int T, int d,
-                               const int32_t* __restrict__ tok_of_row, __nv_bfloat16* __restrict__ xperm,
-                               float* __restrict__ xb, int32_t* __restrict__ count) {
-  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count = 0;
-  if (row >= T) return;
-  const int t = __ldg(&tok_of_row[row]);
-  const uint4* src = reinterpret_cast<const uint4*>(xhl + (size_t)t * 2 * d);
-  uint4* dst = reinterpret_cast<uint4*>(xperm + (size_t)row * d);
-  for (int k = lane; k < d / 8; k += 32) dst[k] = __ldg(&src[k]);
-  if (lane == 0) xb[row] = 0.f;
-}
-
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 // dst[g][nt][kb][r][c] = src[g*N + nt*BN + r][kb*64 + c], 16-byte granules.
@@ -148,8 +131,7 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
 
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
-                    const __nv_bfloat16* hid, int flags, cudaStream_t st, const RouterWs* rw = nullptr,
-                    const float* wabs = nullptr) {
+                    const __nv_bfloat16* hid, int flags, cudaStream_t st) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
   const int tiled = flags & 1, pair = (flags >> 1) & 1, mt = (flags >> 2) & 1;
   const int bn = mp_ffn_down_bn(dp);
@@ -173,12 +155,6 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
     return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
   }
   SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
-  if (rw) {  // the epilogue also emits the next layer's router inputs
-    EpiScatterAddSplit es{y, dp, tok_of_row, (__nv_bfloat16*)rw->xhl, dp, rw->xb, wabs};
-    if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, es, num_sms(), st);
-    if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, es, num_sms(), st);
-    return launch_gemm<64, 8>(ta, tb, s, es, num_sms(), st);
-  }
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, num_sms(), st);
   return launch_gemm<64, 8>(ta, tb, s, e, num_sms(), st);
@@ -215,31 +191,6 @@ extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v
   FFN_CHECKS();
   return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags,
                   (cudaStream_t)stream);
-}
-
-extern "C" size_t mp_router_workspace_bytes(int T, int d);
-
-extern "C" int mp_ffn_gather_split(void* router_ws, size_t router_ws_bytes, int T, int dp, int Fp, int E,
-                                   const int32_t* tok_of_row, void* ws, size_t ws_bytes, void* stream) {
-  FFN_CHECKS();
-  MP_REQUIRE(router_ws_bytes >= mp_router_workspace_bytes(T, dp), MP_ERR_CONFIG, "ffn: router workspace too small");
-  const RouterWs rw(router_ws, T, dp);
-  k_gather_split<<<cdiv(T * 32, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)rw.xhl, T, dp, tok_of_row,
-                                                                       xperm, rw.xb, rw.count);
-  MP_CUDA_TRY(cudaGetLastError());
-  return MP_OK;
-}
-
-extern "C" int mp_ffn_down_router(float* y, int T, int dp, int Fp, int E, const void* v, int flags,
-                                  const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
-                                  const int32_t* exp_begin, void* ws, size_t ws_bytes, void* router_ws,
-                                  size_t router_ws_bytes, const float* w_abs_next, void* stream) {
-  FFN_CHECKS();
-  MP_REQUIRE(router_ws_bytes >= mp_router_workspace_bytes(T, dp), MP_ERR_CONFIG, "ffn: router workspace too small");
-  MP_REQUIRE(!(flags & 6), MP_ERR_CONFIG, "mp_ffn_down_router: single-tile 1-CTA kernel only (flags bit 0)");
-  const RouterWs rw(router_ws, T, dp);
-  return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags, (cudaStream_t)stream,
-                  &rw, w_abs_next);
 }
 
 extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,

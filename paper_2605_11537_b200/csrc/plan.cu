@@ -16,7 +16,14 @@
 // built deterministically (no atomics decide order): per-128-token chunk
 // counts -> per-expert exclusive scan over chunks -> in-chunk rank by a
 // shared-memory broadcast compare.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mp {
 
@@ -261,19 +268,16 @@ __device__ inline void emit_pieces(int32_t* pr, int32_t* pn, int p0, int np, int
 
 // Execution map per layer (src/simulator.py:185-203) + slot rows + GEMM pieces.
 // grid L, block 1024. smem: s_off[E+1] s_n[E] s_row[MS+1] s_pc[MS+1]
-__global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_slots, int split_m,
-                             int32_t* __restrict__ res, int32_t* __restrict__ corrective,
-                             int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
-                             int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
-                             int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin, int pieces_stride,
-                             int32_t* __restrict__ err) {
-  extern __shared__ int sm[];
-  __shared__ int red[40];
+__device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* __restrict__ demand, int E, int max_slots,
+                                int split_m, int32_t* __restrict__ res, int32_t* __restrict__ corrective,
+                                int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
+                                int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
+                                int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin, int pieces_stride,
+                                int32_t* __restrict__ err) {
   int* s_off = sm;              // E + 1
   int* s_n = s_off + E + 1;     // E
   int* s_row = s_n + E;         // max_slots + 1
   int* s_pc = s_row + max_slots + 1;
-  const int l = blockIdx.x;
   const size_t b = (size_t)l * E;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     const int n = demand[b + e], rp = res[b + e];
@@ -333,12 +337,22 @@ __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_
   }
 }
 
-__global__ void k_exec_rank(const int32_t* __restrict__ route, int T, int E, int nch, int max_slots,
-                            const int32_t* __restrict__ cc, const int32_t* __restrict__ off_g,
-                            const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ token_to_slot,
-                            int32_t* __restrict__ row_of_token, int32_t* __restrict__ tok_of_row) {
-  __shared__ int se[kChunk];
-  const int l = blockIdx.y, ch = blockIdx.x;
+__global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_slots, int split_m,
+                             int32_t* __restrict__ res, int32_t* __restrict__ corrective,
+                             int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
+                             int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
+                             int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin, int pieces_stride,
+                             int32_t* __restrict__ err) {
+  extern __shared__ int sm[];
+  __shared__ int red[40];
+  exec_layer_body(blockIdx.x, sm, red, demand, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
+                  piece_row, piece_rows, exp_begin, pieces_stride, err);
+}
+
+__device__ void exec_rank_body(int l, int ch, int* se, const int32_t* __restrict__ route, int T, int E, int nch,
+                               int max_slots, const int32_t* __restrict__ cc, const int32_t* __restrict__ off_g,
+                               const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ token_to_slot,
+                               int32_t* __restrict__ row_of_token, int32_t* __restrict__ tok_of_row) {
   int e;
   const int rin = chunk_rank(route, T, l, ch, se, &e);
   const int t = ch * kChunk + threadIdx.x;
@@ -351,6 +365,64 @@ __global__ void k_exec_rank(const int32_t* __restrict__ route, int T, int E, int
   token_to_slot[(size_t)l * T + t] = s;
   if (row_of_token) row_of_token[(size_t)l * T + t] = row;
   tok_of_row[(size_t)l * T + row] = t;
+}
+
+__global__ void k_exec_rank(const int32_t* __restrict__ route, int T, int E, int nch, int max_slots,
+                            const int32_t* __restrict__ cc, const int32_t* __restrict__ off_g,
+                            const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ token_to_slot,
+                            int32_t* __restrict__ row_of_token, int32_t* __restrict__ tok_of_row) {
+  __shared__ int se[kChunk];
+  exec_rank_body(blockIdx.y, blockIdx.x, se, route, T, E, nch, max_slots, cc, off_g, slot_row_g, token_to_slot,
+                 row_of_token, tok_of_row);
+}
+
+// The whole execution map of mp_exec_map as ONE cooperative launch (grid (nch, L),
+// block kChunk, all blocks co-resident): chunk histograms | per-(layer, expert)
+// exclusive scans over chunks (one expert per block) | slot/piece layout (block
+// (0, l)) | stable ranks, separated by grid-wide barriers. Same arithmetic as the
+// four-kernel form, one launch instead of four.
+__global__ void k_exec_fused(const int32_t* __restrict__ route, int T, int E, int nch, int max_slots, int split_m,
+                             int32_t* __restrict__ cc, int32_t* __restrict__ demand, int32_t* __restrict__ res,
+                             int32_t* __restrict__ corrective, int32_t* __restrict__ num_slots,
+                             int32_t* __restrict__ off_g, int32_t* __restrict__ slot_row_g,
+                             int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
+                             int32_t* __restrict__ exp_begin, int pieces_stride, int32_t* __restrict__ err,
+                             int32_t* __restrict__ token_to_slot, int32_t* __restrict__ row_of_token,
+                             int32_t* __restrict__ tok_of_row) {
+  extern __shared__ int sm[];
+  __shared__ int red[40];
+  cg::grid_group grid = cg::this_grid();
+  const int l = blockIdx.y, ch = blockIdx.x;
+  // 1. chunk histogram
+  for (int e = threadIdx.x; e < E; e += blockDim.x) sm[e] = 0;
+  __syncthreads();
+  {
+    const int t = ch * kChunk + threadIdx.x;
+    if (t < T) atomicAdd(&sm[__ldg(&route[(size_t)l * T + t])], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cc[((size_t)l * nch + ch) * E + e] = sm[e];
+  grid.sync();
+  // 2. per-expert exclusive scan over chunks (experts ch, ch + nch, ... of layer l)
+  for (int e = ch; e < E; e += nch) {
+    int32_t* col = cc + (size_t)l * nch * E + e;
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) sm[c] = col[(size_t)c * E];
+    __syncthreads();
+    const int total = block_exclusive_scan(sm, nch, red);
+    for (int c = threadIdx.x; c < nch; c += blockDim.x) col[(size_t)c * E] = sm[c];
+    if (threadIdx.x == 0) demand[(size_t)l * E + e] = total;
+    __syncthreads();
+  }
+  grid.sync();
+  // 3. slots, rows and GEMM pieces of layer l
+  if (ch == 0)
+    exec_layer_body(l, sm, red, demand, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
+                    piece_row, piece_rows, exp_begin, pieces_stride, err);
+  grid.sync();
+  // 4. stable ranks -> slot, row, permutation
+  if (num_slots[l] <= max_slots)
+    exec_rank_body(l, ch, sm, route, T, E, nch, max_slots, cc, off_g, slot_row_g, token_to_slot, row_of_token,
+                   tok_of_row);
 }
 
 // Segments from an explicit token -> slot map. grid 1, block 1024.
@@ -549,9 +621,31 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
   const size_t sm_h = sizeof(int) * (size_t)E;
   const size_t sm_x = sizeof(int) * ((size_t)2 * E + 1 + 2 * ((size_t)max_slots + 1));
   MP_REQUIRE(sm_h <= 200 * 1024 && sm_x <= 200 * 1024, MP_ERR_CONFIG, "mp_exec_map: E/max_slots too large");
+  const int pieces_stride = max_slots + cdiv(T, kChunk);
+  static const bool no_fused = getenv("MP_EXEC_UNFUSED") != nullptr;  // A/B switch
+  if (!no_fused) {
+    // one cooperative launch; falls back to the four-kernel form when the grid cannot be co-resident
+    const size_t sm_f = std::max(std::max(sm_h, sm_x), sizeof(int) * (size_t)std::max(nch, kChunk));
+    MP_CUDA_TRY(set_smem((const void*)k_exec_fused, sm_f));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nch, L);
+    cfg.blockDim = dim3(kChunk);
+    cfg.dynamicSmemBytes = sm_f;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t ce = cudaLaunchKernelEx(&cfg, k_exec_fused, route, T, E, nch, max_slots, split_m, cc, dem, res,
+                                              corrective, num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin,
+                                              pieces_stride, err, token_to_slot, row_of_token, tok_of_row);
+    if (ce == cudaSuccess) return MP_OK;
+    if (ce != cudaErrorCooperativeLaunchTooLarge) MP_CUDA_TRY(ce);
+    (void)cudaGetLastError();
+  }
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
-  const int pieces_stride = max_slots + cdiv(T, kChunk);
   k_chunk_hist<<<dim3(nch, L), kChunk, sm_h, st>>>(route, T, E, nch, cc);
   k_chunk_prefix<<<L, 1024, 0, st>>>(cc, nch, E, dem);
   k_exec_layer<<<L, 1024, sm_x, st>>>(dem, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row,

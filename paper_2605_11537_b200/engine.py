@@ -52,7 +52,6 @@ class PipelineConfig:
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
     ffn: str = "two"              # two (single-tile units) | mt (multi-tile units, slower: see DESIGN) |
                                   # fused (experimental: one launch, H in an L2 ring)
-    chain_router: bool = True     # GEMM2 epilogue prepares the next layer's router operand
     skew: float = 1.2
     noise: float = 0.1
     seed: int = 0
@@ -252,18 +251,9 @@ class MoEPipeline:
         # pieces (a replica is still one slot; its tiles are independent GEMM units)
         use_mt = cfg.ffn == "mt" and cfg.replication != "off" and d % 256 == 0 and E <= 1024
         split = 1 if (cfg.replication == "split" or cfg.ffn == "fused" or use_mt) else 0
-        # layer chaining: GEMM2 of layer l writes layer l+1's split router operand and bound
-        # scale in its epilogue, so routing of layers >= 1 skips the pre-pass over x
-        chain = cfg.chain_router and cfg.ffn == "two"
-        n = 0
-        if chain and l > 0:
-            _lib.call("mp_route_top1_prepared", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), E, lay.Eg,
-                      ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
-            n += 2
-        else:
-            _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
-                      ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
-            n += 3
+        _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
+                  ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
+        n = 3  # fused split + GEMM (or pre-pass + GEMM), recheck
         _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
                   ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
                   ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]),
@@ -278,12 +268,7 @@ class MoEPipeline:
                 ev[1].record(sp)
                 ev[2].record(sp)
             return n + 4 + 1 + 1 + 1
-        if chain:
-            _lib.call("mp_ffn_gather_split", ptr(self.ws_router), self.ws_router_n, T, d, F, E, ptr(self.tok_of_row[l]),
-                      ptr(self.ws_ffn), self.ws_ffn_n, sp)
-        else:
-            _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n,
-                      sp)
+        _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[0].record(sp)
         flags = lay.tiled | (4 if use_mt else 0)
@@ -291,14 +276,8 @@ class MoEPipeline:
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[1].record(sp)
-        if chain and l + 1 < cfg.num_layers:
-            _lib.call("mp_ffn_down_router", ptr(x), T, d, F, E, ptr(lay.V), flags, ptr(self.tok_of_row[l]),
-                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn),
-                      self.ws_ffn_n, ptr(self.ws_router), self.ws_router_n, ptr(self.layers[l + 1].w_abs), sp)
-        else:
-            _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags, ptr(self.tok_of_row[l]),
-                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn),
-                      self.ws_ffn_n, sp)
+        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags, ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
+                  ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[2].record(sp)
         return n + 4 + 1 + 1 + 1
