@@ -622,9 +622,10 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
   const size_t sm_x = sizeof(int) * ((size_t)2 * E + 1 + 2 * ((size_t)max_slots + 1));
   MP_REQUIRE(sm_h <= 200 * 1024 && sm_x <= 200 * 1024, MP_ERR_CONFIG, "mp_exec_map: E/max_slots too large");
   const int pieces_stride = max_slots + cdiv(T, kChunk);
-  static const bool no_fused = getenv("MP_EXEC_UNFUSED") != nullptr;  // A/B switch
-  if (!no_fused) {
-    // one cooperative launch; falls back to the four-kernel form when the grid cannot be co-resident
+  // MP_EXEC_FUSED=1: one cooperative launch instead of four (measured equal in a CUDA graph,
+  // so the plain four-kernel form stays the default); falls back when the grid cannot be co-resident
+  static const bool fused = getenv("MP_EXEC_FUSED") != nullptr;
+  if (fused) {
     const size_t sm_f = std::max(std::max(sm_h, sm_x), sizeof(int) * (size_t)std::max(nch, kChunk));
     MP_CUDA_TRY(set_smem((const void*)k_exec_fused, sm_f));
     cudaLaunchConfig_t cfg = {};
