@@ -88,18 +88,25 @@ struct Gemm2Smem {
   static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
   static constexpr int kScratchOffset = kVecOffset + 2 * BN * 4;
   static constexpr int kScratchWordsPerWarp = 32 * 20;
-  static constexpr int kBytes = kScratchOffset + 8 * kScratchWordsPerWarp * 4 + 1024;
+  static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;
+  static constexpr int kBytes = kPrepOffset + 1025 * 4 + 1024;
+};
+
+// What every role needs to know about a cluster work unit.
+struct PairUnit {
+  Unit U;       // this CTA's rows (b_row = tile base, both CTAs)
+  int mtiles;   // M tiles of the unit (same for both CTAs)
+  int peer_mt;  // M tiles that carry rows in the peer CTA
 };
 
 // Scheduler concept (pair form):
 //   int num_units() const;                         // cluster work units
-//   Unit unit(int u, int rank) const;              // this CTA's rows; b_row = tile base (both CTAs)
-//   int mtiles(int u) const;                       // M tiles of the unit (same for both CTAs)
-//   int piece_mtiles(int u, int rank) const;       // M tiles that carry rows in CTA `rank`
+//   PairUnit info(int u, int rank) const;          // decoded once per unit per role (prefetched)
+//   void prepare(int* table);                      // all threads, before the roles start
 //   int num_kb(), a_kcol(kb), b_kcol(kb), b_krow(kb)
 template <int BN, int STAGES, class Sched, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
-    k_umma_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched,
+    k_umma_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched_in,
                  Epi epi) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using L = Gemm2Smem<BN, STAGES>;
@@ -132,6 +139,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
+  Sched sched = sched_in;
+  sched.prepare(reinterpret_cast<int*>(smem + L::kPrepOffset));
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
@@ -147,12 +156,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint64_t pol_b = Sched::kStreamB ? policy_evict_first() : policy_evict_normal();
       const uint64_t pol_a = policy_evict_normal();
       uint32_t stage = 0, phase = 0;
+      PairUnit In = cid < nunits ? sched.info(cid, rank) : PairUnit{};
       for (int u = cid; u < nunits; u += ncl) {
-        const Unit U = sched.unit(u, rank);
-        const int mtiles = sched.mtiles(u);
+        const PairUnit I = In;
+        if (u + ncl < nunits) In = sched.info(u + ncl, rank);  // consumed next iteration
+        const Unit U = I.U;
+        const int mtiles = I.mtiles;
         // M tiles that carry rows in each CTA: padding pieces / shorter pieces skip their A loads
         const int my_mt = (U.rows + kBlockM - 1) / kBlockM;
-        const int peer_mt = sched.piece_mtiles(u, rank ^ 1);
+        const int peer_mt = I.peer_mt;
         for (int mt = 0; mt < mtiles; ++mt) {
           const bool load_a = mt < my_mt;
           const uint32_t tx = 2 * L::kBBytes + L::kABytes * ((load_a ? 1 : 0) + (mt < peer_mt ? 1 : 0));
@@ -177,8 +189,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       // ------------------------------------------------------------ MMA issuer (leader CTA)
       constexpr uint32_t idesc = idesc_bf16_f32(2 * kBlockM, BN);
       uint32_t stage = 0, phase = 0, tile = 0;
+      int mt_next = cid < nunits ? sched.info(cid, rank).mtiles : 0;
       for (int u = cid; u < nunits; u += ncl) {
-        const int mtiles = sched.mtiles(u);
+        const int mtiles = mt_next;
+        if (u + ncl < nunits) mt_next = sched.info(u + ncl, rank).mtiles;
         for (int mt = 0; mt < mtiles; ++mt, ++tile) {
           const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
           mbar_wait(&tempty[as], aph ^ 1);
@@ -214,9 +228,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int c0 = split ? half * (BN / 2) : 0;
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
     uint32_t tile = 0;
+    PairUnit In = cid < nunits ? sched.info(cid, rank) : PairUnit{};
     for (int u = cid; u < nunits; u += ncl) {
-      const Unit U = sched.unit(u, rank);
-      const int mtiles = sched.mtiles(u);
+      const PairUnit I = In;
+      if (u + ncl < nunits) In = sched.info(u + ncl, rank);
+      const Unit U = I.U;
+      const int mtiles = I.mtiles;
       for (int mt = 0; mt < mtiles; ++mt, ++tile) {
         const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
         const float* vec = epi.colvec();
@@ -261,8 +278,10 @@ struct Dense2Sched {
     U.n0 = nb * bn;
     return U;
   }
-  __device__ int mtiles(int) const { return 1; }
-  __device__ int piece_mtiles(int u, int rank) const { return unit(u, rank).rows > 0 ? 1 : 0; }
+  __device__ void prepare(int*) {}
+  __device__ PairUnit info(int u, int rank) const {
+    return PairUnit{unit(u, rank), 1, unit(u, rank ^ 1).rows > 0 ? 1 : 0};
+  }
   __device__ int num_kb() const { return kb; }
   __device__ int a_kcol(int k) const { return k * kBlockK; }
   __device__ int b_kcol(int k) const { return k * kBlockK; }
@@ -277,8 +296,14 @@ struct Seg2Sched {
   const int32_t* exp_begin;  // E + 1, all even
   int E, n_tiles, bn, n_per_expert, kb;
   int b_tiled;
+  __device__ void prepare(int* tab) {
+    if (E + 1 > 1025) return;
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) tab[e] = exp_begin[e];
+    __syncthreads();
+    exp_begin = tab;
+  }
   __device__ int num_units() const { return (exp_begin[E] >> 1) * n_tiles; }
-  __device__ void locate(int u, int& e, int& nt, int& pp) const {
+  __device__ PairUnit info(int u, int rank) const {
     int lo = 0, hi = E;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -286,26 +311,17 @@ struct Seg2Sched {
     }
     const int b = exp_begin[lo] >> 1, cnt = (exp_begin[lo + 1] >> 1) - b;
     const int local = u - b * n_tiles;
-    nt = local / cnt;
-    pp = b + (local - nt * cnt);
-    e = lo;
-  }
-  __device__ Unit unit(int u, int rank) const {
-    int e, nt, pp;
-    locate(u, e, nt, pp);
+    const int nt = local / cnt;
+    const int pp = b + (local - nt * cnt);
     const int p = 2 * pp + rank;
-    const int brow = b_tiled ? (e * n_tiles + nt) * kb * bn : e * n_per_expert + nt * bn;
-    return Unit{piece_row[p], piece_rows[p], brow, nt * bn};
-  }
-  __device__ int mtiles(int u) const {
-    int e, nt, pp;
-    locate(u, e, nt, pp);
-    const int r0 = piece_rows[2 * pp], r1 = piece_rows[2 * pp + 1];
-    return max(max((r0 + kBlockM - 1) / kBlockM, (r1 + kBlockM - 1) / kBlockM), 1);
-  }
-  __device__ int piece_mtiles(int u, int rank) const {
-    const int r = unit(u, rank).rows;
-    return (r + kBlockM - 1) / kBlockM;
+    const int brow = b_tiled ? (lo * n_tiles + nt) * kb * bn : lo * n_per_expert + nt * bn;
+    const int rows = __ldg(&piece_rows[p]), prow = __ldg(&piece_rows[p ^ 1]);
+    PairUnit I;
+    I.U = Unit{__ldg(&piece_row[p]), rows, brow, nt * bn};
+    const int my = (rows + kBlockM - 1) / kBlockM, peer = (prow + kBlockM - 1) / kBlockM;
+    I.mtiles = max(max(my, peer), 1);
+    I.peer_mt = peer;
+    return I;
   }
   __device__ int num_kb() const { return kb; }
   __device__ int a_kcol(int k) const { return k * kBlockK; }

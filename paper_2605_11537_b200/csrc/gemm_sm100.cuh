@@ -44,12 +44,18 @@ struct GemmSmem {
   static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
   static constexpr int kScratchOffset = kVecOffset + 2 * BN * 4;
   static constexpr int kScratchWordsPerWarp = 32 * 20;  // 32 rows x (16 + 4 pad) words: store transpose
-  static constexpr int kBytes = kScratchOffset + 8 * kScratchWordsPerWarp * 4 + 1024;  // + alignment slack
+  static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;  // scheduler table (smem)
+  static constexpr int kPrepInts = 1025;
+  static constexpr int kBytes = kPrepOffset + kPrepInts * 4 + 1024;  // + alignment slack
 };
 
 // Scheduler concept:
 //   int num_units() const; Unit unit(int u) const; int num_kb() const;
 //   int a_kcol(int kb) const; int b_kcol(int kb) const;
+//   void prepare(int* table) -- run by ALL threads before the roles start; may stage
+//   read-only scheduling data in shared memory (GemmSmem::kPrepInts ints).
+// Every role decodes the NEXT unit while working on the current one, so the
+// (global-memory) piece lookups of a grouped GEMM never stall the pipeline.
 // Epilogue concept:
 //   static constexpr bool kSplitCols;   // columns independent -> two warpgroups split them
 //   const float* colvec() const;        // per-column vector (bias) or null; staged in smem per tile
@@ -61,7 +67,7 @@ struct GemmSmem {
 
 template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched,
+    k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched_in,
                 Epi epi) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using L = GemmSmem<BN, STAGES>;
@@ -92,6 +98,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  Sched sched = sched_in;
+  sched.prepare(reinterpret_cast<int*>(smem + L::kPrepOffset));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -105,8 +113,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ------------------------------------------------------------ TMA producer
       const uint64_t pol_stream = policy_evict_first();
       uint32_t stage = 0, phase = 0;
+      Unit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x) : Unit{};
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const Unit U = sched.unit(u);
+        const Unit U = Un;
+        if (u + (int)gridDim.x < nunits) Un = sched.unit(u + gridDim.x);  // consumed next iteration
         const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
         for (int mt = 0; mt < mtiles; ++mt) {
           for (int kb = 0; kb < nkb; ++kb) {
@@ -132,8 +142,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = Kind::idesc(kBlockM, BN);
       uint32_t stage = 0, phase = 0, tile = 0;
+      Unit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x) : Unit{};
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const Unit U = sched.unit(u);
+        const Unit U = Un;
+        if (u + (int)gridDim.x < nunits) Un = sched.unit(u + gridDim.x);
         const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
         for (int mt = 0; mt < mtiles; ++mt, ++tile) {
           const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
@@ -171,8 +183,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const bool active = split || half == 0;
     const int c0 = split ? half * (BN / 2) : 0;
     uint32_t tile = 0;
+    Unit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x) : Unit{};
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      const Unit U = sched.unit(u);
+      const Unit U = Un;
+      if (u + (int)gridDim.x < nunits) Un = sched.unit(u + gridDim.x);
       const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
       for (int mt = 0; mt < mtiles; ++mt, ++tile) {
         const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
@@ -208,6 +222,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 // Dense C[M x N] = A[M x K] B[N x K]^T, units = (m block, n block), n fastest.
 struct DenseSched {
+  __device__ void prepare(int*) {}
   static constexpr bool kStreamB = false;
   int M, n_tiles, kb, bn;
   __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
@@ -228,6 +243,7 @@ struct DenseSched {
 
 // Device-built unit list (grouped GEMM over replica segments).
 struct ListSched {
+  __device__ void prepare(int*) {}
   static constexpr bool kStreamB = false;
   const int4* units;      // {a_row, rows, b_row, n0}
   const int* num_units_p;  // device scalar, written by the planner
@@ -251,9 +267,15 @@ struct SegSched {
   static constexpr bool kStreamB = true;
   const int32_t* piece_row;
   const int32_t* piece_rows;
-  const int32_t* exp_begin;  // E + 1 entries
+  const int32_t* exp_begin;  // E + 1 entries (staged into shared memory by prepare when E < kPrepInts)
   int E, n_tiles, bn, n_per_expert, kb;
   int b_tiled;  // B pre-tiled as [E][n_tiles][kb][bn rows][64 cols]: every TMA box is one contiguous burst
+  __device__ void prepare(int* tab) {
+    if (E + 1 > 1025) return;
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) tab[e] = exp_begin[e];
+    __syncthreads();
+    exp_begin = tab;
+  }
   __device__ int num_units() const { return exp_begin[E] * n_tiles; }
   __device__ Unit unit(int u) const {
     int lo = 0, hi = E;  // exp_begin[lo]*n_tiles <= u < exp_begin[hi]*n_tiles
@@ -266,7 +288,7 @@ struct SegSched {
     const int nt = local / cnt;
     const int p = b + (local - nt * cnt);
     const int brow = b_tiled ? (lo * n_tiles + nt) * kb * bn : lo * n_per_expert + nt * bn;
-    return Unit{piece_row[p], piece_rows[p], brow, nt * bn};
+    return Unit{__ldg(&piece_row[p]), __ldg(&piece_rows[p]), brow, nt * bn};
   }
   __device__ int num_kb() const { return kb; }
   __device__ int a_kcol(int k) const { return k * kBlockK; }
@@ -276,6 +298,7 @@ struct SegSched {
 
 // Dense fp32/TF32 GEMM: k-blocks of 32 fp32 (128 B).
 struct DenseTf32Sched {
+  __device__ void prepare(int*) {}
   static constexpr bool kStreamB = false;
   int M, n_tiles, kb, bn;
   __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }
@@ -294,6 +317,7 @@ struct DenseTf32Sched {
 //   acc = x_hi.w_hi + x_hi.w_lo + x_lo.w_hi
 // expressed as 3*nk k-blocks with remapped k coordinates.
 struct Split3Sched {
+  __device__ void prepare(int*) {}
   static constexpr bool kStreamB = false;
   int M, n_tiles, nk, bn, kd;  // kd = padded real K (multiple of 64)
   __device__ int num_units() const { return ((M + kBlockM - 1) / kBlockM) * n_tiles; }

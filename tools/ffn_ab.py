@@ -35,13 +35,21 @@ def main():
     prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
     nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
     sws = torch.empty(nb, dtype=torch.uint8, device=dev)
-    _lib.call("mp_segments_from_slots", ptr(r), ptr(se), T, E, E, 1, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
-              ptr(sws), nb, stream_ptr())
+    segs = {}
+    for sm in (1, 3):  # split pieces; split + even piece count per expert (CTA-pair kernels)
+        t_, pr_, pn_, eb_ = torch.empty(T, **i32), torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
+        _lib.call("mp_segments_from_slots", ptr(r), ptr(se), T, E, E, sm, ptr(t_), ptr(pr_), ptr(pn_), ptr(eb_),
+                  ptr(sws), nb, stream_ptr())
+        segs[sm] = (t_, pr_, pn_, eb_)
+    tor, prow, prows, eb = segs[1]
     fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
     ws = torch.empty(fb, dtype=torch.uint8, device=dev)
     _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
     y = x.clone()
     for fl in flags:
+        tor, prow, prows, eb = segs[3 if fl & 2 else 1]
+        _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
+
         def run():
             if which == "up":
                 _lib.call("mp_ffn_up", T, d, F, E, ptr(U if fl & 1 else U0), fl, ptr(prow), ptr(prows), ptr(eb),
