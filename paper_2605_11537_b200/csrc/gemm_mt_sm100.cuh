@@ -95,10 +95,10 @@ struct FfnMtSched {
       const int s = local / half_p, q = local - s * half_p;
       U.na = 2;
       U.nb = 1;
-      U.a_row[0] = piece_row[b + 2 * q];
-      U.rows[0] = piece_rows[b + 2 * q];
-      U.a_row[1] = piece_row[b + 2 * q + 1];
-      U.rows[1] = piece_rows[b + 2 * q + 1];
+      U.a_row[0] = __ldg(&piece_row[b + 2 * q]);
+      U.rows[0] = __ldg(&piece_rows[b + 2 * q]);
+      U.a_row[1] = __ldg(&piece_row[b + 2 * q + 1]);
+      U.rows[1] = __ldg(&piece_rows[b + 2 * q + 1]);
       U.b_row[0] = U.b_row[1] = slice_row(e, s);
       U.n0[0] = U.n0[1] = s * kMtBN;
     } else {
@@ -180,8 +180,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         return s;
       };
+      MtUnit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x, pre) : MtUnit{};
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const MtUnit U = sched.unit(u, pre);
+        const MtUnit U = Un;
+        if (u + (int)gridDim.x < nunits) Un = sched.unit(u + gridDim.x, pre);  // consumed next iteration
         for (int kb = 0; kb < nkb; ++kb) {
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
@@ -228,8 +230,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         return s;
       };
+      MtUnit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x, pre) : MtUnit{};
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const MtUnit U = sched.unit(u, pre);
+        const MtUnit U = Un;
+        if (u + (int)gridDim.x < nunits) Un = sched.unit(u + gridDim.x, pre);  // consumed next iteration
         const int ntile = U.na * U.nb;
         for (int t = 0; t < ntile; ++t) mbar_wait(&tempty[(tile + t) & 1], (((tile + t) >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -280,8 +284,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int c0 = half * (kMtBN / 2);
     uint32_t* scratch = scratch_all + (warp - 4) * 640;
     uint32_t tile = 0;
+    MtUnit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x, pre) : MtUnit{};
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      const MtUnit U = sched.unit(u, pre);
+      const MtUnit U = Un;
+      if (u + (int)gridDim.x < nunits) Un = sched.unit(u + gridDim.x, pre);
       const int ntile = U.na * U.nb;
       for (int t = 0; t < ntile; ++t, ++tile) {
         const uint32_t as = tile & 1, aph = (tile >> 1) & 1;
