@@ -137,6 +137,14 @@ MP_API size_t mp_sru_workspace_bytes(int T, int d);
 MP_API int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* w_cat, const float* b_cat, int T, int d,
                         const float* c0, float* h_f32, void* h_bf16, float* c_last, int32_t* nonfinite, void* ws,
                         size_t ws_bytes, void* stream);
+/* The same layer in two parts, for callers that pipeline token ranges over streams
+ * (the scan of rows [0, T/2) overlapping the projection of rows [T/2, T), carried by
+ * c_last -> c0): mp_sru_project writes [u | f | r] into ws, mp_sru_scan runs the
+ * recurrence + highway from it. Same ws for both; results equal mp_sru_layer. */
+MP_API int mp_sru_project(const void* x_bf16, const void* w_cat, const float* b_cat, int T, int d, void* ws,
+                          size_t ws_bytes, void* stream);
+MP_API int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16, float* c_last,
+                       int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
 /* c0 (d floats, NULL = zeros, src/predictor.py:190) is the cell state entering token 0 --
  * sru_cell's c_prev, or the carry of a preceding token shard; c_last (nullable) receives the
  * cell state after the last token. nonfinite (1 int) is OR-ed with 1 on NaN/inf state

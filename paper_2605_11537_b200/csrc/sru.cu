@@ -29,6 +29,7 @@ __device__ __forceinline__ float2 ld_bf16x2(const __nv_bfloat16* p) {
 struct bf16x4 {
   __nv_bfloat162 a, b;
 };
+constexpr int kAggDepth = 16;  // tokens of u/f loads in flight per thread
 __global__ void __launch_bounds__(64) k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, int d,
                                                        float* __restrict__ aggA, float* __restrict__ aggB) {
   const int cq = blockIdx.x * blockDim.x + threadIdx.x;
@@ -38,17 +39,17 @@ __global__ void __launch_bounds__(64) k_scan_aggregate(const __nv_bfloat16* __re
   float a[4] = {1.f, 1.f, 1.f, 1.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
   const size_t ld3 = (size_t)3 * d;
 #pragma unroll 1
-  for (int tb = t0; tb < t1; tb += 8) {
-    bf16x4 u[8], f[8];
+  for (int tb = t0; tb < t1; tb += kAggDepth) {
+    bf16x4 u[kAggDepth], f[kAggDepth];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kAggDepth; ++i) {
       const int t = min(tb + i, t1 - 1);
       const __nv_bfloat16* p = ufr + (size_t)t * ld3 + 4 * cq;
       u[i] = *reinterpret_cast<const bf16x4*>(p);
       f[i] = *reinterpret_cast<const bf16x4*>(p + d);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kAggDepth; ++i) {
       if (tb + i < t1) {
         const float2 ua = __bfloat1622float2(u[i].a), ub = __bfloat1622float2(u[i].b);
         const float2 fa = __bfloat1622float2(f[i].a), fb = __bfloat1622float2(f[i].b);
@@ -71,39 +72,72 @@ __global__ void __launch_bounds__(64) k_scan_aggregate(const __nv_bfloat16* __re
 // 3 * sqrt(nch) instead of nch: block = 32 channels x G chunk groups; each
 // (group, channel) composes its chunks' affine maps, one thread per channel
 // scans the G group maps, then every group replays its chunks from its carry.
+// The chunk maps of a group are loaded into registers 16 at a time (independent
+// loads in flight) before the serial composition, and reused by the replay.
 constexpr int kCarryGroups = 16;
-__global__ void k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
+constexpr int kCarryBatch = 16;
+__global__ void __launch_bounds__(32 * kCarryGroups) k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
                              const float* __restrict__ c0, float* __restrict__ carry) {
   __shared__ float sA[kCarryGroups][32], sB[kCarryGroups][32], sC[kCarryGroups][32];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   const int per = cdiv(nch, kCarryGroups);
   const int ch0 = g * per, ch1 = min(nch, ch0 + per);
+  const bool act = c < d;
   float A = 1.f, B = 0.f;
-  if (c < d)
-    for (int ch = ch0; ch < ch1; ++ch) {
-      const size_t o = (size_t)ch * d + c;
-      const float a = __ldg(&aggA[o]), b = __ldg(&aggB[o]);
-      B = fmaf(a, B, b);  // compose: apply (A,B) first, then (a,b)
-      A *= a;
+  float ra[kCarryBatch], rb[kCarryBatch];
+  const bool one_batch = per <= kCarryBatch;  // typical: nch = 512 -> 32 per group -> two batches
+  for (int cb = ch0; cb < ch1; cb += kCarryBatch) {
+#pragma unroll
+    for (int i = 0; i < kCarryBatch; ++i) {
+      const int ch = cb + i;
+      if (act && ch < ch1) {
+        const size_t o = (size_t)ch * d + c;
+        ra[i] = __ldg(&aggA[o]);
+        rb[i] = __ldg(&aggB[o]);
+      }
     }
+#pragma unroll
+    for (int i = 0; i < kCarryBatch; ++i) {
+      if (act && cb + i < ch1) {
+        B = fmaf(ra[i], B, rb[i]);  // compose: apply (A,B) first, then (a,b)
+        A *= ra[i];
+      }
+    }
+  }
   sA[g][cl] = A;
   sB[g][cl] = B;
   __syncthreads();
   if (g == 0) {
-    float run = (c < d && c0) ? c0[c] : 0.f;
+    float run = (act && c0) ? c0[c] : 0.f;
     for (int h = 0; h < kCarryGroups; ++h) {
       sC[h][cl] = run;
       run = fmaf(sA[h][cl], run, sB[h][cl]);
     }
   }
   __syncthreads();
-  if (c < d) {
+  if (act) {
     float run = sC[g][cl];
-    for (int ch = ch0; ch < ch1; ++ch) {
-      const size_t o = (size_t)ch * d + c;
-      carry[o] = run;
-      run = fmaf(__ldg(&aggA[o]), run, __ldg(&aggB[o]));
+    for (int cb = ch0; cb < ch1; cb += kCarryBatch) {
+      if (!one_batch) {
+#pragma unroll
+        for (int i = 0; i < kCarryBatch; ++i) {
+          const int ch = cb + i;
+          if (ch < ch1) {
+            const size_t o = (size_t)ch * d + c;
+            ra[i] = __ldg(&aggA[o]);
+            rb[i] = __ldg(&aggB[o]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < kCarryBatch; ++i) {
+        const int ch = cb + i;
+        if (ch < ch1) {
+          carry[(size_t)ch * d + c] = run;
+          run = fmaf(ra[i], run, rb[i]);
+        }
+      }
     }
   }
 }
@@ -239,32 +273,55 @@ extern "C" size_t mp_sru_workspace_bytes(int T, int d) {
   return al(sizeof(__nv_bfloat16) * (size_t)T * 3 * d) + 3 * al(sizeof(float) * (size_t)nch * d);
 }
 
+struct SruWs {
+  __nv_bfloat16* ufr;
+  float *aggA, *aggB, *carry;
+  SruWs(void* ws, int T, int d) {
+    const int nch = cdiv(T, kScanChunk);
+    char* p = (char*)ws;
+    ufr = (__nv_bfloat16*)p;
+    p += al(sizeof(__nv_bfloat16) * (size_t)T * 3 * d);
+    aggA = (float*)p;
+    p += al(sizeof(float) * (size_t)nch * d);
+    aggB = (float*)p;
+    p += al(sizeof(float) * (size_t)nch * d);
+    carry = (float*)p;
+  }
+};
+
+#define SRU_CHECKS()                                                                                          \
+  MP_REQUIRE(T >= 1, MP_ERR_CONFIG, "batch must contain at least one token");                                  \
+  MP_REQUIRE(d >= 64 && d % 64 == 0, MP_ERR_CONFIG, "mp_sru: d=%d must be a multiple of 64 (pad)", d);           \
+  MP_REQUIRE(ws_bytes >= mp_sru_workspace_bytes(T, d), MP_ERR_CONFIG, "mp_sru: workspace too small");
+
+extern "C" int mp_sru_project(const void* x_bf16, const void* w_cat, const float* b_cat, int T, int d, void* ws,
+                              size_t ws_bytes, void* stream) {
+  SRU_CHECKS();
+  // K1: [u | f | r] = x W_cat^T + b ; sigmoid on the f and r blocks
+  return mp_gemm_bf16(x_bf16, w_cat, SruWs(ws, T, d).ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, stream);
+}
+
+extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16,
+                           float* c_last, int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
+  SRU_CHECKS();
+  cudaStream_t st = (cudaStream_t)stream;
+  const SruWs w(ws, T, d);
+  const int nch = cdiv(T, kScanChunk);
+  // K2: chunk aggregates | carries (from c0) | replay + highway
+  const dim3 gq(cdiv(d / 4, 64), nch);
+  k_scan_aggregate<<<gq, 64, 0, st>>>(w.ufr, T, d, w.aggA, w.aggB);
+  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, c0, w.carry);
+  k_scan_output<<<gq, 64, 0, st>>>(w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
 extern "C" int mp_sru_layer(const void* x_bf16, const float* x_f32, const void* w_cat, const float* b_cat, int T,
                             int d, const float* c0, float* h_f32, void* h_bf16, float* c_last, int32_t* nonfinite,
                             void* ws, size_t ws_bytes, void* stream) {
-  MP_REQUIRE(T >= 1, MP_ERR_CONFIG, "batch must contain at least one token");
-  MP_REQUIRE(d >= 64 && d % 64 == 0, MP_ERR_CONFIG, "mp_sru_layer: d=%d must be a multiple of 64 (pad)", d);
-  MP_REQUIRE(ws_bytes >= mp_sru_workspace_bytes(T, d), MP_ERR_CONFIG, "mp_sru_layer: workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int nch = cdiv(T, kScanChunk);
-  char* p = (char*)ws;
-  __nv_bfloat16* ufr = (__nv_bfloat16*)p;
-  p += al(sizeof(__nv_bfloat16) * (size_t)T * 3 * d);
-  float* aggA = (float*)p;
-  p += al(sizeof(float) * (size_t)nch * d);
-  float* aggB = (float*)p;
-  p += al(sizeof(float) * (size_t)nch * d);
-  float* carry = (float*)p;
-  // K1: [u | f | r] = x W_cat^T + b ; sigmoid on the f and r blocks
-  int rc = mp_gemm_bf16(x_bf16, w_cat, ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, stream);
+  int rc = mp_sru_project(x_bf16, w_cat, b_cat, T, d, ws, ws_bytes, stream);
   if (rc) return rc;
-  // K2
-  const dim3 gq(cdiv(d / 4, 64), nch);
-  k_scan_aggregate<<<gq, 64, 0, st>>>(ufr, T, d, aggA, aggB);
-  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(aggA, aggB, nch, d, c0, carry);
-  k_scan_output<<<gq, 64, 0, st>>>(ufr, x_f32, T, d, carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
-  MP_CUDA_TRY(cudaGetLastError());
-  return MP_OK;
+  return mp_sru_scan(x_f32, T, d, c0, h_f32, h_bf16, c_last, nonfinite, ws, ws_bytes, stream);
 }
 
 extern "C" int mp_heads_argmax(const void* h_bf16, const void* heads, int T, int d, int L, int E, int Eg,

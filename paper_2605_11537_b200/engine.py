@@ -52,6 +52,7 @@ class PipelineConfig:
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
     ffn: str = "two"              # two (single-tile units) | mt (multi-tile units, slower: see DESIGN) |
                                   # fused (experimental: one launch, H in an L2 ring)
+    sru_pipeline: bool = False    # two-stream token-half SRU pipeline (measured slower: 1219 vs 1133 us)
     skew: float = 1.2
     noise: float = 0.1
     seed: int = 0
@@ -194,6 +195,13 @@ class MoEPipeline:
 
         self.ws_sru_n = _lib.size_query("mp_sru_workspace_bytes", T, d)
         self.ws_sru = ws(self.ws_sru_n)
+        # two-stream SRU pipeline over token halves (see _sru_pipelined)
+        self.sru_halves = cfg.sru_pipeline and T % 256 == 0 and T >= 512
+        if self.sru_halves:
+            self.ws_sru_h_n = _lib.size_query("mp_sru_workspace_bytes", T // 2, d)
+            self.ws_sru_h = [ws(self.ws_sru_h_n) for _ in range(2)]
+            self.sru_carry = torch.zeros(d, device=dev)
+            self.sru_stream = torch.cuda.Stream(device=dev)
         self.ws_hist_n = _lib.size_query("mp_histogram_workspace_bytes", L, T, E)
         self.ws_hist = ws(self.ws_hist_n)
         self.ws_place_n = _lib.size_query("mp_place_workspace_bytes", L, T, E)
@@ -216,16 +224,58 @@ class MoEPipeline:
         n = 0
         _lib.call("mp_f32_to_bf16", ptr(x), ptr(self.x16), T * d, sp)
         n += 1
-        cur32, cur16 = x, self.x16
-        for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
-            h32, h16 = self.h32[i % 2], self.h16[i % 2]
-            _lib.call("mp_sru_layer", ptr(cur16), ptr(cur32), ptr(W), ptr(B), T, d, None, ptr(h32), ptr(h16), None,
-                      ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
-            n += 4
-            cur32, cur16 = h32, h16
+        if self.sru_halves:
+            n += self._sru_pipelined(x, sp)
+            cur16 = self.h16[(len(self.sru.w_cat) - 1) % 2]
+        else:
+            cur32, cur16 = x, self.x16
+            for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
+                h32, h16 = self.h32[i % 2], self.h16[i % 2]
+                _lib.call("mp_sru_layer", ptr(cur16), ptr(cur32), ptr(W), ptr(B), T, d, None, ptr(h32), ptr(h16), None,
+                          ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
+                n += 4
+                cur32, cur16 = h32, h16
         _lib.call("mp_heads_argmax", ptr(cur16), ptr(self.sru.heads), T, d, cfg.num_layers, cfg.num_experts,
                   self.sru.Eg, ptr(self.assign), sp)
         return n + 1
+
+    def _sru_pipelined(self, x: torch.Tensor, sp: int) -> int:
+        """SRU stack with the batch split into two token halves on two streams: the scan
+        (memory-bound) of one half overlaps the projection GEMM (tensor-bound) of the other,
+        and layer i+1's projection of a half starts as soon as layer i's scan of that half is
+        done. The scan of the second half starts from the first half's final carry, so the
+        result is the sequential recurrence (same kernels, same arithmetic)."""
+        T, d, T2 = self.cfg.tokens, self.dp, self.cfg.tokens // 2
+        A = torch.cuda.ExternalStream(sp)
+        Bs = self.sru_stream
+        fork = torch.cuda.Event()
+        fork.record(A)
+        Bs.wait_event(fork)
+        ev_g = [[torch.cuda.Event() for _ in range(2)] for _ in range(len(self.sru.w_cat))]
+        ev_s = [[torch.cuda.Event() for _ in range(2)] for _ in range(len(self.sru.w_cat))]
+        self._sru_events = (fork, ev_g, ev_s)  # keep alive while the graph is captured
+        rows16, rows32 = T2 * d * 2, T2 * d * 4
+        n = 0
+        for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
+            in16 = self.x16 if i == 0 else self.h16[(i - 1) % 2]
+            in32 = x if i == 0 else self.h32[(i - 1) % 2]
+            h32, h16 = self.h32[i % 2], self.h16[i % 2]
+            for k in range(2):
+                if i > 0:
+                    A.wait_event(ev_s[i - 1][k])
+                _lib.call("mp_sru_project", ptr(in16) + k * rows16, ptr(W), ptr(B), T2, d, ptr(self.ws_sru_h[k]),
+                          self.ws_sru_h_n, sp)
+                ev_g[i][k].record(A)
+                Bs.wait_event(ev_g[i][k])
+                c0 = None if k == 0 else ptr(self.sru_carry)
+                c_last = ptr(self.sru_carry) if k == 0 else None
+                _lib.call("mp_sru_scan", ptr(in32) + k * rows32, T2, d, c0, ptr(h32) + k * rows32,
+                          ptr(h16) + k * rows16, c_last, ptr(self.nonfinite), ptr(self.ws_sru_h[k]), self.ws_sru_h_n,
+                          Bs.cuda_stream)
+                ev_s[i][k].record(Bs)
+                n += 4
+        A.wait_event(ev_s[-1][1])  # join
+        return n
 
     def plan_and_place(self, sp: int) -> int:
         """Alg. 1: demand histogram -> capped plan -> residency + token walk for all layers."""

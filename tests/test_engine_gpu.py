@@ -9,11 +9,11 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
-def _run(replication="on", ffn="two"):
+def _run(replication="on", ffn="two", sru_pipeline=True, full=False):
     from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig
 
-    cfg = PipelineConfig(num_layers=4, num_experts=32, d_model=256, d_ff=512, tokens=4096, sru_layers=2,
-                         capacity=64, ffn=ffn, replication=replication, seed=3)
+    cfg = PipelineConfig(num_layers=4, num_experts=32, d_model=256, d_ff=512, tokens=4096, sru_layers=3,
+                         capacity=64, ffn=ffn, replication=replication, sru_pipeline=sru_pipeline, seed=3)
     pipe = MoEPipeline(cfg)
     emb, _, oracle_routes = pipe.wl.batch(cfg.tokens)
     x = emb.clone()
@@ -21,6 +21,8 @@ def _run(replication="on", ffn="two"):
     with torch.cuda.stream(s):
         pipe.step(x)
     torch.cuda.synchronize()
+    if full:
+        return pipe
     return x, pipe.route.clone(), oracle_routes
 
 
@@ -31,3 +33,16 @@ def test_engine_routing_exact_and_layout_independent():
         x, r, _ = _run(rep, ffn)
         assert torch.equal(r, r_on), (rep, ffn)
         assert torch.equal(x, x_on), (rep, ffn)
+
+
+def test_two_stream_sru_pipeline_matches_single_stream():
+    """Token-half pipelined SRU (scan of one half overlapping the projection of the other,
+    carry handed over at T/2) == the single-stream stack up to fp32 carry-composition order."""
+    a = _run(sru_pipeline=True, full=True)
+    b = _run(sru_pipeline=False, full=True)
+    last = (a.cfg.sru_layers - 1) % 2
+    ha, hb = a.h32[last], b.h32[last]
+    rel = ((ha - hb).abs().max() / hb.abs().max()).item()
+    assert rel < 1e-5, rel
+    assert (a.assign == b.assign).float().mean().item() > 0.999
+    assert int(a.nonfinite.item()) == 0
