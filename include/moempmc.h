@@ -201,7 +201,9 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
  * builder called with split_m bit 1 (even piece count per expert), dp % 256 == 0;
  * bit 2: multi-tile units (two 128 x 256 accumulator tiles per unit: two pieces of one
  * expert share each weight k-block, or one piece feeds two weight slices) -- pieces of
- * <= 128 rows (split_m bit 0), Fp % 256 == 0 (up) / dp % 256 == 0 (down), E <= 1024.
+ * <= 128 rows (split_m bit 0), Fp % 256 == 0 (up) / dp % 256 == 0 (down), E <= 1024;
+ * bit 3: clusters of 2-4 CTAs computing consecutive weight slices of one piece, the A
+ * tile loaded once and multicast to the cluster (slice count divisible by 2, 3 or 4).
  * Every mode gives bitwise identical results. */
 MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                          size_t ws_bytes, void* stream);

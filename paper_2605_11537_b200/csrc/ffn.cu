@@ -11,6 +11,7 @@
 // weight rows (no copies on one GPU).
 #include "epilogues.cuh"
 #include "gemm2_sm100.cuh"
+#include "gemm_mc_sm100.cuh"
 #include "gemm_mt_sm100.cuh"
 #include "launch.cuh"
 
@@ -80,6 +81,54 @@ static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, i
   return make_tmap_bf16(tb, w, (uint64_t)E * N, K, K, box_rows);
 }
 
+template <int BN, int STAGES, int CL, class Epi>
+static int launch_gemm_mc(const CUtensorMap& ta, const CUtensorMap& tb, const SegMcSched<CL>& s, const Epi& e,
+                          cudaStream_t st) {
+  auto kern = k_umma_gemm_mc<BN, STAGES, CL, SegMcSched<CL>, Epi>;
+  const int smem = GemmSmem<BN, STAGES>::kBytes;
+  static bool configured = false;
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((num_sms() / CL) * CL);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  MP_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, ta, tb, s, e));
+  return MP_OK;
+}
+
+// A-multicast cluster size for n_tiles slices (0: not applicable); MP_MC_CL overrides.
+static int mc_cluster(int n_tiles) {
+  static const int env = getenv("MP_MC_CL") ? atoi(getenv("MP_MC_CL")) : 0;
+  if (env) return (n_tiles % env == 0) ? env : 0;
+  for (int c : {4, 3, 2})
+    if (n_tiles % c == 0) return c;
+  return 0;
+}
+
+template <int BN, int STAGES, class Epi>
+static int launch_seg_mc(int cl, const CUtensorMap& ta, const CUtensorMap& tb, const int32_t* piece_row,
+                         const int32_t* piece_rows, const int32_t* exp_begin, int E, int n_tiles, int n_per_expert,
+                         int kb, int tiled, const Epi& e, cudaStream_t st) {
+  switch (cl) {
+    case 2: return launch_gemm_mc<BN, STAGES, 2>(ta, tb, SegMcSched<2>{piece_row, piece_rows, exp_begin, E, n_tiles, BN, n_per_expert, kb, tiled}, e, st);
+    case 3: return launch_gemm_mc<BN, STAGES, 3>(ta, tb, SegMcSched<3>{piece_row, piece_rows, exp_begin, E, n_tiles, BN, n_per_expert, kb, tiled}, e, st);
+    case 4: return launch_gemm_mc<BN, STAGES, 4>(ta, tb, SegMcSched<4>{piece_row, piece_rows, exp_begin, E, n_tiles, BN, n_per_expert, kb, tiled}, e, st);
+  }
+  MP_REQUIRE(false, MP_ERR_CONFIG, "ffn: no multicast cluster size divides %d slices", n_tiles);
+  return MP_ERR_CONFIG;
+}
+
 static int mt_single() {  // profiling switch: one tile per unit through the multi-tile kernel
   static const int v = getenv("MP_MT_SINGLE") != nullptr;
   return v;
@@ -125,6 +174,10 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
     Seg2Sched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
     return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
   }
+  if (flags & 8) {  // A tile multicast across a cluster of CTAs computing consecutive slices
+    const int cl = mc_cluster(Fp / 256);
+    if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, Fp / 256, Fp, dp / 64, tiled, e, st);
+  }
   SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
   return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
 }
@@ -153,6 +206,10 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
     MP_REQUIRE(bn == 256, MP_ERR_CONFIG, "ffn pair mode needs dp %% 256 == 0");
     Seg2Sched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
     return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
+  }
+  if ((flags & 8) && bn == 256) {
+    const int cl = mc_cluster(dp / 256);
+    if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, dp / 256, dp, Fp / 64, tiled, e, st);
   }
   SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);

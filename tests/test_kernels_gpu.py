@@ -275,6 +275,18 @@ def test_cta_pair_ffn_matches_single_cta(dev, split):
 @pytest.mark.parametrize("skew,d,F,tiled", [(0.0, 256, 768, 1), (1.2, 512, 512, 1), (3.0, 768, 1280, 0),
                                              (1.2, 256, 256, 0), (8.0, 512, 768, 1)])
 def test_multi_tile_ffn_matches_single_tile(dev, skew, d, F, tiled):
+    _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 4)
+
+
+@pytest.mark.parametrize("skew,d,F,tiled", [(0.0, 768, 768, 1), (1.2, 512, 1024, 1), (3.0, 768, 1280, 0),
+                                             (1.2, 256, 512, 1), (8.0, 768, 3072, 1)])
+def test_multicast_cluster_ffn_matches_single_cta(dev, skew, d, F, tiled):
+    """A tile multicast across a cluster of CTAs (one per weight slice) == the single-CTA
+    kernels, bit for bit (cluster sizes 2/3/4 chosen by the slice counts)."""
+    _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 8)
+
+
+def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
     """Multi-tile units (two accumulator tiles sharing A or B) == the single-tile kernels, bit for bit:
     odd and even piece counts per expert, odd slice counts, empty experts, both weight layouts."""
     rng = np.random.default_rng(int(skew * 10) + d + F)
@@ -310,9 +322,10 @@ def test_multi_tile_ffn_matches_single_tile(dev, skew, d, F, tiled):
     y2 = x.clone()
     ws.zero_()
     _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
-    _lib.call("mp_ffn_up", T, d, F, E, ptr(Ut), tiled | 4, ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb, stream_ptr())
+    _lib.call("mp_ffn_up", T, d, F, E, ptr(Ut), tiled | mode, ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb,
+              stream_ptr())
     h2 = ws[h0:h0 + T * F * 2].clone()
-    _lib.call("mp_ffn_down", ptr(y2), T, d, F, E, ptr(Vt), tiled | 4, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
+    _lib.call("mp_ffn_down", ptr(y2), T, d, F, E, ptr(Vt), tiled | mode, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
               ptr(ws), fb, stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(h1, h2)
