@@ -43,56 +43,52 @@ __global__ void k_chunk_hist(const int32_t* __restrict__ assign, int T, int E, i
   for (int e = threadIdx.x; e < E; e += blockDim.x) out[e] = hist[e];
 }
 
-// In place: cc[l][ch][e] <- sum_{ch' < ch} cc[l][ch'][e]; demand[l][e] <- total.
-// grid L, block 1024: G = 1024 / E thread groups each scan a contiguous run of
-// chunks for every expert, then add the totals of the groups before them.
-__global__ void k_chunk_prefix(int32_t* __restrict__ cc, int nch, int E, int32_t* __restrict__ demand) {
-  __shared__ int part[1024];
-  const int l = blockIdx.x;
-  int32_t* base = cc + (size_t)l * nch * E;
-  const int G = (E >= (int)blockDim.x) ? 1 : min((int)blockDim.x / E, nch);
-  const int per = cdiv(nch, G);
-  for (int e0 = 0; e0 < E; e0 += (G == 1 ? blockDim.x : E)) {
-    const int g = (G == 1) ? 0 : threadIdx.x / E;
-    const int e = e0 + ((G == 1) ? threadIdx.x : threadIdx.x % E);
-    const bool act = g < G && e < E;
-    const int ch0 = g * per, ch1 = min(nch, ch0 + per);
-    int run = 0;
-    if (act) {
-      int32_t* p = base + e;
-      int ch = ch0;
-      for (; ch + 4 <= ch1; ch += 4) {
-        const int c0 = p[(size_t)(ch + 0) * E], c1 = p[(size_t)(ch + 1) * E];
-        const int c2 = p[(size_t)(ch + 2) * E], c3 = p[(size_t)(ch + 3) * E];
-        p[(size_t)(ch + 0) * E] = run;
-        p[(size_t)(ch + 1) * E] = run + c0;
-        p[(size_t)(ch + 2) * E] = run + c0 + c1;
-        p[(size_t)(ch + 3) * E] = run + c0 + c1 + c2;
-        run += c0 + c1 + c2 + c3;
-      }
-      for (; ch < ch1; ++ch) {
-        const int c = p[(size_t)ch * E];
-        p[(size_t)ch * E] = run;
-        run += c;
-      }
+// In place: cc[l][ch][e] <- sum_{ch' < ch} cc[l][ch'][e]; demand[l][e] <- total. Grid
+// (ceil(E / 32), L), block 32 x 32 = (expert lane, chunk group); each thread scans
+// a contiguous run of chunks for one expert (coalesced 128 B rows), group totals are
+// scanned in shared memory, then every run adds its group offset.
+__global__ void __launch_bounds__(1024) k_chunk_prefix_cols(int32_t* __restrict__ cc, int nch, int E,
+                                                            int32_t* __restrict__ demand) {
+  __shared__ int part[32][33];
+  const int l = blockIdx.y;
+  const int el = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + el;
+  const int per = cdiv(nch, 32);
+  const int ch0 = g * per, ch1 = min(nch, ch0 + per);
+  int32_t* base = cc + (size_t)l * nch * E + e;
+  int run = 0;
+  if (e < E) {
+    int ch = ch0;
+    for (; ch + 4 <= ch1; ch += 4) {
+      const int c0 = base[(size_t)(ch + 0) * E], c1 = base[(size_t)(ch + 1) * E];
+      const int c2 = base[(size_t)(ch + 2) * E], c3 = base[(size_t)(ch + 3) * E];
+      base[(size_t)(ch + 0) * E] = run;
+      base[(size_t)(ch + 1) * E] = run + c0;
+      base[(size_t)(ch + 2) * E] = run + c0 + c1;
+      base[(size_t)(ch + 3) * E] = run + c0 + c1 + c2;
+      run += c0 + c1 + c2 + c3;
     }
-    if (G == 1) {
-      if (act) demand[(size_t)l * E + e] = run;
-      continue;
+    for (; ch < ch1; ++ch) {
+      const int c = base[(size_t)ch * E];
+      base[(size_t)ch * E] = run;
+      run += c;
     }
-    if (act) part[g * E + (e - e0)] = run;
-    __syncthreads();
-    if (act) {
-      int off = 0;
-      for (int h = 0; h < g; ++h) off += part[h * E + (e - e0)];
-      if (off) {
-        int32_t* p = base + e;
-        for (int ch = ch0; ch < ch1; ++ch) p[(size_t)ch * E] += off;
-      }
-      if (g == G - 1) demand[(size_t)l * E + e] = off + run;
-    }
-    __syncthreads();
   }
+  part[g][el] = run;
+  __syncthreads();
+  if (g == 0) {
+    int acc = 0;
+    for (int h = 0; h < 32; ++h) {
+      const int v = part[h][el];
+      part[h][el] = acc;
+      acc += v;
+    }
+    if (e < E) demand[(size_t)l * E + e] = acc;
+  }
+  __syncthreads();
+  const int off = part[g][el];
+  if (e < E && off)
+    for (int ch = ch0; ch < ch1; ++ch) base[(size_t)ch * E] += off;
 }
 
 // cap_replicas (src/planner.py:36-72) as a closed-form water-fill. grid L, block 1024.
@@ -509,7 +505,7 @@ extern "C" int mp_histogram(const int32_t* assign, int L, int T, int E, int32_t*
   MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_histogram: E=%d too large", E);
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm));
   k_chunk_hist<<<dim3(nch, L), kChunk, sm, st>>>(assign, T, E, nch, cc);
-  k_chunk_prefix<<<L, 1024, 0, st>>>(cc, nch, E, demand);
+  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>(cc, nch, E, demand);
   MP_CUDA_TRY(cudaGetLastError());
   MP_CUDA_TRY(cudaFreeAsync(cc, st));
   return MP_OK;
@@ -530,7 +526,7 @@ extern "C" int mp_histogram_ws(const int32_t* assign, int L, int T, int E, int32
   MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_histogram_ws: E=%d too large", E);
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm));
   k_chunk_hist<<<dim3(nch, L), kChunk, sm, st>>>(assign, T, E, nch, (int32_t*)ws);
-  k_chunk_prefix<<<L, 1024, 0, st>>>((int32_t*)ws, nch, E, demand);
+  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>((int32_t*)ws, nch, E, demand);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -581,7 +577,7 @@ extern "C" int mp_place(const int32_t* assign, int L, int T, int E, const int32_
   } else {
     MP_CUDA_TRY(cudaMemsetAsync(cc, 0, sizeof(int32_t) * (size_t)L * nch * E, st));
   }
-  k_chunk_prefix<<<L, 1024, 0, st>>>(cc, nch, E, dem);
+  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>(cc, nch, E, dem);
   k_place_layer<<<L, 1024, sm, st>>>(dem, E, caps, plan_capacity, state_capacity, res, cap_eff, r_eff, off_g,
                                      offloads, fallback, num_slots);
   if (T > 0)
@@ -648,7 +644,7 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
   k_chunk_hist<<<dim3(nch, L), kChunk, sm_h, st>>>(route, T, E, nch, cc);
-  k_chunk_prefix<<<L, 1024, 0, st>>>(cc, nch, E, dem);
+  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>(cc, nch, E, dem);
   k_exec_layer<<<L, 1024, sm_x, st>>>(dem, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row,
                                       piece_row, piece_rows, exp_begin, pieces_stride, err);
   k_exec_rank<<<dim3(nch, L), kChunk, 0, st>>>(route, T, E, nch, max_slots, cc, off_g, slot_row, token_to_slot,
@@ -680,7 +676,7 @@ extern "C" int mp_segments_from_slots(const int32_t* token_to_slot, const int32_
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_seg_layer, sm_s));
   k_chunk_hist<<<dim3(nch, 1), kChunk, sm_h, st>>>(token_to_slot, T, S, nch, cc);
-  k_chunk_prefix<<<1, 1024, 0, st>>>(cc, nch, S, size);
+  k_chunk_prefix_cols<<<dim3(cdiv(S, 32), 1), 1024, 0, st>>>(cc, nch, S, size);
   k_seg_layer<<<1, 1024, sm_s, st>>>(size, slot_expert, S, E, split_m, slot_row, piece_row, piece_rows, exp_begin);
   k_seg_rank<<<nch, kChunk, 0, st>>>(token_to_slot, T, S, nch, cc, slot_row, tok_of_row);
   MP_CUDA_TRY(cudaGetLastError());
