@@ -77,6 +77,23 @@ int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t co
   return MP_OK;
 }
 
+// 2-D bf16 row-major store map for EpiStoreBf16Tma: box = [32 rows x 32 cols] (64 B rows), SWIZZLE_64B.
+int make_tmap_bf16_store(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems) {
+  auto enc = get_encode();
+  MP_REQUIRE(enc != nullptr, MP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  MP_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && (row_stride_elems * 2) % 16 == 0, MP_ERR_CONFIG,
+             "tensor map: base and row stride must be 16-byte aligned");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  MP_REQUIRE(r == CUDA_SUCCESS, MP_ERR_CUDA, "cuTensorMapEncodeTiled(store) failed (%d)", (int)r);
+  return MP_OK;
+}
+
 // 2-D fp32 row-major tensor map, box = [box_rows x 32 cols] (128 B), SWIZZLE_128B (TF32 operands).
 int make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                   uint32_t box_rows) {
@@ -123,6 +140,14 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
     EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
     const int cu = cdiv(M, 2 * kBlockM) * (N / bn);
     return launch_gemm2<256, 6>(ta, tb2, s2, e, std::min(2 * cu, num_sms()), st);
+  }
+  static const bool tma_store = getenv("MP_STG_EPILOGUE") == nullptr;  // A/B switch: st.global epilogue
+  if (c_dtype == 0 && tma_store && bn == 256 && ldc > 0) {  // bf16 tile through TMA bulk stores
+    CUtensorMap tc;
+    rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
+    if (rc) return rc;
+    EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
+    return launch_gemm<256, 4>(ta, tb, s, et, grid, st, &tc);
   }
   if (c_dtype == 0) {
     EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};

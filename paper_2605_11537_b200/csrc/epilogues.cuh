@@ -117,6 +117,64 @@ struct EpiStoreBf16 {
   }
 };
 
+// EpiStoreBf16 with the tile written by TMA bulk stores: each warp packs its 32 rows x
+// 32 columns (64 B rows) into its scratch as a SWIZZLE_64B box and one lane issues
+// cp.async.bulk.tensor (global writes leave the LSU/L1 path; the box lands as whole
+// 64 B row segments). Warps whose 32 rows are not all inside the unit (the tail of a
+// piece -- the next rows belong to another piece) fall back to st.global.
+// tm (the GEMM kernel's tmC parameter): bf16 [rows x ldo] map, box 32 x 32, SWIZZLE_64B
+// (make_tmap_bf16_store).
+struct EpiStoreBf16Tma {
+  static constexpr bool kSplitCols = true;
+  static constexpr bool kTmaStore = true;  // the kernel passes its tmC parameter to run()
+  __nv_bfloat16* out;
+  int ldo;
+  const float* bias;
+  int act;
+  int sig_from;
+  __device__ __forceinline__ const float* colvec() const { return bias; }
+  template <int NC>
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec,
+                                      uint32_t* scratch, const CUtensorMap* tm) const {
+    const int lane = threadIdx.x & 31;
+    const int row0 = mt * kBlockM + (r & ~31);
+    const int nvalid = U.rows - row0;
+    __nv_bfloat16* base = out + (size_t)(U.a_row + row0) * ldo + U.n0 + c0;
+    uint8_t* box = reinterpret_cast<uint8_t*>(scratch);
+    const int sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16-byte chunk q of row `lane` lives at q ^ ((lane / 2) % 4)
+    tmem_chunks<NC>(taddr, [&](int c, float* v) {
+      apply_act(v, bias ? svec + c : nullptr, act, U.n0 + c0 + c >= sig_from);
+      if (nvalid >= 32) {
+        if (lane == 0) bulk_wait_read0();  // previous box of this warp has been read
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 w;
+          w.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+          w.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+          w.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+          w.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+          *reinterpret_cast<uint4*>(box + lane * 64 + ((q ^ sw) << 4)) = w;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(tm, box, U.n0 + c0 + c, U.a_row + row0);
+          bulk_commit();
+        }
+      } else if (nvalid > 0) {
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        store_chunk_bf16(v, scratch, [&](int i) -> __nv_bfloat16* {
+          return i < nvalid ? base + (size_t)i * ldo + c : nullptr;
+        });
+      }
+    });
+    if (lane == 0) bulk_wait0();  // box reads done and this tile's rows globally written
+    __syncwarp();
+  }
+};
+
 // out[row, n0 + c] = act(acc + bias) in fp32
 struct EpiStoreF32 {
   static constexpr bool kSplitCols = true;

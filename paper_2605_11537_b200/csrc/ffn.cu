@@ -157,6 +157,7 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
   // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256
   const int tiled = flags & 1, pair = (flags >> 1) & 1, mt = (flags >> 2) & 1;
   static const bool diag_nostore = getenv("MP_DIAG_NOSTORE") != nullptr;  // profiling switch only
+  static const bool tma_store = getenv("MP_STG_EPILOGUE") == nullptr;     // A/B switch: st.global epilogue
   EpiStoreBf16 e{hid, diag_nostore ? 0 : Fp, nullptr, 1, 0};
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
@@ -179,6 +180,13 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
     if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, Fp / 256, Fp, dp / 64, tiled, e, st);
   }
   SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
+  if (tma_store && !diag_nostore) {
+    CUtensorMap tc;
+    rc = make_tmap_bf16_store(&tc, hid, T, Fp, Fp);
+    if (rc) return rc;
+    EpiStoreBf16Tma et{hid, Fp, nullptr, 1, 0};
+    return launch_gemm<256, 4>(ta, tb, s, et, num_sms(), st, &tc);
+  }
   return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
 }
 

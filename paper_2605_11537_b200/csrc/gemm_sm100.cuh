@@ -35,6 +35,16 @@ struct Unit {
   int n0;     // output column offset of this BN slice
 };
 
+// Epilogues that write through a TMA store map (kernel parameter tmC) declare kTmaStore.
+template <class E, class = void>
+struct TmaStoreOf {
+  static constexpr bool value = false;
+};
+template <class E>
+struct TmaStoreOf<E, decltype(void(E::kTmaStore))> {
+  static constexpr bool value = E::kTmaStore;
+};
+
 template <int BN, int STAGES>
 struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;
@@ -42,7 +52,7 @@ struct GemmSmem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
   static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
-  static constexpr int kScratchOffset = kVecOffset + 2 * BN * 4;
+  static constexpr int kScratchOffset = (kVecOffset + 2 * BN * 4 + 1023) / 1024 * 1024;  // TMA-store boxes
   static constexpr int kScratchWordsPerWarp = 32 * 20;  // 32 rows x (16 + 4 pad) words: store transpose
   static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;  // scheduler table (smem)
   static constexpr int kPrepInts = 1025;
@@ -68,7 +78,7 @@ struct GemmSmem {
 template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched_in,
-                Epi epi) {
+                Epi epi, const __grid_constant__ CUtensorMap tmC) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using L = GemmSmem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -200,8 +210,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         if (active) {
           const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c0;
-          epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
-                               scratch_all + (warp - 4) * L::kScratchWordsPerWarp);
+          if constexpr (TmaStoreOf<Epi>::value)
+            epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
+                                 scratch_all + (warp - 4) * L::kScratchWordsPerWarp, &tmC);
+          else
+            epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
+                                 scratch_all + (warp - 4) * L::kScratchWordsPerWarp);
         }
         tc_fence_before();
         __syncwarp();

@@ -15,12 +15,14 @@ int num_sms();
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                    uint32_t box_rows);
 
+int make_tmap_bf16_store(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems);
+
 int make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                   uint32_t box_rows);
 
 template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched, const Epi& epi, int grid,
-                cudaStream_t st) {
+                cudaStream_t st, const CUtensorMap* tc = nullptr) {
   auto kern = k_umma_gemm<BN, STAGES, Sched, Epi, Kind>;
   const int smem = GemmSmem<BN, STAGES>::kBytes;
   static bool configured = false;  // one attribute call per instantiation
@@ -29,7 +31,8 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched
     configured = true;
   }
   if (grid < 1) grid = 1;
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi);
+  CUtensorMap none{};
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi, tc ? *tc : none);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
