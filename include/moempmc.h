@@ -145,6 +145,17 @@ MP_API int mp_sru_project(const void* x_bf16, const void* w_cat, const float* b_
                           size_t ws_bytes, void* stream);
 MP_API int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16, float* c_last,
                        int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
+/* Token-sharded SRU (one sequence split over G ranks): each rank runs
+ * mp_sru_project on its rows, mp_sru_scan_total (chunk maps + carries from 0; tot =
+ * [A (d) | B (d)], the shard's whole-range affine map c_end = A c_start + B), all-gathers
+ * tot (2d fp32 per rank), folds the lower ranks' maps with mp_sru_fold_carry
+ * (tots: G x 2d, c0 = the sequence's initial state or NULL) and finishes with
+ * mp_sru_scan_finish from that carry. Equals the unsharded layer up to fp32
+ * re-association of the carry. */
+MP_API int mp_sru_scan_total(int T, int d, float* tot, void* ws, size_t ws_bytes, void* stream);
+MP_API int mp_sru_fold_carry(const float* tots, int rank, int d, const float* c0, float* carry_in, void* stream);
+MP_API int mp_sru_scan_finish(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16,
+                              float* c_last, int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream);
 /* c0 (d floats, NULL = zeros, src/predictor.py:190) is the cell state entering token 0 --
  * sru_cell's c_prev, or the carry of a preceding token shard; c_last (nullable) receives the
  * cell state after the last token. nonfinite (1 int) is OR-ed with 1 on NaN/inf state

@@ -50,6 +50,9 @@ SIGNATURES: dict[str, tuple] = {
     "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_sru_project": (_I, [_P, _P, _P, _I, _I, _P, _Z, _P]),
     "mp_sru_scan": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_sru_scan_total": (_I, [_I, _I, _P, _P, _Z, _P]),
+    "mp_sru_fold_carry": (_I, [_P, _I, _I, _P, _P, _P]),
+    "mp_sru_scan_finish": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_sparsemax_rows": (_I, [_P, _I, _I, _P, _P]),
     "mp_segments_workspace_bytes": (_Z, [_I, _I]),
     "mp_segments_from_slots": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _Z, _P]),

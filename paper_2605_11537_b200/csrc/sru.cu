@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(64) k_scan_aggregate(const __nv_bfloat16* __re
 constexpr int kCarryGroups = 16;
 constexpr int kCarryBatch = 16;
 __global__ void __launch_bounds__(32 * kCarryGroups) k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
-                             const float* __restrict__ c0, float* __restrict__ carry) {
+                             const float* __restrict__ c0, float* __restrict__ carry, float* __restrict__ tot) {
   __shared__ float sA[kCarryGroups][32], sB[kCarryGroups][32], sC[kCarryGroups][32];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
@@ -110,9 +110,15 @@ __global__ void __launch_bounds__(32 * kCarryGroups) k_scan_carry(const float* _
   __syncthreads();
   if (g == 0) {
     float run = (act && c0) ? c0[c] : 0.f;
+    float all = 1.f;
     for (int h = 0; h < kCarryGroups; ++h) {
       sC[h][cl] = run;
       run = fmaf(sA[h][cl], run, sB[h][cl]);
+      all *= sA[h][cl];
+    }
+    if (tot && act) {  // the whole range as one affine map c_end = all * c_start + (c_end from c_start = 0)
+      tot[c] = all;
+      tot[d + c] = run;
     }
   }
   __syncthreads();
@@ -227,6 +233,17 @@ __global__ void __launch_bounds__(64) k_scan_output(const __nv_bfloat16* __restr
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+// carry into shard `rank` of a token-sharded sequence: fold the shards' whole-range maps
+// tots[g] = (A_g [d], B_g [d]) of shards g < rank onto c = c0 (or 0).
+__global__ void k_sru_fold(const float* __restrict__ tots, int rank, int d, const float* __restrict__ c0,
+                           float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  float run = c0 ? c0[c] : 0.f;
+  for (int g = 0; g < rank; ++g) run = fmaf(tots[(size_t)g * 2 * d + c], run, tots[(size_t)g * 2 * d + d + c]);
+  out[c] = run;
+}
+
 // sparsemax rows (src/predictor.py:198-209) in float64, one thread per row:
 // insertion-sort descending into local memory, sorted-threshold tau.
 __global__ void k_sparsemax(const double* __restrict__ z, int n, int E, double* __restrict__ out) {
@@ -310,7 +327,43 @@ extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, fl
   // K2: chunk aggregates | carries (from c0) | replay + highway
   const dim3 gq(cdiv(d / 4, 64), nch);
   k_scan_aggregate<<<gq, 64, 0, st>>>(w.ufr, T, d, w.aggA, w.aggB);
-  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, c0, w.carry);
+  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, c0, w.carry, nullptr);
+  k_scan_output<<<gq, 64, 0, st>>>(w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+// Token-sharded SRU: every rank projects its own rows, then
+//   mp_sru_scan_total   pass A + carries from 0; tot (2d) = the shard's whole-range map
+//   (all-gather tot over ranks; mp_sru_fold_carry -> this shard's carry-in)
+//   mp_sru_scan_finish  carries from carry-in + replay (pass A results reused from ws)
+extern "C" int mp_sru_scan_total(int T, int d, float* tot, void* ws, size_t ws_bytes, void* stream) {
+  SRU_CHECKS();
+  cudaStream_t st = (cudaStream_t)stream;
+  const SruWs w(ws, T, d);
+  const int nch = cdiv(T, kScanChunk);
+  const dim3 gq(cdiv(d / 4, 64), nch);
+  k_scan_aggregate<<<gq, 64, 0, st>>>(w.ufr, T, d, w.aggA, w.aggB);
+  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, nullptr, w.carry, tot);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_sru_fold_carry(const float* tots, int rank, int d, const float* c0, float* carry_in, void* stream) {
+  MP_REQUIRE(rank >= 0 && d >= 1, MP_ERR_CONFIG, "mp_sru_fold_carry: bad rank/d");
+  k_sru_fold<<<cdiv(d, 256), 256, 0, (cudaStream_t)stream>>>(tots, rank, d, c0, carry_in);
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_sru_scan_finish(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16,
+                                  float* c_last, int32_t* nonfinite, void* ws, size_t ws_bytes, void* stream) {
+  SRU_CHECKS();
+  cudaStream_t st = (cudaStream_t)stream;
+  const SruWs w(ws, T, d);
+  const int nch = cdiv(T, kScanChunk);
+  const dim3 gq(cdiv(d / 4, 64), nch);
+  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, c0, w.carry, nullptr);
   k_scan_output<<<gq, 64, 0, st>>>(w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;

@@ -359,12 +359,43 @@ class MoEPipeline:
         self.ws_ghist_n = _lib.size_query("mp_histogram_workspace_bytes", cfg.num_layers, GT, cfg.num_experts)
         self.ws_ghist = torch.empty(self.ws_ghist_n, dtype=torch.uint8, device=self.dev)
 
+    def predict_sharded(self, x: torch.Tensor, sp: int) -> int:
+        """Predictor over a token-sharded batch: the G ranks' token ranges are ONE sequence
+        (the reference scans the whole batch, src/predictor.py:175-195). Per SRU layer each
+        rank projects its rows, reduces its range to one affine carry map (2d fp32),
+        all-gathers the maps, folds the lower ranks' maps into its carry-in and replays
+        from it."""
+        import torch.distributed as dist
+
+        cfg, T, d = self.cfg, self.cfg.tokens, self.dp
+        if getattr(self, "sru_tot", None) is None:
+            self.sru_tot = torch.empty(2 * d, device=self.dev)
+            self.sru_tots = torch.empty(self.world, 2 * d, device=self.dev)
+            self.sru_carry_in = torch.empty(d, device=self.dev)
+        _lib.call("mp_f32_to_bf16", ptr(x), ptr(self.x16), T * d, sp)
+        n = 1
+        cur32, cur16 = x, self.x16
+        for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
+            h32, h16 = self.h32[i % 2], self.h16[i % 2]
+            _lib.call("mp_sru_project", ptr(cur16), ptr(W), ptr(B), T, d, ptr(self.ws_sru), self.ws_sru_n, sp)
+            _lib.call("mp_sru_scan_total", T, d, ptr(self.sru_tot), ptr(self.ws_sru), self.ws_sru_n, sp)
+            parts = list(self.sru_tots.unbind(0))
+            dist.all_gather(parts, self.sru_tot, group=self.group)
+            _lib.call("mp_sru_fold_carry", ptr(self.sru_tots), self.rank, d, None, ptr(self.sru_carry_in), sp)
+            _lib.call("mp_sru_scan_finish", ptr(cur32), T, d, ptr(self.sru_carry_in), ptr(h32), ptr(h16), None,
+                      ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
+            n += 6
+            cur32, cur16 = h32, h16
+        _lib.call("mp_heads_argmax", ptr(cur16), ptr(self.sru.heads), T, d, cfg.num_layers, cfg.num_experts,
+                  self.sru.Eg, ptr(self.assign), sp)
+        return n + 1
+
     def step_ep(self, x: torch.Tensor, events=None) -> int:
         import torch.distributed as dist
 
         cfg, L, T, E = self.cfg, self.cfg.num_layers, self.cfg.tokens, self.cfg.num_experts
         sp = stream_ptr()
-        n = self.predict(x, sp)
+        n = self.predict_sharded(x, sp) if self.world > 1 else self.predict(x, sp)
         parts = list(self.g_assign.view(L, self.world, T).unbind(1))
         if self.world > 1:
             gathered = [torch.empty(L, T, dtype=torch.int32, device=self.dev) for _ in range(self.world)]

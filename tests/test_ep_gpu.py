@@ -74,3 +74,45 @@ def test_expert_parallel_single_rank_equals_dense_forward():
     ep.forward(x_ep)
     torch.cuda.synchronize()
     assert torch.equal(x_ep, x_ref)
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_token_sharded_sru_equals_whole_sequence(G):
+    """the G ranks' token ranges are one SRU sequence. Each simulated rank
+    projects its rows, reduces them to one carry map, the maps are 'all-gathered' (here:
+    stacked), folded into each rank's carry-in, and the replay from it must reproduce the
+    unsharded layer (fp32 carry re-association only)."""
+    dev = require_device()
+    T, d = 256 * G * 2, 256
+    g = torch.Generator(device=dev).manual_seed(G)
+    x = torch.randn(T, d, device=dev, generator=g) * 0.5
+    xb = x.bfloat16()
+    w = (torch.randn(3 * d, d, device=dev, generator=g) / d ** 0.5).bfloat16()
+    b = torch.randn(3 * d, device=dev, generator=g) * 0.1
+    nf = torch.zeros(1, dtype=torch.int32, device=dev)
+    n = _lib.size_query("mp_sru_workspace_bytes", T, d)
+    ws = torch.empty(n, dtype=torch.uint8, device=dev)
+    h_ref = torch.empty(T, d, device=dev)
+    h16 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+    _lib.call("mp_sru_layer", ptr(xb), ptr(x), ptr(w), ptr(b), T, d, None, ptr(h_ref), ptr(h16), None, ptr(nf),
+              ptr(ws), n, stream_ptr())
+    Tg = T // G
+    ng = _lib.size_query("mp_sru_workspace_bytes", Tg, d)
+    wss = [torch.empty(ng, dtype=torch.uint8, device=dev) for _ in range(G)]
+    tots = torch.empty(G, 2 * d, device=dev)
+    for r in range(G):  # every rank: project + whole-range map
+        rows = slice(r * Tg, (r + 1) * Tg)
+        _lib.call("mp_sru_project", ptr(xb[rows]), ptr(w), ptr(b), Tg, d, ptr(wss[r]), ng, stream_ptr())
+        _lib.call("mp_sru_scan_total", Tg, d, ptr(tots[r]), ptr(wss[r]), ng, stream_ptr())
+    h = torch.empty(T, d, device=dev)
+    hb = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+    cin = torch.empty(d, device=dev)
+    for r in range(G):  # after the all-gather: fold + replay
+        rows = slice(r * Tg, (r + 1) * Tg)
+        _lib.call("mp_sru_fold_carry", ptr(tots), r, d, None, ptr(cin), stream_ptr())
+        _lib.call("mp_sru_scan_finish", ptr(x[rows]), Tg, d, ptr(cin), ptr(h[rows]), ptr(hb[rows]), None, ptr(nf),
+                  ptr(wss[r]), ng, stream_ptr())
+    torch.cuda.synchronize()
+    rel = ((h - h_ref).abs().max() / h_ref.abs().max()).item()
+    assert rel < 1e-5, rel
+    assert int(nf.item()) == 0
