@@ -353,3 +353,47 @@ def evaluate_accuracy(predicted, oracle) -> float:
     if pred.shape != oracle.shape:
         raise ConfigurationError(f"shape mismatch: predicted {pred.shape} vs oracle {oracle.shape}")
     return float(np.mean(pred == oracle))
+
+
+# ---------------------------------------------------------------- parameter files
+SRU_PARAMS_FORMAT_VERSION = "1"
+
+
+def save_sru_params(params: SruParams, path) -> None:
+    """``moesim-sru-params v1`` (src/predictor.py:400-420): float64 rows, 17 significant digits."""
+    from .workload import fmt_f64
+
+    out = [f"moesim-sru-params v{SRU_PARAMS_FORMAT_VERSION} sru_layers={params.num_sru_layers} "
+           f"moe_layers={params.num_moe_layers} experts={params.num_experts} d_model={params.d_model}"]
+    for i, lay in enumerate(params.layers):
+        for tag, t in (("w", lay.w), ("wf", lay.w_f), ("wr", lay.w_r), ("bf", lay.b_f.reshape(1, -1)),
+                       ("br", lay.b_r.reshape(1, -1))):
+            out.extend(f"{tag}{i} " + " ".join(fmt_f64(v) for v in row) for row in t)
+    for l in range(params.num_moe_layers):
+        out.extend(f"head{l} " + " ".join(fmt_f64(v) for v in row) for row in params.heads[l])
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("\n".join(out) + "\n")
+
+
+def load_sru_params(path) -> SruParams:
+    """Inverse of save_sru_params (src/predictor.py:423-468), same TraceParseError cases."""
+    from .errors import TraceParseError
+    from .workload import parse_param_header, read_rows
+
+    with open(path, encoding="utf-8") as fh:
+        h = parse_param_header(fh.readline(), "moesim-sru-params", ("sru_layers", "moe_layers", "experts", "d_model"))
+        d = h["d_model"]
+        ln = [1]
+        layers = [SruLayerParams(w=read_rows(fh, f"w{i}", d, d, ln), w_f=read_rows(fh, f"wf{i}", d, d, ln),
+                                 w_r=read_rows(fh, f"wr{i}", d, d, ln), b_f=read_rows(fh, f"bf{i}", 1, d, ln)[0],
+                                 b_r=read_rows(fh, f"br{i}", 1, d, ln)[0])
+                  for i in range(h["sru_layers"])]
+        heads = np.stack([read_rows(fh, f"head{l}", h["experts"], d, ln) for l in range(h["moe_layers"])])
+        if fh.readline():
+            raise TraceParseError("trailing data after parameter rows", line=ln[0] + 1)
+    return SruParams(layers=layers, heads=heads)
+
+
+def load_sru_params_device(path, device=None) -> "DeviceSru":
+    """load_sru_params + the device layout the kernels use (bf16 W_cat, fp32 b_cat, heads)."""
+    return _device_sru(load_sru_params(path), device or require_device())

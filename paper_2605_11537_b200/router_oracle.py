@@ -334,3 +334,42 @@ def moe_forward(batch, params: ToyMoeParams, placement=DENSE_BASELINE) -> np.nda
     else:
         _run_layers_device(x, dm, placement=_validated_placement(placement, params, T, dev))
     return x[:, : params.d_model].cpu().numpy()
+
+
+# ---------------------------------------------------------------- parameter files
+PARAMS_FORMAT_VERSION = "1"
+
+
+def save_params(params: ToyMoeParams, path) -> None:
+    """``moesim-moe-params v1`` (src/router_oracle.py:184-206): one float32 tensor row per line."""
+    from .workload import fmt_f32
+
+    out = [f"moesim-moe-params v{PARAMS_FORMAT_VERSION} layers={params.num_layers} experts={params.num_experts} "
+           f"d_model={params.d_model} d_ff={params.d_ff}"]
+    for name, t in (("router", params.router_weights), ("expert_u", params.expert_u), ("expert_v", params.expert_v)):
+        out.extend(name + " " + " ".join(fmt_f32(v) for v in row) for row in t.reshape(-1, t.shape[-1]))
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.write("\n".join(out) + "\n")
+
+
+def load_params(path) -> ToyMoeParams:
+    """Inverse of save_params (src/router_oracle.py:209-251), same TraceParseError cases."""
+    from .errors import TraceParseError
+    from .workload import parse_param_header, read_rows
+
+    with open(path, encoding="utf-8") as fh:
+        h = parse_param_header(fh.readline(), "moesim-moe-params", ("layers", "experts", "d_model", "d_ff"))
+        L, E, d, F = h["layers"], h["experts"], h["d_model"], h["d_ff"]
+        ln = [1]
+        t = {}
+        for name, shape, width in (("router", (L, E, d), d), ("expert_u", (L, E, F, d), d),
+                                   ("expert_v", (L, E, d, F), F)):
+            t[name] = read_rows(fh, name, int(np.prod(shape[:-1])), width, ln, np.float32).reshape(shape)
+        if fh.readline():
+            raise TraceParseError("trailing data after parameter rows", line=ln[0] + 1)
+    return ToyMoeParams(router_weights=t["router"], expert_u=t["expert_u"], expert_v=t["expert_v"])
+
+
+def load_params_device(path, device=None) -> "DeviceMoe":
+    """load_params + the device layout the kernels use (split-bf16 router, bf16 K-major experts)."""
+    return _device_moe(load_params(path), device or require_device())

@@ -20,7 +20,7 @@ from pathlib import Path
 
 import numpy as np
 
-REF = sys.argv[1] if len(sys.argv) > 1 else "/root/reference/pkg/src"
+REF = next((a for a in sys.argv[1:] if not a.startswith("--")), "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 sys.dont_write_bytecode = True
 
@@ -253,7 +253,36 @@ def workload_pins():
     return pins
 
 
+def io_files():
+    """Files written by the reference's own writers (moesim-trace v1, moesim-sru-params v1,
+    moesim-moe-params v1: src/workload.py:336-344, src/predictor.py:400-420,
+    src/router_oracle.py:184-206) plus the arrays they hold."""
+    from moesim.predictor import save_sru_params
+    from moesim.router_oracle import save_params
+    from moesim.workload import write_trace
+
+    io = OUT / "io"
+    io.mkdir(exist_ok=True)
+    tr = generate_trace(ModelShape(2, 4, 8, 5), 2, skew=1.2, seed=3)
+    write_trace(tr, io / "trace.txt")
+    sp = init_params(2, 4, 8, num_sru_layers=2, seed=4)
+    save_sru_params(sp, io / "sru_params.txt")
+    mp = random_params(ModelShape(2, 4, 8, 5), d_ff=16, seed=5)
+    save_params(mp, io / "moe_params.txt")
+    arrays = {"emb": np.stack([b.embeddings for b in tr.batches]),
+              "routing": np.stack([b.oracle_routing for b in tr.batches]),
+              "heads": sp.heads, "router": mp.router_weights, "u": mp.expert_u, "v": mp.expert_v}
+    for i, lay in enumerate(sp.layers):
+        for k in ("w", "w_f", "w_r", "b_f", "b_r"):
+            arrays[f"sru{i}_{k}"] = getattr(lay, k)
+    np.savez_compressed(io / "io.npz", **arrays)
+
+
 def main():
+    if "--only-io" in sys.argv:
+        io_files()
+        return
+    io_files()
     (OUT / "planner.json").write_text(json.dumps(planner_cases()))
     (OUT / "placement.json").write_text(json.dumps(placement_cases()))
     (OUT / "exec.json").write_text(json.dumps(exec_cases()))
