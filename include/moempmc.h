@@ -190,6 +190,30 @@ MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w
                             const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
                             void* stream);
 
+/* ------------------------------------------------------------------ predictor training
+ * SRU training on the GPU (reference src/predictor.py:238-379), float64 like the
+ * reference. Layouts: (S sequences, T tokens, d) row-major.
+ *   mp_sru_train_fwd   f = sigma(fpre + b_f), r = sigma(rpre + b_r), c_t = f c_{t-1} + (1 - f) u,
+ *                      g = tanh(c), h = r g + (1 - r) x (caches f, r, c, g)
+ *   mp_sru_train_bwd   reverse-time BPTT of one layer: du, dfp (d f_pre), drp (d r_pre),
+ *                      dh_out = dh (1 - r), per-sequence bias-gradient sums (S x d)
+ *   mp_train_ce        softmax cross-entropy of one MoE layer's head logits (S*T x E):
+ *                      row losses and dlogits = (p - onehot) / S; labels (S, L, T) int64
+ *   mp_train_colsum / mp_train_sum  deterministic reductions; mp_train_axpy y += alpha x;
+ *   mp_train_nonfinite flag |= any non-finite. The dense products are host-issued GEMMs. */
+MP_API int mp_sru_train_fwd(const double* u, const double* fpre, const double* rpre, const double* b_f,
+                            const double* b_r, const double* x, int S, int T, int d, double* f, double* r, double* c,
+                            double* g, double* h, void* stream);
+MP_API int mp_sru_train_bwd(const double* dh, const double* x, const double* u, const double* f, const double* r,
+                            const double* c, const double* g, int S, int T, int d, double* du, double* dfp,
+                            double* drp, double* dh_out, double* bsum_f, double* bsum_r, void* stream);
+MP_API int mp_train_colsum(const double* in, int R, int n, double* out, void* stream);
+MP_API int mp_train_ce(const double* logits, const int64_t* labels, int S, int T, int L, int layer, int E,
+                       double* dlogits, double* row_loss, void* stream);
+MP_API int mp_train_sum(const double* in, int n, double* out, void* stream);
+MP_API int mp_train_axpy(double* y, const double* x, size_t n, double alpha, void* stream);
+MP_API int mp_train_nonfinite(const double* x, size_t n, int32_t* flag, void* stream);
+
 /* ------------------------------------------------------------------ K6 gather + K7 + K8
  * One MoE layer's expert FFNs over replica segments, fused with the ungated
  * residual combine (src/router_oracle.py:101-111, 127-134):

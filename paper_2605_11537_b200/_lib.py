@@ -31,6 +31,7 @@ _P = ctypes.c_void_p
 _I = ctypes.c_int
 _Z = ctypes.c_size_t
 _F = ctypes.c_float
+_D = ctypes.c_double
 
 # name -> (restype, argtypes); mirrors include/moempmc.h
 SIGNATURES: dict[str, tuple] = {
@@ -50,6 +51,13 @@ SIGNATURES: dict[str, tuple] = {
     "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_sru_project": (_I, [_P, _P, _P, _I, _I, _P, _Z, _P]),
     "mp_sru_scan": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_sru_train_fwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "mp_sru_train_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "mp_train_colsum": (_I, [_P, _I, _I, _P, _P]),
+    "mp_train_ce": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "mp_train_sum": (_I, [_P, _I, _P, _P]),
+    "mp_train_axpy": (_I, [_P, _P, _Z, _D, _P]),
+    "mp_train_nonfinite": (_I, [_P, _Z, _P, _P]),
     "mp_sru_scan_total": (_I, [_I, _I, _P, _P, _Z, _P]),
     "mp_sru_fold_carry": (_I, [_P, _I, _I, _P, _P, _P]),
     "mp_sru_scan_finish": (_I, [_P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),

@@ -278,11 +278,47 @@ def io_files():
     np.savez_compressed(io / "io.npz", **arrays)
 
 
+def training_cases():
+    """Gradients and a short training run from the reference itself (src/predictor.py:238-379)."""
+    from moesim.predictor import loss_and_grads, train_predictor
+    from moesim.workload import RoutingTrace
+
+    rng = np.random.default_rng(21)
+    arrays = {}
+    for k, (S, T, d, L, E, nl) in enumerate([(2, 5, 6, 2, 3, 2), (3, 17, 16, 1, 4, 3), (1, 64, 32, 2, 8, 2)]):
+        p = init_params(L, E, d, num_sru_layers=nl, seed=k)
+        x = rng.normal(size=(S, T, d))
+        y = rng.integers(0, E, size=(S, L, T))
+        loss, g = loss_and_grads(p, x, y)
+        arrays[f"g{k}_x"], arrays[f"g{k}_y"], arrays[f"g{k}_loss"] = x, y, np.array(loss)
+        arrays[f"g{k}_meta"] = np.array([S, T, d, L, E, nl, k])
+        arrays[f"g{k}_heads"] = g.heads
+        for i, lay in enumerate(g.layers):
+            for name in ("w", "w_f", "w_r", "b_f", "b_r"):
+                arrays[f"g{k}_{i}_{name}"] = getattr(lay, name)
+    shape = ModelShape(num_layers=2, experts_per_layer=4, d_model=16, batch_size=32)
+    tr = generate_trace(shape, num_batches=12, skew=1.2, seed=9)
+    res = train_predictor(RoutingTrace(shape, tr.batches), epochs=4, learning_rate=0.01, seed=3, num_sru_layers=2,
+                          sequences_per_step=5)
+    arrays["t_emb"] = np.stack([b.embeddings for b in tr.batches])
+    arrays["t_lab"] = np.stack([b.oracle_routing for b in tr.batches])
+    arrays["t_curve"] = np.array(res.loss_curve)
+    arrays["t_heads"] = res.params.heads
+    for i, lay in enumerate(res.params.layers):
+        for name in ("w", "w_f", "w_r", "b_f", "b_r"):
+            arrays[f"t_{i}_{name}"] = getattr(lay, name)
+    np.savez_compressed(OUT / "train.npz", **arrays)
+
+
 def main():
     if "--only-io" in sys.argv:
         io_files()
         return
+    if "--only-train" in sys.argv:
+        training_cases()
+        return
     io_files()
+    training_cases()
     (OUT / "planner.json").write_text(json.dumps(planner_cases()))
     (OUT / "placement.json").write_text(json.dumps(placement_cases()))
     (OUT / "exec.json").write_text(json.dumps(exec_cases()))

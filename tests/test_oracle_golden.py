@@ -177,3 +177,24 @@ def test_config1_end_to_end(meta):
     assign, hidden = O.predict_assignment(tr[0][0], layers, heads)
     np.testing.assert_allclose(hidden, z["cfg1_pred_hidden"], rtol=1e-10, atol=1e-12)
     assert (assign == z["cfg1_pred_assign"]).all()
+
+
+def test_training_oracle_matches_reference_bitwise():
+    """oracle/training_oracle.py == the reference's loss_and_grads / train_predictor
+    (tests/golden/train.npz), bit for bit."""
+    from oracle import training_oracle as TO
+    from oracle.moesim_oracle import init_sru_params
+
+    z = np.load(G / "train.npz")
+    for k in range(3):
+        S, T, d, L, E, nl, seed = (int(v) for v in z[f"g{k}_meta"])
+        layers, heads = init_sru_params(L, E, d, nl, seed)
+        loss, lg, hg = TO.loss_and_grads(layers, heads, z[f"g{k}_x"], z[f"g{k}_y"])
+        assert loss == float(z[f"g{k}_loss"])
+        assert np.array_equal(hg, z[f"g{k}_heads"])
+        for i in range(nl):
+            for j, n in enumerate(("w", "w_f", "w_r", "b_f", "b_r")):
+                assert np.array_equal(lg[i][j], z[f"g{k}_{i}_{n}"])
+    layers, heads, curve = TO.train_predictor(z["t_emb"], z["t_lab"], 2, 4, 16, 4, 0.01, 3, 2, 5)
+    assert np.array_equal(np.array(curve), z["t_curve"])
+    assert np.array_equal(heads, z["t_heads"])
