@@ -271,24 +271,30 @@ extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E
 }
 
 // ============================================================================
-// Fused, interleaved expert FFN: GEMM1 (relu) and GEMM2 (scatter + residual) of
-// every piece in ONE persistent launch, with the hidden activations H kept in
-// an L2-resident ring of 128-row slots instead of a T x F HBM buffer.
+// Fused expert FFN: GEMM1 (relu) and GEMM2 (scatter + residual) of every piece in
+// ONE persistent launch, the hidden activations H kept in an L2-resident ring of
+// 128-row slots instead of a T x F HBM buffer (activation traffic costs ~54 us per
+// layer at T = 16k when H goes through HBM: tools/ffn_ab.py, FFN_T=4096 vs 16384).
 //
-// Unit order (static round-robin over CTAs, every role walks the same list):
-//   group q = [12 GEMM1 units of piece q (BN slices of F)] +
-//             [ 3 GEMM2 units of piece q - kLag (BN slices of d)]
-// Piece p's H rows live in ring slot p % kSlots (kSlots > kLag). Dependencies
-// both point to EARLIER groups, so the persistent schedule cannot deadlock:
-//   GEMM2(p) waits done1[p] == n_tiles1   (H of piece p complete)  -- group p + kLag
-//   GEMM1(p) waits done2[p - kSlots] == n_tiles2 (slot free again)  -- group p - kSlots + kLag
+// Work list (static round-robin over CTAs, every role walks the same list): the
+// pieces (expert order) are cut into chunks of f.chunk consecutive pieces, and
+//   G1(0) G1(1) G2(0) G1(2) G2(1) ... G1(C-1) G2(C-2) G2(C-1)
+// where inside a segment the units are expert-major, then BN slice, then piece --
+// the order of the two-launch path, so CTAs running at the same time still share
+// one weight tile through L2. Piece p's H rows live in ring slot p % (3 f.chunk)
+// (3 chunks: the slot's previous occupant is two segments older).
+// Dependencies point to EARLIER list positions only, so the persistent schedule
+// cannot deadlock:
+//   GEMM2(p) waits done1[p] == n_tiles1                (H of piece p complete)
+//   GEMM1(p) waits done2[p - 3 f.chunk] == n_tiles2     (ring slot drained)
 // Writers publish with __threadfence + atomicAdd after a named barrier of the
 // epilogue warps; readers acquire, then fence.proxy.async before TMA reads.
 // ============================================================================
 namespace mp {
 
-constexpr int kFfnLag = 16;
-constexpr int kFfnSlots = 48;
+constexpr int kFfnChunkMax = 32;          // pieces per chunk (runtime f.chunk <= this)
+constexpr int kFfnSlots = 3 * kFfnChunkMax;  // ring capacity (the schedule uses 3 * f.chunk slots)
+constexpr int kFfnMaxE = 1024;
 
 struct FfnFused {
   const int32_t* piece_row;
@@ -302,7 +308,11 @@ struct FfnFused {
   int ldx;
   int32_t* done1;
   int32_t* done2;
-  int P_unused;
+  int chunk;  // pieces per chunk; slots = 3 * chunk
+  // shared-memory tables (set in the kernel prologue)
+  const int* eb;    // exp_begin copy (E + 1)
+  const int* seg;   // unit prefix over segments (nseg + 1)
+  int P, nseg;
 };
 
 struct FUnit {
@@ -310,45 +320,74 @@ struct FUnit {
   int p, e, nt, rows, a_row, b_row;
 };
 
-__device__ __forceinline__ int ffn_num_pieces(const FfnFused& f) { return f.exp_begin[f.E]; }
+// prologue (all threads): tables in smem; returns the number of units
+__device__ int ffn_prepare(FfnFused& f, int* s_eb, int* s_seg) {
+  for (int e = threadIdx.x; e <= f.E; e += blockDim.x) s_eb[e] = f.exp_begin[e];
+  __syncthreads();
+  const int P = s_eb[f.E];
+  const int C = (P + f.chunk - 1) / f.chunk;
+  const int nseg = 2 * C;
+  if (threadIdx.x == 0) {
+    int acc = 0, k = 0;
+    auto push = [&](int c, int per) {
+      s_seg[k++] = acc;
+      acc += (min(P, (c + 1) * f.chunk) - c * f.chunk) * per;
+    };
+    for (int c = 0; c < C; ++c) {
+      push(c, f.nt1);  // segment 2c: G1(c)
+      if (c >= 1) push(c - 1, f.nt2);  // segment 2c + 1: G2(c - 1)
+    }
+    if (C >= 1) push(C - 1, f.nt2);
+    s_seg[k] = acc;
+  }
+  __syncthreads();
+  f.eb = s_eb;
+  f.seg = s_seg;
+  f.P = P;
+  f.nseg = nseg;
+  return nseg > 0 ? s_seg[nseg] : 0;
+}
 
 __device__ __forceinline__ FUnit ffn_unit(const FfnFused& f, int u) {
-  const int per = f.nt1 + f.nt2;
-  const int q = u / per, local = u - q * per;
-  const int P = ffn_num_pieces(f);
-  FUnit U;
-  U.kind = -1;
-  int p, nt;
-  if (local < f.nt1) {
-    p = q;
-    nt = local;
-    if (p >= P) return U;
-    U.kind = 0;
-  } else {
-    p = q - kFfnLag;
-    nt = local - f.nt1;
-    if (p < 0 || p >= P) return U;
-    U.kind = 1;
+  int lo = 0, hi = f.nseg;  // segment: seg[lo] <= u < seg[lo + 1]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (f.seg[mid] <= u) lo = mid; else hi = mid;
   }
-  U.rows = f.piece_rows[p];
+  // segment 0 = G1(0); odd k = G1((k + 1) / 2) except the last; even k >= 2 = G2(k / 2 - 1)
+  const bool last = lo == f.nseg - 1;
+  const int kind = (lo == 0 || ((lo & 1) && !last)) ? 0 : 1;
+  const int c = kind == 0 ? (lo + 1) / 2 : (last ? (f.nseg / 2 - 1) : lo / 2 - 1);
+  const int nt_all = kind == 0 ? f.nt1 : f.nt2;
+  const int a = c * f.chunk, b = min(f.P, a + f.chunk);
+  const int local = u - f.seg[lo];
+  // expert of the unit: largest e with (clamp(eb[e]) - a) * nt_all <= local
+  int el = 0, eh = f.E;
+  while (eh - el > 1) {
+    const int mid = (el + eh) >> 1;
+    const int q = (min(max(f.eb[mid], a), b) - a) * nt_all;
+    if (q <= local) el = mid; else eh = mid;
+  }
+  const int pe0 = min(max(f.eb[el], a), b), pe1 = min(max(f.eb[el + 1], a), b);
+  const int cnt = pe1 - pe0;
+  const int rem = local - (pe0 - a) * nt_all;
+  const int nt = rem / cnt;
+  FUnit U;
+  U.kind = kind;
+  U.p = pe0 + (rem - nt * cnt);
+  U.e = el;
+  U.nt = nt;
+  U.rows = __ldg(&f.piece_rows[U.p]);
   if (U.rows <= 0) {
     U.kind = -1;
     return U;
   }
-  int lo = 0, hi = f.E;  // expert of piece p: exp_begin[lo] <= p < exp_begin[lo + 1]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (f.exp_begin[mid] <= p) lo = mid; else hi = mid;
-  }
-  U.p = p;
-  U.e = lo;
-  U.nt = nt;
-  if (U.kind == 0) {
-    U.a_row = f.piece_row[p];
-    U.b_row = (lo * f.nt1 + nt) * f.kb1 * 256;
+  if (kind == 0) {
+    U.a_row = __ldg(&f.piece_row[U.p]);
+    U.b_row = (el * f.nt1 + nt) * f.kb1 * 256;
   } else {
-    U.a_row = (p % kFfnSlots) * kBlockM;
-    U.b_row = (lo * f.nt2 + nt) * f.kb2 * 256;
+    U.a_row = (U.p % (3 * f.chunk)) * kBlockM;
+    U.b_row = (el * f.nt2 + nt) * f.kb2 * 256;
   }
   return U;
 }
@@ -364,7 +403,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_ffn_fused(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmU,
-                const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmV, FfnFused f) {
+                const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmV, FfnFused f_in) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   constexpr int BN = 256, STAGES = 4;
   using L = GemmSmem<BN, STAGES>;
@@ -394,11 +433,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  FfnFused f = f_in;
+  const int nunits = ffn_prepare(f, reinterpret_cast<int*>(smem + L::kPrepOffset),
+                                 reinterpret_cast<int*>(smem + L::kPrepOffset) + kFfnMaxE + 1);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int nunits = (ffn_num_pieces(f) + kFfnLag) * (f.nt1 + f.nt2);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -412,7 +453,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const CUtensorMap* tb = U.kind == 0 ? &tmU : &tmV;
         const int nkb = U.kind == 0 ? f.kb1 : f.kb2;
         if (U.kind == 0) {
-          const int prev = U.p - kFfnSlots;  // ring slot must be drained by the previous occupant
+          const int prev = U.p - 3 * f.chunk;  // ring slot must be drained by the previous occupant
           if (prev >= 0 && f.piece_rows[prev] > 0)
             while (ld_acquire_gpu(&f.done2[prev]) < f.nt2) __nanosleep(64);
         } else {
@@ -479,7 +520,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c0;
       if (U.kind == 0) {
-        const Unit V{(U.p % kFfnSlots) * kBlockM, U.rows, U.b_row, U.nt * BN};  // H rows -> ring slot
+        const Unit V{(U.p % (3 * f.chunk)) * kBlockM, U.rows, U.b_row, U.nt * BN};  // H rows -> ring slot
         EpiStoreBf16 e{f.ring, f.F, nullptr, 1, 0};
         e.template run<BN / 2>(V, 0, r, taddr, c0, nullptr, scratch);
       } else {
@@ -523,8 +564,13 @@ extern "C" size_t mp_ffn_fused_workspace_bytes(int T, int dp, int Fp, int max_pi
 extern "C" int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* u_tiled, const void* v_tiled,
                             const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
                             const int32_t* exp_begin, int max_pieces, void* ws, size_t ws_bytes, void* stream) {
-  MP_REQUIRE(T >= 1 && E >= 1 && dp % 256 == 0 && Fp % 256 == 0, MP_ERR_CONFIG,
-             "mp_ffn_fused: need dp %% 256 == 0 and Fp %% 256 == 0");
+  MP_REQUIRE(T >= 1 && E >= 1 && E <= kFfnMaxE && dp % 256 == 0 && Fp % 256 == 0, MP_ERR_CONFIG,
+             "mp_ffn_fused: need E <= %d, dp %% 256 == 0 and Fp %% 256 == 0", kFfnMaxE);
+  constexpr int kTable = GemmSmem<256, 4>::kPrepInts;
+  static const int chunk = getenv("MP_FFN_CHUNK") ? std::max(1, std::min(kFfnChunkMax, atoi(getenv("MP_FFN_CHUNK"))))
+                                                  : 32;  // A/B switch (8: 6.22, 16: 5.40, 32: 5.23 ms/step)
+  MP_REQUIRE(2 * ((max_pieces + chunk - 1) / chunk) + 1 + kFfnMaxE + 1 <= kTable, MP_ERR_CONFIG,
+             "mp_ffn_fused: piece capacity %d too large for the schedule table", max_pieces);
   MP_REQUIRE(ws_bytes >= mp_ffn_fused_workspace_bytes(T, dp, Fp, max_pieces), MP_ERR_CONFIG,
              "mp_ffn_fused: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
@@ -544,7 +590,7 @@ extern "C" int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* 
   if (!rc) rc = make_tmap_bf16(&tv, v_tiled, (uint64_t)E * dp * (Fp / 64), 64, 64, 256);
   if (rc) return rc;
   FfnFused f{piece_row, piece_rows, exp_begin, tok_of_row, E, Fp / 256, dp / 256, dp / 64, Fp / 64, Fp, ring,
-             x, dp, done, done + max_pieces, 0};
+             x, dp, done, done + max_pieces, chunk, nullptr, nullptr, 0, 0};
   const int smem = GemmSmem<256, 4>::kBytes;
   static bool configured = false;
   if (!configured) {

@@ -55,7 +55,7 @@ struct GemmSmem {
   static constexpr int kScratchOffset = (kVecOffset + 2 * BN * 4 + 1023) / 1024 * 1024;  // TMA-store boxes
   static constexpr int kScratchWordsPerWarp = 32 * 20;  // 32 rows x (16 + 4 pad) words: store transpose
   static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;  // scheduler table (smem)
-  static constexpr int kPrepInts = 1025;
+  static constexpr int kPrepInts = 2048;
   static constexpr int kBytes = kPrepOffset + kPrepInts * 4 + 1024;  // + alignment slack
 };
 

@@ -17,7 +17,8 @@ from tools.gemm_probe import timeit  # noqa: E402
 def main():
     which, case, flags = sys.argv[1], sys.argv[2], [int(f) for f in sys.argv[3:] if not f.startswith("--")]
     dev = require_device()
-    T, E, d, F = 16384, 128, 768, 3072
+    import os
+    T, E, d, F = int(os.environ.get("FFN_T", 16384)), 128, 768, 3072
     U = (torch.randn(E * F, d, device=dev) / 30).bfloat16()
     V = (torch.randn(E * d, F, device=dev) / 55).bfloat16()
     U0, V0 = U.clone(), V.clone()
