@@ -29,6 +29,12 @@ __device__ __forceinline__ void add_bias32(float* v, const float* __restrict__ b
   }
 }
 
+// *p += v as one L2 vector reduction (no value returned; sm_90+ .v4.f32)
+__device__ __forceinline__ void red_add_v4(float4* p, float4 v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 // Software-pipelined walk over NC accumulator columns: the TMEM load of chunk
 // c+32 is in flight while chunk c is processed. f(c, v[32]) consumes a chunk.
 template <int NC, class F>
@@ -224,15 +230,10 @@ struct EpiScatterAdd {
 #pragma unroll
     for (int it = 0; it < 4; ++it) tt[it] = __shfl_sync(0xffffffffu, tok, it * 8 + (lane >> 2));
     tmem_chunks<NC>(taddr, [&](int c, float* v) {
-      // all 8 residual reads of the chunk are issued up front (independent rows): one
-      // memory latency per chunk instead of one per row group
-      float4 o[2][4];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int it = 0; it < 4; ++it)
-          if (tt[it] >= 0) o[h][it] = *(reinterpret_cast<const float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq);
-      // two 16-column halves: lane = row -> smem, then 8 rows x 64 B per instruction
+      // two 16-column halves: lane = row -> smem, then 8 rows x 64 B per instruction.
+      // The residual update is a vector reduction performed in L2 (red.global.add.v4.f32):
+      // top-1 routing gives every element exactly one addend, so x + y is rounded once,
+      // exactly like a load-add-store, and the order cannot vary.
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -243,14 +244,7 @@ struct EpiScatterAdd {
         for (int it = 0; it < 4; ++it) {
           const int row = it * 8 + (lane >> 2);
           const float4 a = *reinterpret_cast<const float4*>(scratch + row * 20 + pq * 4);
-          if (tt[it] >= 0) {
-            float4 r = o[h][it];
-            r.x += a.x;
-            r.y += a.y;
-            r.z += a.z;
-            r.w += a.w;
-            *(reinterpret_cast<float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq) = r;
-          }
+          if (tt[it] >= 0) red_add_v4(reinterpret_cast<float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq, a);
         }
         __syncwarp();
       }
