@@ -22,7 +22,10 @@ extern "C" int mp_ffn_down_bn(int dp);
 
 namespace mp {
 
-// xperm[row] = bf16(x[tok_of_row[row]]); one warp per row, 8-byte lanes.
+// xperm[row] = bf16(x[tok_of_row[row]]); one warp per row, 8-byte lanes. All of a
+// row's loads are issued before the first store (row length known at compile time
+// for the common widths).
+template <int KQ>  // dp / 4 float4 per row; 0 = runtime
 __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const int32_t* __restrict__ tok_of_row,
                               __nv_bfloat16* __restrict__ xperm) {
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -31,13 +34,29 @@ __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const 
   const int t = __ldg(&tok_of_row[row]);
   const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * dp);
   uint2* dst = reinterpret_cast<uint2*>(xperm + (size_t)row * dp);
-  for (int k = lane; k < dp / 4; k += 32) {
-    const float4 v = __ldg(&src[k]);
-    uint2 w;
-    w.x = pack_bf16x2(v.x, v.y);
-    w.y = pack_bf16x2(v.z, v.w);
-    dst[k] = w;
+  if constexpr (KQ > 0) {
+    constexpr int N = (KQ + 31) / 32;
+    float4 v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (lane + 32 * i < KQ) v[i] = __ldg(&src[lane + 32 * i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (lane + 32 * i < KQ) dst[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x, v[i].y), pack_bf16x2(v[i].z, v[i].w));
+  } else {
+    for (int k = lane; k < dp / 4; k += 32) {
+      const float4 v = __ldg(&src[k]);
+      dst[k] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+    }
   }
+}
+
+static void gather_rows(const float* x, int T, int dp, const int32_t* tok_of_row, __nv_bfloat16* xperm,
+                        cudaStream_t st) {
+  const int grid = cdiv(T * 32, 256);
+  if (dp == 768) k_gather_rows<192><<<grid, 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+  else if (dp == 1024) k_gather_rows<256><<<grid, 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+  else k_gather_rows<0><<<grid, 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
 }
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -238,7 +257,7 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
 extern "C" int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                              size_t ws_bytes, void* stream) {
   FFN_CHECKS();
-  k_gather_rows<<<cdiv(T * 32, 256), 256, 0, (cudaStream_t)stream>>>(x, T, dp, tok_of_row, xperm);
+  gather_rows(x, T, dp, tok_of_row, xperm, (cudaStream_t)stream);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -263,7 +282,7 @@ extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E
                           const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
   FFN_CHECKS();
   cudaStream_t st = (cudaStream_t)stream;
-  k_gather_rows<<<cdiv(T * 32, 256), 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+  gather_rows(x, T, dp, tok_of_row, xperm, st);
   MP_CUDA_TRY(cudaGetLastError());
   int rc = ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, 0, st);
   if (rc) return rc;
@@ -581,7 +600,7 @@ extern "C" int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* 
   p += al(sizeof(__nv_bfloat16) * (size_t)kFfnSlots * kBlockM * Fp);
   int32_t* done = (int32_t*)p;
   MP_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(int32_t) * 2 * (size_t)max_pieces, st));
-  k_gather_rows<<<cdiv(T * 32, 256), 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+  gather_rows(x, T, dp, tok_of_row, xperm, st);
   MP_CUDA_TRY(cudaGetLastError());
   CUtensorMap tx, tu, th, tv;
   int rc = make_tmap_bf16(&tx, xperm, T, dp, dp, kBlockM);
