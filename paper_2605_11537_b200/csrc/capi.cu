@@ -59,6 +59,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
+bool pdl_enabled() {  // opt-in: measured 5.51 vs 5.34 ms/step with PDL edges in the step graph
+  static const bool on = getenv("MP_PDL") != nullptr;
+  return on;
+}
+
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                    uint32_t box_rows) {
   auto enc = get_encode();
@@ -164,6 +169,8 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
 
 namespace mp {
 __global__ void k_f32_to_bf16(const float4* __restrict__ x, uint2* __restrict__ y, size_t n4) {
+  griddep_launch_dependents();
+  griddep_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     const float4 v = x[i];
     y[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
@@ -176,7 +183,7 @@ extern "C" int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream) {
              "mp_f32_to_bf16: n %% 4 != 0 or misaligned");
   const size_t n4 = n / 4;
   const int grid = (int)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
-  if (n4) k_f32_to_bf16<<<grid, 256, 0, (cudaStream_t)stream>>>((const float4*)x, (uint2*)y, n4);
+  if (n4) MP_CUDA_TRY(launch_pdl(k_f32_to_bf16, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const float4*)x, (uint2*)y, n4));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -4,6 +4,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <utility>
+
 #include "moempmc.h"
 
 namespace mp {
@@ -12,6 +14,16 @@ constexpr int kChunk = 128;       // tokens per rank/histogram chunk (= GEMM M t
 constexpr int kBlockMRows = 128;  // rows per GEMM M tile (pieces in split_m mode)
 
 __host__ __device__ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// Programmatic dependent launch: let the next kernel in the stream start launching
+// (its CTAs fill SMs as ours retire and run their prologue), and block until the
+// previous kernel has completed and its writes are visible. Both are no-ops when the
+// launch carries no programmatic dependency.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 
 // Block-wide inclusive sum for up to 1024 threads (blockDim multiple of 32).
 __device__ inline int block_sum(int v, int* red /* >= 32 ints smem */) {
@@ -99,6 +111,28 @@ struct RouterWs {
     list = count + 1;
   }
 };
+
+// Kernel launch with programmatic stream serialization (PDL) allowed: inside a CUDA
+// graph this becomes a programmatic edge, so the kernel's launch and prologue overlap
+// the previous kernel's tail; every kernel calls griddep_wait() before touching data
+// a predecessor produced. Opt-in with MP_PDL=1: in the whole-step CUDA graph the
+// programmatic edges measured slower (5.51 vs 5.34 ms/step), so plain edges are default.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace mp
 

@@ -43,6 +43,8 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
                           int32_t* __restrict__ recv_counts, int32_t* __restrict__ num_local_rows,
                           int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
                           int32_t* __restrict__ exp_begin, int32_t* __restrict__ err) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int sm[];
   __shared__ int red[40];
   int* s_off = sm;                   // E + 1
@@ -149,6 +151,8 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
 // Sender: global rank -> slot -> send position; one thread per token (chunked stable rank).
 __global__ void k_ep_send_pos(const int32_t* __restrict__ route, int T, int E, int nch, const int32_t* __restrict__ cc,
                               EpPlanWs w, int32_t* __restrict__ send_pos) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ int se[kChunk];
   const int ch = blockIdx.x;
   const int t = ch * kChunk + threadIdx.x;
@@ -168,6 +172,8 @@ __global__ void k_ep_send_pos(const int32_t* __restrict__ route, int T, int E, i
 // sendbuf[send_pos[t]] = bf16(x[t]); one warp per token.
 __global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32_t* __restrict__ send_pos,
                           __nv_bfloat16* __restrict__ sendbuf) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T) return;
   const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * d);
@@ -182,6 +188,8 @@ __global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32
 // Receiver: local row of every received row, per (source, hosted slot) run. grid G.
 __global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ num_slots_p, int rank, EpPlanWs w,
                               int32_t* __restrict__ recv_of_local) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int g = blockIdx.x;
   const int ns = *num_slots_p;
   for (int s = 0; s < ns; ++s) {
@@ -195,6 +203,8 @@ __global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ 
 // xperm[row] = buf[idx[row]] for bf16 rows; one warp per row.
 __global__ void k_gather_bf16(const __nv_bfloat16* __restrict__ buf, int n, int d, const int32_t* __restrict__ idx,
                               __nv_bfloat16* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= n) return;
   const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)__ldg(&idx[row]) * d);
@@ -205,6 +215,8 @@ __global__ void k_gather_bf16(const __nv_bfloat16* __restrict__ buf, int n, int 
 // x[t] += yback[send_pos[t]] (fp32; each token owns one row -> no atomics). one warp per token.
 __global__ void k_ep_combine(float* __restrict__ x, int T, int d, const float* __restrict__ yback,
                              const int32_t* __restrict__ send_pos) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (t >= T) return;
   float4* dst = reinterpret_cast<float4*>(x + (size_t)t * d);

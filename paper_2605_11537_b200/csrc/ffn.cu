@@ -28,6 +28,8 @@ namespace mp {
 template <int KQ>  // dp / 4 float4 per row; 0 = runtime
 __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const int32_t* __restrict__ tok_of_row,
                               __nv_bfloat16* __restrict__ xperm) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= T) return;
@@ -51,18 +53,20 @@ __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const 
   }
 }
 
-static void gather_rows(const float* x, int T, int dp, const int32_t* tok_of_row, __nv_bfloat16* xperm,
-                        cudaStream_t st) {
-  const int grid = cdiv(T * 32, 256);
-  if (dp == 768) k_gather_rows<192><<<grid, 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
-  else if (dp == 1024) k_gather_rows<256><<<grid, 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
-  else k_gather_rows<0><<<grid, 256, 0, st>>>(x, T, dp, tok_of_row, xperm);
+static cudaError_t gather_rows(const float* x, int T, int dp, const int32_t* tok_of_row, __nv_bfloat16* xperm,
+                               cudaStream_t st) {
+  const dim3 grid(cdiv(T * 32, 256)), block(256);
+  if (dp == 768) return launch_pdl(k_gather_rows<192>, grid, block, 0, st, x, T, dp, tok_of_row, xperm);
+  if (dp == 1024) return launch_pdl(k_gather_rows<256>, grid, block, 0, st, x, T, dp, tok_of_row, xperm);
+  return launch_pdl(k_gather_rows<0>, grid, block, 0, st, x, T, dp, tok_of_row, xperm);
 }
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 // dst[g][nt][kb][r][c] = src[g*N + nt*BN + r][kb*64 + c], 16-byte granules.
 __global__ void k_tile_kmajor(const uint4* __restrict__ src, uint4* __restrict__ dst, int G, int N, int K, int BN) {
+  griddep_launch_dependents();
+  griddep_wait();
   const size_t total = (size_t)G * N * K / 8;
   const int kq = K / 8;  // 16-byte granules per source row
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -257,7 +261,7 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
 extern "C" int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                              size_t ws_bytes, void* stream) {
   FFN_CHECKS();
-  gather_rows(x, T, dp, tok_of_row, xperm, (cudaStream_t)stream);
+  MP_CUDA_TRY(gather_rows(x, T, dp, tok_of_row, xperm, (cudaStream_t)stream));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -282,7 +286,7 @@ extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E
                           const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
   FFN_CHECKS();
   cudaStream_t st = (cudaStream_t)stream;
-  gather_rows(x, T, dp, tok_of_row, xperm, st);
+  MP_CUDA_TRY(gather_rows(x, T, dp, tok_of_row, xperm, st));
   MP_CUDA_TRY(cudaGetLastError());
   int rc = ffn_up(T, dp, Fp, E, u, piece_row, piece_rows, exp_begin, xperm, hid, 0, st);
   if (rc) return rc;
@@ -452,6 +456,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  griddep_launch_dependents();
+  griddep_wait();
   FfnFused f = f_in;
   const int nunits = ffn_prepare(f, reinterpret_cast<int*>(smem + L::kPrepOffset),
                                  reinterpret_cast<int*>(smem + L::kPrepOffset) + kFfnMaxE + 1);
@@ -600,7 +606,7 @@ extern "C" int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* 
   p += al(sizeof(__nv_bfloat16) * (size_t)kFfnSlots * kBlockM * Fp);
   int32_t* done = (int32_t*)p;
   MP_CUDA_TRY(cudaMemsetAsync(done, 0, sizeof(int32_t) * 2 * (size_t)max_pieces, st));
-  gather_rows(x, T, dp, tok_of_row, xperm, st);
+  MP_CUDA_TRY(gather_rows(x, T, dp, tok_of_row, xperm, st));
   MP_CUDA_TRY(cudaGetLastError());
   CUtensorMap tx, tu, th, tv;
   int rc = make_tmap_bf16(&tx, xperm, T, dp, dp, kBlockM);

@@ -139,6 +139,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
+  griddep_launch_dependents();
+  griddep_wait();
   Sched sched = sched_in;
   sched.prepare(reinterpret_cast<int*>(smem + L::kPrepOffset));
   tc_fence_before();

@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  griddep_launch_dependents();
+  griddep_wait();
   Sched sched = sched_in;
   sched.prepare(reinterpret_cast<int*>(smem + L::kPrepOffset));
   tc_fence_before();

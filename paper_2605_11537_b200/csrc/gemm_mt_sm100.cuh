@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * kMtBN);
+  griddep_launch_dependents();
+  griddep_wait();
   const int E = sched.E;
   for (int e = threadIdx.x; e < E; e += blockDim.x) pre[e] = sched.units_of(e);
   __syncthreads();

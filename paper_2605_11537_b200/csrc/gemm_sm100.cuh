@@ -19,6 +19,7 @@
 // splits its rows into independent units. Units are assigned to CTAs
 // round-robin (static persistent schedule), so every role walks the same list.
 #pragma once
+#include "common.cuh"
 #include "ptx.cuh"
 
 namespace mp {
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  griddep_wait();  // the prologue above overlapped the previous kernel's tail
   Sched sched = sched_in;
   sched.prepare(reinterpret_cast<int*>(smem + L::kPrepOffset));
   tc_fence_before();

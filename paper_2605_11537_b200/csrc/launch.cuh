@@ -32,8 +32,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched
   }
   if (grid < 1) grid = 1;
   CUtensorMap none{};
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi, tc ? *tc : none);
-  MP_CUDA_TRY(cudaGetLastError());
+  MP_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kGemmThreads), smem, st, ta, tb, sched, epi, tc ? *tc : none));
   return MP_OK;
 }
 

@@ -29,6 +29,8 @@ namespace mp {
 
 // counts per (layer, chunk, expert); grid (nch, L), block kChunk
 __global__ void k_chunk_hist(const int32_t* __restrict__ assign, int T, int E, int nch, int32_t* __restrict__ cc) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int hist[];
   const int l = blockIdx.y, ch = blockIdx.x;
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
@@ -49,6 +51,8 @@ __global__ void k_chunk_hist(const int32_t* __restrict__ assign, int T, int E, i
 // scanned in shared memory, then every run adds its group offset.
 __global__ void __launch_bounds__(1024) k_chunk_prefix_cols(int32_t* __restrict__ cc, int nch, int E,
                                                             int32_t* __restrict__ demand) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ int part[32][33];
   const int l = blockIdx.y;
   const int el = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -94,6 +98,8 @@ __global__ void __launch_bounds__(1024) k_chunk_prefix_cols(int32_t* __restrict_
 // cap_replicas (src/planner.py:36-72) as a closed-form water-fill. grid L, block 1024.
 __global__ void k_cap_replicas(const int32_t* __restrict__ demand, int E, int capacity, int unit,
                                int32_t* __restrict__ caps, int32_t* __restrict__ infeasible) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int sd[];
   __shared__ int red[40];
   const int l = blockIdx.x;
@@ -155,6 +161,8 @@ __global__ void k_place_layer(const int32_t* __restrict__ demand, int E, const i
                               int32_t* __restrict__ cap_eff, int32_t* __restrict__ r_eff,
                               int32_t* __restrict__ off_g, int32_t* __restrict__ offloads,
                               int32_t* __restrict__ fallback, int32_t* __restrict__ num_slots) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int s_cnt[];  // E
   __shared__ int red[40];
   const int l = blockIdx.x;
@@ -214,6 +222,8 @@ __global__ void k_place_rank(const int32_t* __restrict__ assign, int T, int E, i
                              const int32_t* __restrict__ cap_eff, const int32_t* __restrict__ r_eff,
                              const int32_t* __restrict__ off_g, int32_t* __restrict__ token_to_slot,
                              int32_t* __restrict__ token_event) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ int se[kChunk];
   const int l = blockIdx.y, ch = blockIdx.x;
   int e;
@@ -339,6 +349,8 @@ __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_
                              int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
                              int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin, int pieces_stride,
                              int32_t* __restrict__ err) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int sm[];
   __shared__ int red[40];
   exec_layer_body(blockIdx.x, sm, red, demand, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
@@ -367,6 +379,8 @@ __global__ void k_exec_rank(const int32_t* __restrict__ route, int T, int E, int
                             const int32_t* __restrict__ cc, const int32_t* __restrict__ off_g,
                             const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ token_to_slot,
                             int32_t* __restrict__ row_of_token, int32_t* __restrict__ tok_of_row) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ int se[kChunk];
   exec_rank_body(blockIdx.y, blockIdx.x, se, route, T, E, nch, max_slots, cc, off_g, slot_row_g, token_to_slot,
                  row_of_token, tok_of_row);
@@ -385,6 +399,8 @@ __global__ void k_exec_fused(const int32_t* __restrict__ route, int T, int E, in
                              int32_t* __restrict__ exp_begin, int pieces_stride, int32_t* __restrict__ err,
                              int32_t* __restrict__ token_to_slot, int32_t* __restrict__ row_of_token,
                              int32_t* __restrict__ tok_of_row) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int sm[];
   __shared__ int red[40];
   cg::grid_group grid = cg::this_grid();
@@ -426,6 +442,8 @@ __global__ void k_exec_fused(const int32_t* __restrict__ route, int T, int E, in
 __global__ void k_seg_layer(const int32_t* __restrict__ size, const int32_t* __restrict__ slot_expert, int S, int E,
                             int split_m, int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
                             int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin) {
+  griddep_launch_dependents();
+  griddep_wait();
   extern __shared__ int sm[];
   __shared__ int red[40];
   int* s_row = sm;          // S + 1
@@ -470,6 +488,8 @@ __global__ void k_seg_layer(const int32_t* __restrict__ size, const int32_t* __r
 
 __global__ void k_seg_rank(const int32_t* __restrict__ key, int T, int S, int nch, const int32_t* __restrict__ cc,
                            const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ tok_of_row) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ int se[kChunk];
   const int ch = blockIdx.x;
   int s;
@@ -504,8 +524,8 @@ extern "C" int mp_histogram(const int32_t* assign, int L, int T, int E, int32_t*
   const size_t sm = sizeof(int) * (size_t)E;
   MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_histogram: E=%d too large", E);
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm));
-  k_chunk_hist<<<dim3(nch, L), kChunk, sm, st>>>(assign, T, E, nch, cc);
-  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>(cc, nch, E, demand);
+  MP_CUDA_TRY(launch_pdl(k_chunk_hist, dim3(dim3(nch, L)), dim3(kChunk), sm, st, assign, T, E, nch, cc));
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), L)), dim3(1024), 0, st, cc, nch, E, demand));
   MP_CUDA_TRY(cudaGetLastError());
   MP_CUDA_TRY(cudaFreeAsync(cc, st));
   return MP_OK;
@@ -525,8 +545,8 @@ extern "C" int mp_histogram_ws(const int32_t* assign, int L, int T, int E, int32
   const size_t sm = sizeof(int) * (size_t)E;
   MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_histogram_ws: E=%d too large", E);
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm));
-  k_chunk_hist<<<dim3(nch, L), kChunk, sm, st>>>(assign, T, E, nch, (int32_t*)ws);
-  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>((int32_t*)ws, nch, E, demand);
+  MP_CUDA_TRY(launch_pdl(k_chunk_hist, dim3(dim3(nch, L)), dim3(kChunk), sm, st, assign, T, E, nch, (int32_t*)ws));
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), L)), dim3(1024), 0, st, (int32_t*)ws, nch, E, demand));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -539,7 +559,7 @@ extern "C" int mp_cap_replicas(const int32_t* demand, int L, int E, int capacity
   const size_t sm = sizeof(int) * (size_t)E;
   MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_cap_replicas: E=%d too large", E);
   MP_CUDA_TRY(set_smem((const void*)k_cap_replicas, sm));
-  k_cap_replicas<<<L, 1024, sm, st>>>(demand, E, capacity, unit_rows, caps, infeasible);
+  MP_CUDA_TRY(launch_pdl(k_cap_replicas, dim3(L), dim3(1024), sm, st, demand, E, capacity, unit_rows, caps, infeasible));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -573,16 +593,16 @@ extern "C" int mp_place(const int32_t* assign, int L, int T, int E, const int32_
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm));
   MP_CUDA_TRY(set_smem((const void*)k_place_layer, sm));
   if (T > 0) {
-    k_chunk_hist<<<dim3(nch, L), kChunk, sm, st>>>(assign, T, E, nch, cc);
+    MP_CUDA_TRY(launch_pdl(k_chunk_hist, dim3(dim3(nch, L)), dim3(kChunk), sm, st, assign, T, E, nch, cc));
   } else {
     MP_CUDA_TRY(cudaMemsetAsync(cc, 0, sizeof(int32_t) * (size_t)L * nch * E, st));
   }
-  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>(cc, nch, E, dem);
-  k_place_layer<<<L, 1024, sm, st>>>(dem, E, caps, plan_capacity, state_capacity, res, cap_eff, r_eff, off_g,
-                                     offloads, fallback, num_slots);
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), L)), dim3(1024), 0, st, cc, nch, E, dem));
+  MP_CUDA_TRY(launch_pdl(k_place_layer, dim3(L), dim3(1024), sm, st, dem, E, caps, plan_capacity, state_capacity, res, cap_eff, r_eff, off_g,
+                                     offloads, fallback, num_slots));
   if (T > 0)
-    k_place_rank<<<dim3(nch, L), kChunk, 0, st>>>(assign, T, E, nch, cc, cap_eff, r_eff, off_g, token_to_slot,
-                                                  token_event);
+    MP_CUDA_TRY(launch_pdl(k_place_rank, dim3(dim3(nch, L)), dim3(kChunk), 0, st, assign, T, E, nch, cc, cap_eff, r_eff, off_g, token_to_slot,
+                                                  token_event));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -643,12 +663,12 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
   }
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
-  k_chunk_hist<<<dim3(nch, L), kChunk, sm_h, st>>>(route, T, E, nch, cc);
-  k_chunk_prefix_cols<<<dim3(cdiv(E, 32), L), 1024, 0, st>>>(cc, nch, E, dem);
-  k_exec_layer<<<L, 1024, sm_x, st>>>(dem, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row,
-                                      piece_row, piece_rows, exp_begin, pieces_stride, err);
-  k_exec_rank<<<dim3(nch, L), kChunk, 0, st>>>(route, T, E, nch, max_slots, cc, off_g, slot_row, token_to_slot,
-                                               row_of_token, tok_of_row);
+  MP_CUDA_TRY(launch_pdl(k_chunk_hist, dim3(dim3(nch, L)), dim3(kChunk), sm_h, st, route, T, E, nch, cc));
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), L)), dim3(1024), 0, st, cc, nch, E, dem));
+  MP_CUDA_TRY(launch_pdl(k_exec_layer, dim3(L), dim3(1024), sm_x, st, dem, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row,
+                                      piece_row, piece_rows, exp_begin, pieces_stride, err));
+  MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, L)), dim3(kChunk), 0, st, route, T, E, nch, max_slots, cc, off_g, slot_row, token_to_slot,
+                                               row_of_token, tok_of_row));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -675,8 +695,8 @@ extern "C" int mp_segments_from_slots(const int32_t* token_to_slot, const int32_
   MP_REQUIRE(sm_h <= 200 * 1024 && sm_s <= 200 * 1024, MP_ERR_CONFIG, "mp_segments_from_slots: S too large");
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_seg_layer, sm_s));
-  k_chunk_hist<<<dim3(nch, 1), kChunk, sm_h, st>>>(token_to_slot, T, S, nch, cc);
-  k_chunk_prefix_cols<<<dim3(cdiv(S, 32), 1), 1024, 0, st>>>(cc, nch, S, size);
+  MP_CUDA_TRY(launch_pdl(k_chunk_hist, dim3(dim3(nch, 1)), dim3(kChunk), sm_h, st, token_to_slot, T, S, nch, cc));
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(S, 32), 1)), dim3(1024), 0, st, cc, nch, S, size));
   k_seg_layer<<<1, 1024, sm_s, st>>>(size, slot_expert, S, E, split_m, slot_row, piece_row, piece_rows, exp_begin);
   k_seg_rank<<<nch, kChunk, 0, st>>>(token_to_slot, T, S, nch, cc, slot_row, tok_of_row);
   MP_CUDA_TRY(cudaGetLastError());

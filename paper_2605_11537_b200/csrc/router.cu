@@ -20,6 +20,8 @@ constexpr float kRouterEps = 1.f / 4096.f;
 // xhl[t] = [bf16(x) | bf16(x - bf16(x))], xb[t] = sum_k |x_k| * wabs[k]. one warp per token.
 __global__ void k_router_prep(const float* __restrict__ x, int ldx, int T, int d, const float* __restrict__ wabs,
                               __nv_bfloat16* __restrict__ xhl, float* __restrict__ xb, int32_t* __restrict__ count) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count = 0;
@@ -45,6 +47,8 @@ __global__ void k_router_prep(const float* __restrict__ x, int ldx, int T, int d
 __global__ void k_router_recheck(const float* __restrict__ x, int ldx, int d, const float* __restrict__ w, int E,
                                  const int32_t* __restrict__ count, const int32_t* __restrict__ list,
                                  int32_t* __restrict__ route) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -127,6 +131,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * EG < 32 ? 32 : 2 * EG);
+  griddep_wait();  // x is the previous layer's output
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -323,9 +328,8 @@ static int launch_router_fused(const float* x, int ldx, int T, int d, const void
   }
   MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
   const int units = cdiv(T, kBlockM);
-  kern<<<units < num_sms() ? units : num_sms(), kGemmThreads, smem, st>>>(tb, x, ldx, T, d, w_abs, E, route, eps,
-                                                                           count, list);
-  MP_CUDA_TRY(cudaGetLastError());
+  MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, x, ldx,
+                         T, d, w_abs, E, route, eps, count, list));
   return MP_OK;
 }
 
@@ -346,6 +350,8 @@ extern "C" int mp_router_weight_absmax(const float* w_f32, int E, int d, float* 
 
 namespace mp {
 __global__ void k_wabs(const float* __restrict__ w, int E, int d, float* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= d) return;
   float m = 0.f;
@@ -375,7 +381,7 @@ static int route_gemm(const float* x, int ldx, int T, int d, const void* w_hl, c
   else if (Eg == 128) rc = launch_gemm<128, 6>(ta, tb, s, e, grid, st);
   else rc = launch_gemm<64, 8>(ta, tb, s, e, grid, st);
   if (rc) return rc;
-  k_router_recheck<<<num_sms(), 256, 0, st>>>(x, ldx, d, w_f32, E, rw.count, rw.list, route);
+  MP_CUDA_TRY(launch_pdl(k_router_recheck, dim3(num_sms()), dim3(256), 0, st, x, ldx, d, w_f32, E, rw.count, rw.list, route));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -397,7 +403,7 @@ extern "C" int mp_route_top1_ex(const float* x, int ldx, int T, int d, const voi
     int rc = Eg == 128 ? launch_router_fused<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
                        : launch_router_fused<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
     if (rc) return rc;
-    k_router_recheck<<<num_sms(), 256, 0, st>>>(x, ldx, d, w_f32, E, rw.count, rw.list, route);
+    MP_CUDA_TRY(launch_pdl(k_router_recheck, dim3(num_sms()), dim3(256), 0, st, x, ldx, d, w_f32, E, rw.count, rw.list, route));
     MP_CUDA_TRY(cudaGetLastError());
     return MP_OK;
   }

@@ -32,6 +32,8 @@ struct bf16x4 {
 constexpr int kAggDepth = 16;  // tokens of u/f loads in flight per thread
 __global__ void __launch_bounds__(64) k_scan_aggregate(const __nv_bfloat16* __restrict__ ufr, int T, int d,
                                                        float* __restrict__ aggA, float* __restrict__ aggB) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int cq = blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * cq >= d) return;
   const int ch = blockIdx.y;
@@ -78,6 +80,8 @@ constexpr int kCarryGroups = 16;
 constexpr int kCarryBatch = 16;
 __global__ void __launch_bounds__(32 * kCarryGroups) k_scan_carry(const float* __restrict__ aggA, const float* __restrict__ aggB, int nch, int d,
                              const float* __restrict__ c0, float* __restrict__ carry, float* __restrict__ tot) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ float sA[kCarryGroups][32], sB[kCarryGroups][32], sC[kCarryGroups][32];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
@@ -175,6 +179,8 @@ __global__ void __launch_bounds__(64) k_scan_output(const __nv_bfloat16* __restr
                                                     const float* __restrict__ carry, float* __restrict__ h32,
                                                     __nv_bfloat16* __restrict__ h16, float* __restrict__ c_last,
                                                     int32_t* __restrict__ nonfinite) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int cq = blockIdx.x * blockDim.x + threadIdx.x;  // channel quad
   if (4 * cq >= d) return;
   const int ch = blockIdx.y;
@@ -237,6 +243,8 @@ static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 // tots[g] = (A_g [d], B_g [d]) of shards g < rank onto c = c0 (or 0).
 __global__ void k_sru_fold(const float* __restrict__ tots, int rank, int d, const float* __restrict__ c0,
                            float* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d) return;
   float run = c0 ? c0[c] : 0.f;
@@ -247,6 +255,8 @@ __global__ void k_sru_fold(const float* __restrict__ tots, int rank, int d, cons
 // sparsemax rows (src/predictor.py:198-209) in float64, one thread per row:
 // insertion-sort descending into local memory, sorted-threshold tau.
 __global__ void k_sparsemax(const double* __restrict__ z, int n, int E, double* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double srt[256];
@@ -326,9 +336,9 @@ extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, fl
   const int nch = cdiv(T, kScanChunk);
   // K2: chunk aggregates | carries (from c0) | replay + highway
   const dim3 gq(cdiv(d / 4, 64), nch);
-  k_scan_aggregate<<<gq, 64, 0, st>>>(w.ufr, T, d, w.aggA, w.aggB);
-  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, c0, w.carry, nullptr);
-  k_scan_output<<<gq, 64, 0, st>>>(w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
+  MP_CUDA_TRY(launch_pdl(k_scan_aggregate, dim3(gq), dim3(64), 0, st, w.ufr, T, d, w.aggA, w.aggB));
+  MP_CUDA_TRY(launch_pdl(k_scan_carry, dim3(cdiv(d, 32)), dim3(32 * kCarryGroups), 0, st, w.aggA, w.aggB, nch, d, c0, w.carry, nullptr));
+  MP_CUDA_TRY(launch_pdl(k_scan_output, dim3(gq), dim3(64), 0, st, w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -343,8 +353,8 @@ extern "C" int mp_sru_scan_total(int T, int d, float* tot, void* ws, size_t ws_b
   const SruWs w(ws, T, d);
   const int nch = cdiv(T, kScanChunk);
   const dim3 gq(cdiv(d / 4, 64), nch);
-  k_scan_aggregate<<<gq, 64, 0, st>>>(w.ufr, T, d, w.aggA, w.aggB);
-  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, nullptr, w.carry, tot);
+  MP_CUDA_TRY(launch_pdl(k_scan_aggregate, dim3(gq), dim3(64), 0, st, w.ufr, T, d, w.aggA, w.aggB));
+  MP_CUDA_TRY(launch_pdl(k_scan_carry, dim3(cdiv(d, 32)), dim3(32 * kCarryGroups), 0, st, w.aggA, w.aggB, nch, d, nullptr, w.carry, tot));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -363,8 +373,8 @@ extern "C" int mp_sru_scan_finish(const float* x_f32, int T, int d, const float*
   const SruWs w(ws, T, d);
   const int nch = cdiv(T, kScanChunk);
   const dim3 gq(cdiv(d / 4, 64), nch);
-  k_scan_carry<<<cdiv(d, 32), 32 * kCarryGroups, 0, st>>>(w.aggA, w.aggB, nch, d, c0, w.carry, nullptr);
-  k_scan_output<<<gq, 64, 0, st>>>(w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite);
+  MP_CUDA_TRY(launch_pdl(k_scan_carry, dim3(cdiv(d, 32)), dim3(32 * kCarryGroups), 0, st, w.aggA, w.aggB, nch, d, c0, w.carry, nullptr));
+  MP_CUDA_TRY(launch_pdl(k_scan_output, dim3(gq), dim3(64), 0, st, w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -35,6 +35,8 @@ __global__ void k_sru_train_fwd(const double* __restrict__ u, const double* __re
                                 const double* __restrict__ br, const double* __restrict__ x, int S, int T, int d,
                                 double* __restrict__ f, double* __restrict__ r, double* __restrict__ c,
                                 double* __restrict__ g, double* __restrict__ h) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S * d) return;
   const int s = i / d, ch = i - s * d;
@@ -64,6 +66,8 @@ __global__ void k_sru_train_bwd(const double* __restrict__ dh, const double* __r
                                 const double* __restrict__ g, int S, int T, int d, double* __restrict__ du,
                                 double* __restrict__ dfp, double* __restrict__ drp, double* __restrict__ dh_out,
                                 double* __restrict__ bsum_f, double* __restrict__ bsum_r) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= S * d) return;
   const int s = i / d, ch = i - s * d;
@@ -91,6 +95,8 @@ __global__ void k_sru_train_bwd(const double* __restrict__ dh, const double* __r
 
 // out[j] = sum_i in[i][j] in row order (deterministic).
 __global__ void k_train_colsum(const double* __restrict__ in, int R, int n, double* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   double s = 0.0;
@@ -103,6 +109,8 @@ __global__ void k_train_colsum(const double* __restrict__ in, int R, int n, doub
 // labels: element (row) at labels[row * lstride] (one MoE layer of the (S, L, T) array).
 __global__ void k_train_ce(const double* __restrict__ z, const int64_t* __restrict__ labels, int S, int T, int L,
                            int layer, int E, double inv_S, double* __restrict__ dz, double* __restrict__ row_loss) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= S * T) return;
   const int s = row / T, t = row - s * T;
@@ -124,6 +132,8 @@ __global__ void k_train_ce(const double* __restrict__ z, const int64_t* __restri
 
 // Single-block deterministic sum of n doubles (fixed tree over a fixed thread layout).
 __global__ void k_train_sum(const double* __restrict__ in, int n, double* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ double sh[256];
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) s = add(s, in[i]);
@@ -138,12 +148,16 @@ __global__ void k_train_sum(const double* __restrict__ in, int n, double* __rest
 
 // y += alpha * x (SGD step), elementwise without contraction.
 __global__ void k_train_axpy(double* __restrict__ y, const double* __restrict__ x, size_t n, double alpha) {
+  griddep_launch_dependents();
+  griddep_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     y[i] = sub(y[i], mul(-alpha, x[i]));
 }
 
 // flag |= any non-finite among n values
 __global__ void k_train_nonfinite(const double* __restrict__ x, size_t n, int32_t* __restrict__ flag) {
+  griddep_launch_dependents();
+  griddep_wait();
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     if (!isfinite(x[i])) {
       atomicOr(flag, 1);
