@@ -255,26 +255,29 @@ struct EpiScatterAdd {
 // Per-row argmax over column groups of width `group` (first index wins ties,
 // like numpy.argmax). Columns >= valid inside a group are padding.
 // out[g * M + row] for group g = global column / group.
-struct EpiGroupArgmax {
-  static constexpr bool kSplitCols = false;
+// kSplit: the two epilogue warpgroups take one column half each (valid when a group
+// never straddles the halves, i.e. group <= BN / 2 and BN / 2 % group == 0).
+template <bool kSplit>
+struct EpiGroupArgmaxT {
+  static constexpr bool kSplitCols = kSplit;
   int32_t* out;
   int M;
   int group;
   int valid;
   int ngroups;
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
-  template <int BN>
-  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int, const float*,
+  template <int NC>
+  __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float*,
                                       uint32_t*) const {
     const int rr = mt * kBlockM + r;
     const bool ok = rr < U.rows;
     float best = -INFINITY;
     int bi = 0;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 0; c < NC; c += 32) {
       float v[32];
       tmem_ld32(taddr + c, v);
-      const int gc = U.n0 + c;
+      const int gc = U.n0 + c0 + c;
       const int g = gc / group;
       const int base = gc - g * group;
 #pragma unroll
@@ -292,6 +295,8 @@ struct EpiGroupArgmax {
     }
   }
 };
+
+using EpiGroupArgmax = EpiGroupArgmaxT<false>;
 
 // Router epilogue: top-1 plus a certification test. The split-bf16 product is
 // within err_scale * |x|_2 of the exact fp32-input logit; when the top-2 gap is

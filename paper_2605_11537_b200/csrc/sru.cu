@@ -404,6 +404,10 @@ extern "C" int mp_heads_argmax(const void* h_bf16, const void* heads, int T, int
   EpiGroupArgmax e{assign, T, Eg, E, L};
   const int units = cdiv(T, kBlockM) * (N / bn);
   const int grid = units < num_sms() ? units : num_sms();
+  if (bn == 256 && Eg <= 128) {  // one group per column half: both epilogue warpgroups work
+    EpiGroupArgmaxT<true> es{assign, T, Eg, E, L};
+    return launch_gemm<256, 4>(ta, tb, s, es, grid, st);
+  }
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, grid, st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, grid, st);
   return launch_gemm<64, 8>(ta, tb, s, e, grid, st);
