@@ -248,6 +248,9 @@ MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, in
                        const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
                        size_t ws_bytes, void* stream);
 MP_API int mp_ffn_down_bn(int dp);
+/* Diagnostics: per-CTA %globaltimer start / end (ns) of the last grouped-GEMM launch
+ * (host arrays of n <= 1024). */
+MP_API int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1, int n);
 /* One MoE layer's FFN as ONE persistent launch (after a gather): GEMM1 and GEMM2 units
  * of every piece interleaved, the hidden activations living in an L2-resident ring of
  * 128-row slots (never a T x F HBM buffer), device-side completion counters ordering

@@ -269,3 +269,4 @@ extern "C" int mp_l2_persist(void* ptr, size_t bytes, float hit_ratio, void* str
   MP_CUDA_TRY(cudaStreamSetAttribute((cudaStream_t)stream, cudaStreamAttributeAccessPolicyWindow, &attr));
   return MP_OK;
 }
+

@@ -626,3 +626,11 @@ extern "C" int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* 
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
+
+// Diagnostics: per-CTA start/end %globaltimer (ns) of the last grouped-GEMM launch (n <= 1024).
+extern "C" int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1, int n) {
+  MP_REQUIRE(n >= 1 && n <= 1024, MP_ERR_CONFIG, "mp_debug_cta_times: n in [1, 1024]");
+  MP_CUDA_TRY(cudaMemcpyFromSymbol(t0, mp::g_cta_t0, sizeof(unsigned long long) * n));
+  MP_CUDA_TRY(cudaMemcpyFromSymbol(t1, mp::g_cta_t1, sizeof(unsigned long long) * n));
+  return MP_OK;
+}

@@ -46,6 +46,18 @@ struct TmaStoreOf<E, decltype(void(E::kTmaStore))> {
   static constexpr bool value = E::kTmaStore;
 };
 
+// Per-CTA start / end timestamps (%globaltimer, ns) of the last k_umma_gemm launch of
+// this translation unit, for load-balance diagnostics (mp_debug_cta_times reads the
+// copy of ffn.cu, i.e. the grouped expert GEMMs).
+static __device__ unsigned long long g_cta_t0[1024];
+static __device__ unsigned long long g_cta_t1[1024];
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <int BN, int STAGES>
 struct GemmSmem {
   static constexpr int kABytes = kBlockM * kBlockK * 2;
@@ -96,6 +108,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
+    if (blockIdx.x < 1024) g_cta_t0[blockIdx.x] = global_ns();
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) {
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t1[blockIdx.x] = global_ns();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 2 * BN);

@@ -59,7 +59,25 @@ def main():
                 _lib.call("mp_ffn_down", ptr(y), T, d, F, E, ptr(V if fl & 1 else V0), fl, ptr(tor), ptr(prow),
                           ptr(prows), ptr(eb), ptr(ws), fb, stream_ptr())
         print(f"{which} {case} flags={fl}: {timeit(run, iters=10):.1f} us", flush=True)
+        torch.cuda.synchronize()
+        cta_spread(f"  {which} {case}")
     torch.cuda.synchronize()
+
+
+
+def cta_spread(label=""):
+    """Per-CTA start/end spread of the last grouped-GEMM launch (load-balance diagnostic)."""
+    import ctypes
+
+    n = 148
+    t0 = (ctypes.c_ulonglong * n)()
+    t1 = (ctypes.c_ulonglong * n)()
+    _lib.call("mp_debug_cta_times", ctypes.cast(t0, ctypes.c_void_p).value, ctypes.cast(t1, ctypes.c_void_p).value, n)
+    a, b = np.array(t0[:n], dtype=np.float64), np.array(t1[:n], dtype=np.float64)
+    s = a.min()
+    ends = np.sort(b - s) / 1e3
+    print(f"{label} CTA end times (us from first start): min {ends[0]:.1f}  p10 {ends[14]:.1f}  median "
+          f"{ends[74]:.1f}  p90 {ends[133]:.1f}  max {ends[-1]:.1f}; start spread {(a.max() - s) / 1e3:.1f}")
 
 
 if __name__ == "__main__":
