@@ -151,7 +151,7 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
     CUtensorMap tc;
     rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
     if (rc) return rc;
-    EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
+    EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from, 0};
     return launch_gemm<256, 4>(ta, tb, s, et, grid, st, &tc);
   }
   if (c_dtype == 0) {

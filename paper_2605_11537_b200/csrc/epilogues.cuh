@@ -138,6 +138,7 @@ struct EpiStoreBf16Tma {
   const float* bias;
   int act;
   int sig_from;
+  int keep_l2;  // 1: stores carry an L2 evict_last hint (the output is re-read right away)
   __device__ __forceinline__ const float* colvec() const { return bias; }
   template <int NC>
   __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec,
@@ -165,7 +166,10 @@ struct EpiStoreBf16Tma {
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(tm, box, U.n0 + c0 + c, U.a_row + row0);
+          if (keep_l2)
+            tma_store_2d_hint(tm, box, U.n0 + c0 + c, U.a_row + row0, policy_evict_last());
+          else
+            tma_store_2d(tm, box, U.n0 + c0 + c, U.a_row + row0);
           bulk_commit();
         }
       } else if (nvalid > 0) {
