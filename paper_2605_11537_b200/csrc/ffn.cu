@@ -27,13 +27,14 @@ namespace mp {
 // for the common widths).
 template <int KQ>  // dp / 4 float4 per row; 0 = runtime
 __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const int32_t* __restrict__ tok_of_row,
-                              __nv_bfloat16* __restrict__ xperm) {
+                              __nv_bfloat16* __restrict__ xperm, int32_t* __restrict__ done) {
   griddep_launch_dependents();
   griddep_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= T) return;
   const int t = __ldg(&tok_of_row[row]);
+  if (done && lane == 0) done[row] = 0;  // GEMM2's per-piece consumption counters
   const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * dp);
   uint2* dst = reinterpret_cast<uint2*>(xperm + (size_t)row * dp);
   if constexpr (KQ > 0) {
@@ -54,11 +55,11 @@ __global__ void k_gather_rows(const float* __restrict__ x, int T, int dp, const 
 }
 
 static cudaError_t gather_rows(const float* x, int T, int dp, const int32_t* tok_of_row, __nv_bfloat16* xperm,
-                               cudaStream_t st) {
+                               cudaStream_t st, int32_t* done = nullptr) {
   const dim3 grid(cdiv(T * 32, 256)), block(256);
-  if (dp == 768) return launch_pdl(k_gather_rows<192>, grid, block, 0, st, x, T, dp, tok_of_row, xperm);
-  if (dp == 1024) return launch_pdl(k_gather_rows<256>, grid, block, 0, st, x, T, dp, tok_of_row, xperm);
-  return launch_pdl(k_gather_rows<0>, grid, block, 0, st, x, T, dp, tok_of_row, xperm);
+  if (dp == 768) return launch_pdl(k_gather_rows<192>, grid, block, 0, st, x, T, dp, tok_of_row, xperm, done);
+  if (dp == 1024) return launch_pdl(k_gather_rows<256>, grid, block, 0, st, x, T, dp, tok_of_row, xperm, done);
+  return launch_pdl(k_gather_rows<0>, grid, block, 0, st, x, T, dp, tok_of_row, xperm, done);
 }
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -96,7 +97,8 @@ extern "C" int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, i
 }
 
 extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
-  return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp);
+  return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp) +
+         al(sizeof(int32_t) * (size_t)T);
 }
 
 static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, int tiled, int box_rows) {
@@ -217,7 +219,7 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
 
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
-                    const __nv_bfloat16* hid, int flags, cudaStream_t st) {
+                    const __nv_bfloat16* hid, int flags, cudaStream_t st, int32_t* hdone = nullptr) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
   const int tiled = flags & 1, pair = (flags >> 1) & 1, mt = (flags >> 2) & 1;
   const int bn = mp_ffn_down_bn(dp);
@@ -234,7 +236,7 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
   }
   rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
   if (rc) return rc;
-  EpiScatterAdd e{y, dp, tok_of_row};
+  EpiScatterAdd e{y, dp, tok_of_row, nullptr, nullptr, 0, 0};
   if (pair) {
     MP_REQUIRE(bn == 256, MP_ERR_CONFIG, "ffn pair mode needs dp %% 256 == 0");
     Seg2Sched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
@@ -245,6 +247,12 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
     if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, dp / 256, dp, Fp / 64, tiled, e, st);
   }
   SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
+  if ((flags & 16) && hdone) {  // drop each piece's H from L2 after its last slice unit
+    EpiScatterAdd ed{y, dp, tok_of_row, hdone, hid, Fp, dp / bn};
+    if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, ed, num_sms(), st);
+    if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, ed, num_sms(), st);
+    return launch_gemm<64, 8>(ta, tb, s, ed, num_sms(), st);
+  }
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, num_sms(), st);
   return launch_gemm<64, 8>(ta, tb, s, e, num_sms(), st);
@@ -257,13 +265,15 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
   MP_REQUIRE(ws_bytes >= mp_ffn_workspace_bytes(T, dp, Fp), MP_ERR_CONFIG, "ffn: workspace too small");          \
   __nv_bfloat16* xperm = (__nv_bfloat16*)ws;                                                                    \
   __nv_bfloat16* hid = (__nv_bfloat16*)((char*)ws + al(sizeof(__nv_bfloat16) * (size_t)T * dp));                \
+  int32_t* hdone = (int32_t*)((char*)hid + al(sizeof(__nv_bfloat16) * (size_t)T * Fp));                       \
   (void)xperm;                                                                                                  \
-  (void)hid;
+  (void)hid;                                                                                                    \
+  (void)hdone;
 
 extern "C" int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                              size_t ws_bytes, void* stream) {
   FFN_CHECKS();
-  MP_CUDA_TRY(gather_rows(x, T, dp, tok_of_row, xperm, (cudaStream_t)stream));
+  MP_CUDA_TRY(gather_rows(x, T, dp, tok_of_row, xperm, (cudaStream_t)stream, hdone));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }
@@ -280,7 +290,7 @@ extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v
                            const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
   FFN_CHECKS();
   return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags,
-                  (cudaStream_t)stream);
+                  (cudaStream_t)stream, hdone);
 }
 
 extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,

@@ -216,6 +216,8 @@ class MoEPipeline:
         self.ws_fused_n = _lib.size_query("mp_ffn_fused_workspace_bytes", T, d, F, pstride)
         self.ws_fused = ws(self.ws_fused_n) if cfg.ffn == "fused" else None
         self.launches_per_step = None
+        import os
+        self.h_discard = os.environ.get("MP_H_DISCARD") is not None  # opt-in: measured no gain
 
     # ------------------------------------------------------------------ pieces of a step
     def predict(self, x: torch.Tensor, sp: int) -> int:
@@ -326,7 +328,9 @@ class MoEPipeline:
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[1].record(sp)
-        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags, ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
+        # bit 4: GEMM2 drops each piece's H from L2 once consumed (counters zeroed by the gather)
+        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags | (16 if self.h_discard else 0),
+                  ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
                   ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[2].record(sp)

@@ -289,6 +289,13 @@ def test_multicast_cluster_ffn_matches_single_cta(dev, skew, d, F, tiled):
     _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 8)
 
 
+@pytest.mark.parametrize("skew,d,F,tiled", [(1.2, 768, 3072, 1), (3.0, 512, 768, 0), (0.0, 256, 512, 1)])
+def test_hidden_discard_keeps_results(dev, skew, d, F, tiled):
+    """flags bit 4: GEMM2 discards each piece's hidden rows from L2 after its last slice unit;
+    the results must not change (no unit may read H after the discard)."""
+    _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 16)
+
+
 def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
     """Multi-tile units (two accumulator tiles sharing A or B) == the single-tile kernels, bit for bit:
     odd and even piece counts per expert, odd slice counts, empty experts, both weight layouts."""
