@@ -239,6 +239,225 @@ __global__ void __launch_bounds__(64) k_scan_output(const __nv_bfloat16* __restr
 
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Single-pass form of K2 (default): one launch reads u/f/r/x once and writes h once.
+// Block = kSpWarps consecutive 32-token chunks x one strip of 128 channels (lane = 4
+// channels). Blocks take tickets in launch order; a block
+//   1. computes its chunks' affine maps (c_out = A c_in + B) and the block map,
+//   2. publishes the block map (flag 1), looks back over its predecessors in the strip in
+//      windows of 32 (flags read by one warp, maps composed backwards per channel) until a
+//      predecessor with a published inclusive carry (flag 2; block 0 always has one),
+//   3. publishes its own inclusive carry (flag 2), then replays its chunks (u/f re-read hits
+//      L2) and applies the highway output.
+// A block only waits on blocks with smaller tickets, which are already running.
+// Reference: sru_forward (src/predictor.py:177-195); the recurrence is the one of
+// k_scan_aggregate / k_scan_carry / k_scan_output above (same per-step arithmetic).
+constexpr int kSpWarps = 8;
+constexpr int kSpTokens = kSpWarps * kScanChunk;
+constexpr int kSpPF = 2;  // replay: tokens per prefetch group (double buffered)
+constexpr int kSpAgg = 8;  // u/f tokens in flight per thread in step 1
+// 3 blocks per SM (<= 80 registers): all T / 256 x d / 128 blocks of the bench shape resident
+// in one wave (two blocks per SM: 74 us, three: 53 us, four with spills: 65 us).
+
+__device__ __forceinline__ int sp_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sp_st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bfloat16* __restrict__ ufr,
+                                                              const float* __restrict__ x, int T, int d,
+                                                              const float* __restrict__ c0, float* __restrict__ h32,
+                                                              __nv_bfloat16* __restrict__ h16,
+                                                              float* __restrict__ c_last, int32_t* __restrict__ nonfinite,
+                                                              int* flags, float* agg, float* incl, int nblk) {
+  griddep_launch_dependents();
+  griddep_wait();
+  __shared__ float sA[kSpWarps][128], sB[kSpWarps][128];
+  __shared__ float sCin[128];
+  __shared__ int s_ticket, s_lo, s_found;
+  const int nstr = d / 128 + (d % 128 != 0);
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&flags[nstr * nblk], 1);
+  __syncthreads();
+  const int str = s_ticket % nstr, blk = s_ticket / nstr;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cq = str * 32 + lane;
+  const bool act = 4 * cq < d;
+  const int t0 = (blk * kSpWarps + w) * kScanChunk, t1 = min(T, t0 + kScanChunk);
+  const size_t ld3 = (size_t)3 * d;
+  // ---- 1. chunk maps
+  {
+    float a[4] = {1.f, 1.f, 1.f, 1.f}, b[4] = {0.f, 0.f, 0.f, 0.f};
+    if (act) {
+#pragma unroll 1
+      for (int tb = t0; tb < t1; tb += kSpAgg) {
+        bf16x4 u[kSpAgg], f[kSpAgg];
+#pragma unroll
+        for (int i = 0; i < kSpAgg; ++i) {
+          const int t = min(tb + i, t1 - 1);
+          const __nv_bfloat16* p = ufr + (size_t)t * ld3 + 4 * cq;
+          u[i] = *reinterpret_cast<const bf16x4*>(p);
+          f[i] = *reinterpret_cast<const bf16x4*>(p + d);
+        }
+#pragma unroll
+        for (int i = 0; i < kSpAgg; ++i) {
+          if (tb + i < t1) {
+            const float2 ua = __bfloat1622float2(u[i].a), ub = __bfloat1622float2(u[i].b);
+            const float2 fa = __bfloat1622float2(f[i].a), fb = __bfloat1622float2(f[i].b);
+            const float uu[4] = {ua.x, ua.y, ub.x, ub.y}, ff[4] = {fa.x, fa.y, fb.x, fb.y};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              b[j] = fmaf(ff[j], b[j] - uu[j], uu[j]);
+              a[j] *= ff[j];
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sA[w][4 * lane + j] = a[j];
+      sB[w][4 * lane + j] = b[j];
+    }
+  }
+  __syncthreads();
+  // ---- 2. block map; sA/sB become the exclusive prefix maps of the chunks inside the block
+  const int me = str * nblk + blk;
+  const int c = threadIdx.x;  // channel of the strip (threads < 128)
+  float BA = 1.f, BB = 0.f;
+  if (c < 128) {
+#pragma unroll
+    for (int k = 0; k < kSpWarps; ++k) {
+      const float ak = sA[k][c], bk = sB[k][c];
+      sA[k][c] = BA;
+      sB[k][c] = BB;
+      BB = fmaf(ak, BB, bk);
+      BA *= ak;
+    }
+  }
+  float cin = 0.f;
+  if (blk == 0) {
+    if (c < 128) {
+      const int ch = str * 128 + c;
+      cin = (c0 != nullptr && ch < d) ? c0[ch] : 0.f;
+    }
+  } else {
+    if (c < 128) {
+      agg[(size_t)me * 256 + c] = BA;
+      agg[(size_t)me * 256 + 128 + c] = BB;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sp_st_release(&flags[me], 1);
+    float MA = 1.f, MB = 0.f;  // composition of the maps of the blocks walked so far
+    int base = blk - 1;
+    for (;;) {
+      if (w == 0) {
+        const int idx = base - lane;
+        int f = 0;
+        if (idx >= 0)
+          while ((f = sp_ld_acquire(&flags[str * nblk + idx])) < 1) __nanosleep(32);
+        const unsigned m = __ballot_sync(0xffffffffu, f == 2);
+        if (lane == 0) {
+          s_found = m != 0;
+          s_lo = m ? base - (__ffs(m) - 1) : base - 31;
+        }
+      }
+      __syncthreads();
+      const int lo = s_lo, found = s_found;
+      if (c < 128) {
+        const int stop = found ? lo + 1 : lo;
+        for (int j = base; j >= stop; j -= 8) {  // 8 independent loads in flight
+          float ra[8], rb[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (j - i >= stop) {
+              const size_t o = (size_t)(str * nblk + j - i) * 256 + c;
+              ra[i] = __ldcg(&agg[o]);
+              rb[i] = __ldcg(&agg[o + 128]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (j - i >= stop) {  // M <- M o map(j - i)
+              MB = fmaf(MA, rb[i], MB);
+              MA *= ra[i];
+            }
+          }
+        }
+        if (found) cin = fmaf(MA, __ldcg(&incl[(size_t)(str * nblk + lo) * 128 + c]), MB);
+      }
+      if (found) break;
+      base = lo - 1;
+      __syncthreads();  // s_lo / s_found reused
+    }
+  }
+  // ---- 3. publish the inclusive carry, then replay
+  if (c < 128) {
+    incl[(size_t)me * 128 + c] = fmaf(BA, cin, BB);
+    sCin[c] = cin;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) sp_st_release(&flags[me], 2);
+  if (!act || t0 >= T) return;
+  float cc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) cc[j] = fmaf(sA[w][4 * lane + j], sCin[4 * lane + j], sB[w][4 * lane + j]);
+  float c0r = cc[0], c1r = cc[1], c2r = cc[2], c3r = cc[3];
+  bool bad = false;
+  bf16x4 bu[2][kSpPF], bfv[2][kSpPF], br[2][kSpPF];
+  float4 bx[2][kSpPF];
+  auto fetch = [&](int buf, int tb) {
+#pragma unroll
+    for (int i = 0; i < kSpPF; ++i) {
+      const int t = min(tb + i, t1 - 1);
+      const __nv_bfloat16* p = ufr + (size_t)t * ld3 + 4 * cq;
+      bu[buf][i] = *reinterpret_cast<const bf16x4*>(p);
+      bfv[buf][i] = *reinterpret_cast<const bf16x4*>(p + d);
+      br[buf][i] = *reinterpret_cast<const bf16x4*>(p + 2 * d);
+      bx[buf][i] = *reinterpret_cast<const float4*>(x + (size_t)t * d + 4 * cq);
+    }
+  };
+  fetch(0, t0);
+#pragma unroll 1
+  for (int tb = t0; tb < t1; tb += 2 * kSpPF) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int tc = tb + half * kSpPF;
+      if (tc >= t1) break;
+      if (tc + kSpPF < t1) fetch(half ^ 1, tc + kSpPF);
+#pragma unroll
+      for (int i = 0; i < kSpPF; ++i) {
+        const int t = tc + i;
+        if (t < t1) {
+          const float2 ua = __bfloat1622float2(bu[half][i].a), ub = __bfloat1622float2(bu[half][i].b);
+          const float2 fa = __bfloat1622float2(bfv[half][i].a), fb = __bfloat1622float2(bfv[half][i].b);
+          const float2 ra = __bfloat1622float2(br[half][i].a), rb = __bfloat1622float2(br[half][i].b);
+          const float4 xv = bx[half][i];
+          float4 h;
+          h.x = sru_step(c0r, ua.x, fa.x, ra.x, xv.x);
+          h.y = sru_step(c1r, ua.y, fa.y, ra.y, xv.y);
+          h.z = sru_step(c2r, ub.x, fb.x, rb.x, xv.z);
+          h.w = sru_step(c3r, ub.y, fb.y, rb.y, xv.w);
+          bad |= !(isfinite(h.x) && isfinite(h.y) && isfinite(h.z) && isfinite(h.w) &&
+                   isfinite(c0r + c1r + c2r + c3r));
+          *reinterpret_cast<float4*>(h32 + (size_t)t * d + 4 * cq) = h;
+          bf16x4 hb;
+          hb.a = __floats2bfloat162_rn(h.x, h.y);
+          hb.b = __floats2bfloat162_rn(h.z, h.w);
+          *reinterpret_cast<bf16x4*>(h16 + (size_t)t * d + 4 * cq) = hb;
+        }
+      }
+    }
+  }
+  if (c_last && t1 == T) *reinterpret_cast<float4*>(c_last + 4 * cq) = make_float4(c0r, c1r, c2r, c3r);
+  if (bad) atomicOr(nonfinite, 1);  // reference raises NumericError (src/predictor.py:170-171)
+}
+
+
 // carry into shard `rank` of a token-sharded sequence: fold the shards' whole-range maps
 // tots[g] = (A_g [d], B_g [d]) of shards g < rank onto c = c0 (or 0).
 __global__ void k_sru_fold(const float* __restrict__ tots, int rank, int d, const float* __restrict__ c0,
@@ -297,12 +516,15 @@ using namespace mp;
 
 extern "C" size_t mp_sru_workspace_bytes(int T, int d) {
   const int nch = cdiv(T, kScanChunk);
-  return al(sizeof(__nv_bfloat16) * (size_t)T * 3 * d) + 3 * al(sizeof(float) * (size_t)nch * d);
+  const size_t sp_blocks = (size_t)cdiv(d, 128) * cdiv(T, kSpTokens);  // single-pass scan flags + ticket
+  return al(sizeof(__nv_bfloat16) * (size_t)T * 3 * d) + 3 * al(sizeof(float) * (size_t)nch * d) +
+         al(sizeof(int) * (sp_blocks + 1));
 }
 
 struct SruWs {
   __nv_bfloat16* ufr;
   float *aggA, *aggB, *carry;
+  int* sp_flags;  // single-pass scan: per-block flags (+ ticket counter); block maps in aggA, carries in carry
   SruWs(void* ws, int T, int d) {
     const int nch = cdiv(T, kScanChunk);
     char* p = (char*)ws;
@@ -313,6 +535,8 @@ struct SruWs {
     aggB = (float*)p;
     p += al(sizeof(float) * (size_t)nch * d);
     carry = (float*)p;
+    p += al(sizeof(float) * (size_t)nch * d);
+    sp_flags = (int*)p;
   }
 };
 
@@ -334,6 +558,14 @@ extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, fl
   cudaStream_t st = (cudaStream_t)stream;
   const SruWs w(ws, T, d);
   const int nch = cdiv(T, kScanChunk);
+  static const bool three_pass = getenv("MP_SRU_3PASS") != nullptr;  // A/B switch: the three-kernel form
+  if (!three_pass) {
+    const int nblk = cdiv(T, kSpTokens), nstr = cdiv(d, 128);
+    MP_CUDA_TRY(cudaMemsetAsync(w.sp_flags, 0, sizeof(int) * ((size_t)nstr * nblk + 1), st));
+    MP_CUDA_TRY(launch_pdl(k_scan_fused, dim3(nstr * nblk), dim3(32 * kSpWarps), 0, st, w.ufr, x_f32, T, d, c0, h_f32,
+                           (__nv_bfloat16*)h_bf16, c_last, nonfinite, w.sp_flags, w.aggA, w.carry, nblk));
+    return MP_OK;
+  }
   // K2: chunk aggregates | carries (from c0) | replay + highway
   const dim3 gq(cdiv(d / 4, 64), nch);
   MP_CUDA_TRY(launch_pdl(k_scan_aggregate, dim3(gq), dim3(64), 0, st, w.ufr, T, d, w.aggA, w.aggB));

@@ -133,6 +133,41 @@ def test_sru_layer_matches_fp64(dev):
     assert err < 1e-2, err
 
 
+@pytest.mark.parametrize("T,d", [(20000, 256), (8193, 192), (257, 64)])
+def test_sru_scan_long_sequences(dev, T, d):
+    """mp_sru_scan over many look-back windows (T / 256 blocks per 128-channel strip), with a
+    carry-in and the final cell state, against a float64 scan of the same bf16 u/f/r."""
+    g = torch.Generator().manual_seed(T)
+    u = torch.randn(T, d, generator=g) * 0.5
+    f = torch.sigmoid(torch.randn(T, d, generator=g) * 2 + 2)  # long memory: carries matter
+    r = torch.sigmoid(torch.randn(T, d, generator=g))
+    ufr = torch.cat([u, f, r], 1).bfloat16()
+    x = torch.randn(T, d, generator=g)
+    c0 = torch.randn(d, generator=g)
+    uu, ff, rr = (v.double() for v in ufr.float().split(d, 1))
+    c = c0.double()
+    href = torch.empty(T, d, dtype=torch.float64)
+    for t in range(T):
+        c = ff[t] * c + (1 - ff[t]) * uu[t]
+        href[t] = rr[t] * torch.tanh(c) + (1 - rr[t]) * x[t].double()
+    nbytes = _lib.size_query("mp_sru_workspace_bytes", T, d)
+    ws = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    ws[: ufr.numel() * 2].view(torch.bfloat16).copy_(ufr.reshape(-1).to(dev))
+    xd, c0d = x.to(dev), c0.to(dev)
+    h32 = torch.empty(T, d, device=dev)
+    h16 = torch.empty(T, d, device=dev, dtype=torch.bfloat16)
+    cl = torch.empty(d, device=dev)
+    nf = torch.zeros(1, dtype=torch.int32, device=dev)
+    for _ in range(2):  # the second call reuses the workspace flags (reset per call)
+        _lib.call("mp_sru_scan", ptr(xd), T, d, ptr(c0d), ptr(h32), ptr(h16), ptr(cl), ptr(nf), ptr(ws), nbytes,
+                  stream_ptr())
+        torch.cuda.synchronize()
+        assert int(nf.item()) == 0
+        err = float((h32.double().cpu() - href).abs().max() / href.abs().max())
+        assert err < 1e-4, err
+        assert float((cl.double().cpu() - c).abs().max()) < 1e-4
+
+
 def test_exec_map_and_ffn(dev):
     rng = np.random.default_rng(3)
     T, E, d, F = 1500, 10, 128, 256

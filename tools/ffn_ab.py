@@ -60,12 +60,12 @@ def main():
                           ptr(prows), ptr(eb), ptr(ws), fb, stream_ptr())
         print(f"{which} {case} flags={fl}: {timeit(run, iters=10):.1f} us", flush=True)
         torch.cuda.synchronize()
-        cta_spread(f"  {which} {case}")
+        cta_spread(f"  {which} {case}", units=(prows, eb, 12 if which == "up" else 3))
     torch.cuda.synchronize()
 
 
 
-def cta_spread(label=""):
+def cta_spread(label="", units=None):
     """Per-CTA start/end spread of the last grouped-GEMM launch (load-balance diagnostic)."""
     import ctypes
 
@@ -78,6 +78,32 @@ def cta_spread(label=""):
     ends = np.sort(b - s) / 1e3
     print(f"{label} CTA end times (us from first start): min {ends[0]:.1f}  p10 {ends[14]:.1f}  median "
           f"{ends[74]:.1f}  p90 {ends[133]:.1f}  max {ends[-1]:.1f}; start spread {(a.max() - s) / 1e3:.1f}")
+    if units is not None:  # static round-robin unit assignment (SegSched order) vs end time
+        prows, eb, nt = units
+        ebh = eb.cpu().numpy()
+        pr = prows.cpu().numpy()
+        E = len(ebh) - 1
+        lst = []
+        for e in range(E):
+            cnt = ebh[e + 1] - ebh[e]
+            for t in range(nt):
+                for p in range(ebh[e], ebh[e + 1]):
+                    lst.append(pr[p])
+        lst = np.array(lst)
+        g = 148
+        nunits = np.array([len(lst[c::g]) for c in range(g)])
+        mt = np.array([int(np.sum((lst[c::g] + 127) // 128)) for c in range(g)])
+        rows = np.array([int(np.sum(lst[c::g])) for c in range(g)])
+        e_ = (b - s) / 1e3
+        print(f"    units {len(lst)}; per CTA units {nunits.min()}-{nunits.max()}, m-tiles {mt.min()}-{mt.max()}, "
+              f"rows {rows.min()}-{rows.max()}")
+        for k in sorted(set(mt)):
+            sel = mt == k
+            print(f"    m-tiles {k}: {sel.sum()} CTAs, end {e_[sel].min():.1f}-{e_[sel].max():.1f} us")
+        A = np.stack([nunits, rows, np.ones(g)], 1)
+        coef, *_ = np.linalg.lstsq(A, e_, rcond=None)
+        print(f"    fit end ~ {coef[0]:.2f} us/unit + {coef[1]*128:.2f} us/128 rows + {coef[2]:.1f}; "
+              f"resid std {np.std(e_ - A @ coef):.2f}")
 
 
 if __name__ == "__main__":

@@ -29,6 +29,15 @@ def main():
 
     print(f"sru layer: {timeit(run, iters=20):.1f} us")
 
+    def scan():
+        _lib.call("mp_sru_scan", ptr(x), T, d, None, ptr(h32), ptr(h16), None, ptr(nf), ptr(ws), n, stream_ptr())
+
+    print(f"sru scan: {timeit(scan, iters=20):.1f} us")
+    import os
+    out = os.environ.get("SRU_PROBE_OUT")
+    if out:  # for cross-mode comparisons
+        torch.save(h32.cpu(), out)
+
 
 if __name__ == "__main__":
     main()
