@@ -121,8 +121,11 @@ int make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t col
 
 using namespace mp;
 
-extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc,
-                            const float* bias, int act, int sig_from, void* stream) {
+namespace mp {
+// store_hint (TMA-store epilogue only): 0 none, 1 L2 evict_last (the output is consumed right
+// away, e.g. the SRU u/f/r read by the scan: layer 102 -> 98 us), 2 evict_first
+int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc, const float* bias,
+              int act, int sig_from, int store_hint, void* stream) {
   MP_REQUIRE(M >= 1 && N >= 64 && K >= 64 && K % 64 == 0 && N % 64 == 0, MP_ERR_CONFIG,
              "mp_gemm_bf16: need K%%64==0, N%%64==0 (M=%d N=%d K=%d)", M, N, K);
   MP_REQUIRE(ldc >= N || ldc == 0, MP_ERR_CONFIG, "mp_gemm_bf16: ldc < N");
@@ -151,7 +154,7 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
     CUtensorMap tc;
     rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
     if (rc) return rc;
-    EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from, 0};
+    EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from, store_hint};
     return launch_gemm<256, 4>(ta, tb, s, et, grid, st, &tc);
   }
   if (c_dtype == 0) {
@@ -165,6 +168,12 @@ extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N,
     if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, grid, st);
     return launch_gemm<64, 8>(ta, tb, s, e, grid, st);
   }
+}
+}  // namespace mp
+
+extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc,
+                            const float* bias, int act, int sig_from, void* stream) {
+  return gemm_bf16(A, B, C, M, N, K, c_dtype, ldc, bias, act, sig_from, 0, stream);
 }
 
 namespace mp {

@@ -138,7 +138,7 @@ struct EpiStoreBf16Tma {
   const float* bias;
   int act;
   int sig_from;
-  int keep_l2;  // 1: stores carry an L2 evict_last hint (the output is re-read right away)
+  int keep_l2;  // 1: stores carry an L2 evict_last hint (the output is re-read right away), 2: evict_first
   __device__ __forceinline__ const float* colvec() const { return bias; }
   template <int NC>
   __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float* svec,
@@ -166,8 +166,10 @@ struct EpiStoreBf16Tma {
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          if (keep_l2)
+          if (keep_l2 == 1)
             tma_store_2d_hint(tm, box, U.n0 + c0 + c, U.a_row + row0, policy_evict_last());
+          else if (keep_l2 == 2)  // streaming output: do not evict the GEMM's L2-resident operands
+            tma_store_2d_hint(tm, box, U.n0 + c0 + c, U.a_row + row0, policy_evict_first());
           else
             tma_store_2d(tm, box, U.n0 + c0 + c, U.a_row + row0);
           bulk_commit();
@@ -180,8 +182,8 @@ struct EpiStoreBf16Tma {
         });
       }
     });
-    if (lane == 0) bulk_wait0();  // box reads done and this tile's rows globally written
-    __syncwarp();
+    // no wait here: the next box waits for this warp's previous box to be READ (its smem is
+    // reused); the kernel waits for the writes themselves once, before the CTA exits
   }
 };
 

@@ -58,17 +58,22 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int ASTAGES = 0>
 struct GemmSmem {
+  // ASTAGES == 0: one ring of STAGES x (A | B) stages. ASTAGES > 0: separate rings, STAGES
+  // B stages then ASTAGES A stages, each with its own full/empty barriers (the weight
+  // stream runs further ahead than the L2-resident activations).
   static constexpr int kABytes = kBlockM * kBlockK * 2;
   static constexpr int kBBytes = BN * kBlockK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBarOffset = STAGES * kStageBytes;
-  static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+  static constexpr int kARingOffset = STAGES * kBBytes;
+  static constexpr int kRingBytes = ASTAGES ? STAGES * kBBytes + ASTAGES * kABytes : STAGES * kStageBytes;
+  static constexpr int kBarOffset = kRingBytes;
+  static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 2 * ASTAGES + 4) * 8 + 16;
   static constexpr int kScratchOffset = (kVecOffset + 2 * BN * 4 + 1023) / 1024 * 1024;  // TMA-store boxes
   static constexpr int kScratchWordsPerWarp = 32 * 20;  // 32 rows x (16 + 4 pad) words: store transpose
   static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;  // scheduler table (smem)
-  static constexpr int kPrepInts = 2048;
+  static constexpr int kPrepInts = ASTAGES ? 1025 : 2048;
   static constexpr int kBytes = kPrepOffset + kPrepInts * 4 + 1024;  // + alignment slack
 };
 
@@ -88,17 +93,19 @@ struct GemmSmem {
 //    (lane quadrant, accumulator stage, column c0); the thread handles tile columns
 //    [c0, c0 + NC)).
 
-template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
+template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16, int ASTAGES = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched_in,
                 Epi epi, const __grid_constant__ CUtensorMap tmC) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using L = GemmSmem<BN, STAGES>;
+  using L = GemmSmem<BN, STAGES, ASTAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
+  uint64_t* afull = empty + STAGES;  // split rings only
+  uint64_t* aempty = afull + ASTAGES;
+  uint64_t* tfull = aempty + ASTAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* svec = reinterpret_cast<float*>(smem + L::kVecOffset);  // [2][BN]
@@ -114,6 +121,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < ASTAGES; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -133,9 +144,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nunits = sched.num_units();
   const int nkb = sched.num_kb();
 
-  if (warp == 0) {
+  if (warp == 0 || (ASTAGES > 0 && warp == 3)) {
     if (lane == 0) {
-      // ------------------------------------------------------------ TMA producer
+      // ------------------------------------------------------------ TMA producer(s)
+      // unified ring: warp 0 loads A and B; split rings: warp 0 loads B, warp 3 loads A
+      const bool do_b = warp == 0, do_a = ASTAGES == 0 || warp == 3;
       const uint64_t pol_stream = policy_evict_first();
       uint32_t stage = 0, phase = 0;
       Unit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x) : Unit{};
@@ -145,18 +158,41 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int mtiles = (U.rows + kBlockM - 1) / kBlockM;
         for (int mt = 0; mt < mtiles; ++mt) {
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            uint8_t* sa = smem + stage * L::kStageBytes;
-            uint8_t* sb = sa + L::kABytes;
-            mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
-            tma_load_2d(sa, &tmA, &full[stage], sched.a_kcol(kb), U.a_row + mt * kBlockM);
-            if constexpr (Sched::kStreamB)  // weights are read once per step: do not let them evict reused tiles
-              tma_load_2d_hint(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb), pol_stream);
-            else
-              tma_load_2d(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb));
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
+            if constexpr (ASTAGES == 0) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* sa = smem + stage * L::kStageBytes;
+              uint8_t* sb = sa + L::kABytes;
+              mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
+              tma_load_2d(sa, &tmA, &full[stage], sched.a_kcol(kb), U.a_row + mt * kBlockM);
+              if constexpr (Sched::kStreamB)  // weights are read once per step: do not let them evict reused tiles
+                tma_load_2d_hint(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb), pol_stream);
+              else
+                tma_load_2d(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb));
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            } else if (do_b) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              uint8_t* sb = smem + stage * L::kBBytes;
+              mbar_arrive_expect_tx(&full[stage], L::kBBytes);
+              if constexpr (Sched::kStreamB)
+                tma_load_2d_hint(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb), pol_stream);
+              else
+                tma_load_2d(sb, &tmB, &full[stage], sched.b_kcol(kb), U.b_row + sched.b_krow(kb));
+              if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            } else if (do_a) {
+              mbar_wait(&aempty[stage], phase ^ 1);
+              uint8_t* sa = smem + L::kARingOffset + stage * L::kABytes;
+              mbar_arrive_expect_tx(&afull[stage], L::kABytes);
+              tma_load_2d(sa, &tmA, &afull[stage], sched.a_kcol(kb), U.a_row + mt * kBlockM);
+              if (++stage == (ASTAGES ? ASTAGES : 1)) {
+                stage = 0;
+                phase ^= 1;
+              }
             }
           }
         }
@@ -167,6 +203,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ------------------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = Kind::idesc(kBlockM, BN);
       uint32_t stage = 0, phase = 0, tile = 0;
+      uint32_t astage = 0, aphase = 0;
       Unit Un = blockIdx.x < nunits ? sched.unit(blockIdx.x) : Unit{};
       for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const Unit U = Un;
@@ -179,10 +216,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t d_tmem = tmem_base + as * BN;
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&full[stage], phase);
+            uint64_t adesc, bdesc;
+            if constexpr (ASTAGES == 0) {
+              const uint8_t* sa = smem + stage * L::kStageBytes;
+              adesc = sw128_kmajor_desc(smem_u32(sa));
+              bdesc = sw128_kmajor_desc(smem_u32(sa + L::kABytes));
+            } else {
+              mbar_wait(&afull[astage], aphase);
+              adesc = sw128_kmajor_desc(smem_u32(smem + L::kARingOffset + astage * L::kABytes));
+              bdesc = sw128_kmajor_desc(smem_u32(smem + stage * L::kBBytes));
+            }
             tc_fence_after();
-            const uint8_t* sa = smem + stage * L::kStageBytes;
-            const uint64_t adesc = sw128_kmajor_desc(smem_u32(sa));
-            const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sa + L::kABytes));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               // advance 32 B of K inside the swizzle atom: +2 in the >>4 address field
@@ -192,6 +236,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
+            }
+            if constexpr (ASTAGES > 0) {
+              umma_commit(&aempty[astage]);
+              if (++astage == ASTAGES) {
+                astage = 0;
+                aphase ^= 1;
+              }
             }
           }
           umma_commit(&tfull[as]);
@@ -236,6 +287,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[as]);
       }
+    }
+    if constexpr (TmaStoreOf<Epi>::value) {
+      if (lane == 0) bulk_wait0();  // this warp's TMA stores complete before the CTA exits
     }
   }
   tc_fence_before();

@@ -11,6 +11,9 @@ namespace mp {
 
 int num_sms();
 
+int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc, const float* bias,
+              int act, int sig_from, int store_hint, void* stream);
+
 // 2-D bf16 row-major [rows x cols] tensor map, box = [box_rows x 64 cols], SWIZZLE_128B.
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                    uint32_t box_rows);
@@ -20,11 +23,12 @@ int make_tmap_bf16_store(CUtensorMap* map, const void* ptr, uint64_t rows, uint6
 int make_tmap_f32(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                   uint32_t box_rows);
 
-template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16>
+template <int BN, int STAGES, class Sched, class Epi, class Kind = KindBF16, int ASTAGES = 0>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched, const Epi& epi, int grid,
                 cudaStream_t st, const CUtensorMap* tc = nullptr) {
-  auto kern = k_umma_gemm<BN, STAGES, Sched, Epi, Kind>;
-  const int smem = GemmSmem<BN, STAGES>::kBytes;
+  auto kern = k_umma_gemm<BN, STAGES, Sched, Epi, Kind, ASTAGES>;
+  const int smem = GemmSmem<BN, STAGES, ASTAGES>::kBytes;
+  static_assert(GemmSmem<BN, STAGES, ASTAGES>::kBytes <= 232448, "GEMM shared memory over the sm_100 limit");
   static bool configured = false;  // one attribute call per instantiation
   if (!configured) {
     MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

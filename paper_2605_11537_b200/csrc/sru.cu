@@ -549,7 +549,7 @@ extern "C" int mp_sru_project(const void* x_bf16, const void* w_cat, const float
                               size_t ws_bytes, void* stream) {
   SRU_CHECKS();
   // K1: [u | f | r] = x W_cat^T + b ; sigmoid on the f and r blocks
-  return mp_gemm_bf16(x_bf16, w_cat, SruWs(ws, T, d).ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, stream);
+  return gemm_bf16(x_bf16, w_cat, SruWs(ws, T, d).ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, /*evict_last*/ 1, stream);
 }
 
 extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16,
