@@ -333,6 +333,278 @@ static int launch_router_fused(const float* x, int ldx, int T, int d, const void
   return MP_OK;
 }
 
+
+// k_router_fused with x staged by TMA: a fourth role (warp 3) streams x fp32 k-blocks
+// (two 128 x 32 SWIZZLE_128B boxes) into a 3-deep shared-memory ring, so the
+// converters read x from shared memory instead of holding global loads in registers
+// (the register form is latency-bound: 18 % warps active, x at 2.2 TB/s). The operand
+// ring is 2 deep (measured equal to 3 deep for the register form). EG <= 128.
+constexpr int kRxStages = 2;
+constexpr int kRxXStages = 3;
+template <int EG>
+struct RxSmem {
+  static constexpr int kB = 2 * EG * 128;
+  static constexpr int kA = 128 * 128;
+  static constexpr int kStage = kB + 2 * kA;
+  static constexpr int kXs = 128 * 64 * 4;  // one x k-block: 128 rows x 64 fp32 as two 16 KB boxes
+  static constexpr int kXOffset = kRxStages * kStage;
+  static constexpr int kBarOffset = kXOffset + kRxXStages * kXs;
+  // full[S], conv[S], empty[S], xfull[X], xempty[X], tfull, tempty
+  static constexpr int kXbOffset = kBarOffset + (3 * kRxStages + 2 * kRxXStages + 2) * 8 + 8;
+  static constexpr int kBytes = kXbOffset + 128 * 4 + 1024;
+};
+
+template <int EG>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_router_fused_tx(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int T, int d,
+                      const float* __restrict__ wabs, int E, int32_t* __restrict__ route, float eps,
+                      int32_t* __restrict__ count, int32_t* __restrict__ list) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  using L = RxSmem<EG>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+  uint64_t* conv = full + kRxStages;
+  uint64_t* empty = conv + kRxStages;
+  uint64_t* xfull = empty + kRxStages;
+  uint64_t* xempty = xfull + kRxXStages;
+  uint64_t* tfull = xempty + kRxXStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  float* s_xb = reinterpret_cast<float*>(smem + L::kXbOffset);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = d / 64;
+  const int units = (T + kBlockM - 1) / kBlockM;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmX);
+    for (int s = 0; s < kRxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], kRfConvThreads / 32);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kRxXStages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], kRfConvThreads / 32);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * EG < 32 ? 32 : 2 * EG);
+  griddep_wait();  // x is the previous layer's output
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ------------------------------------------------ B producer
+      uint32_t stage = 0, phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sb = smem + stage * L::kStage;
+          mbar_arrive_expect_tx(&full[stage], L::kB);
+          tma_load_2d(sb, &tmB, &full[stage], kb * 64, 0);
+          tma_load_2d(sb + EG * 128, &tmB, &full[stage], d + kb * 64, 0);
+          if (++stage == kRxStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ------------------------------------------------ x producer
+      uint32_t stage = 0, phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&xempty[stage], phase ^ 1);
+          uint8_t* sx = smem + L::kXOffset + stage * L::kXs;
+          mbar_arrive_expect_tx(&xfull[stage], L::kXs);
+          tma_load_2d(sx, &tmX, &xfull[stage], kb * 64, u * kBlockM);  // rows >= T: zero fill
+          tma_load_2d(sx + L::kXs / 2, &tmX, &xfull[stage], kb * 64 + 32, u * kBlockM);
+          if (++stage == kRxXStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ------------------------------------------------ MMA issuer
+      constexpr uint32_t id_all = idesc_bf16_f32(kBlockM, 2 * EG);
+      constexpr uint32_t id_hi = idesc_bf16_f32(kBlockM, EG);
+      uint32_t stage = 0, phase = 0, tile = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
+        mbar_wait(tempty, (tile & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          mbar_wait(&conv[stage], phase);
+          tc_fence_after();
+          uint8_t* sb = smem + stage * L::kStage;
+          const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sb));
+          const uint64_t dhi = sw128_kmajor_desc(smem_u32(sb + L::kB));
+          const uint64_t dlo = sw128_kmajor_desc(smem_u32(sb + L::kB + L::kA));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            umma_bf16(tmem_base, dhi + 2 * k, bdesc + 2 * k, id_all, (kb | k) != 0);
+            umma_bf16(tmem_base, dlo + 2 * k, bdesc + 2 * k, id_hi, 1);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == kRxStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(tfull);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ convert + epilogue
+    const int ct = threadIdx.x - 128;  // 0..255
+    const int jc = ct & 7;             // 32-byte (8 fp32) column chunk of the k-block
+    const int r0 = ct >> 3;            // rows r0 + 32 i, i = 0..3
+    const int box = jc >> 2, c16 = (jc & 3) * 2;  // x box (32 columns) and 16-byte chunk inside a 128 B row
+    uint32_t stage = 0, phase = 0, xstage = 0, xphase = 0, tile = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
+      const int row_base = u * kBlockM;
+      float part[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&xfull[xstage], xphase);
+        const uint8_t* sx = smem + L::kXOffset + xstage * L::kXs + box * (L::kXs / 2);
+        float4 cur[4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + 32 * i;
+          cur[i][0] = *reinterpret_cast<const float4*>(sx + r * 128 + (((c16) ^ (r & 7)) << 4));
+          cur[i][1] = *reinterpret_cast<const float4*>(sx + r * 128 + (((c16 + 1) ^ (r & 7)) << 4));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[xstage]);
+        if (++xstage == kRxXStages) {
+          xstage = 0;
+          xphase ^= 1;
+        }
+        const float4 w0 = __ldg(reinterpret_cast<const float4*>(wabs + kb * 64 + 8 * jc));
+        const float4 w1 = __ldg(reinterpret_cast<const float4*>(wabs + kb * 64 + 8 * jc + 4));
+        mbar_wait(&empty[stage], phase ^ 1);  // MMA done with this stage's operand tiles
+        uint8_t* shi = smem + stage * L::kStage + L::kB;
+        uint8_t* slo = shi + L::kA;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + 32 * i;
+          const float f[8] = {cur[i][0].x, cur[i][0].y, cur[i][0].z, cur[i][0].w,
+                              cur[i][1].x, cur[i][1].y, cur[i][1].z, cur[i][1].w};
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+            const float2 hf = __bfloat1622float2(h);
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(f[2 * q] - hf.x, f[2 * q + 1] - hf.y);
+            hw[q] = *reinterpret_cast<const uint32_t*>(&h);
+            lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
+          }
+          const int off = r * 128 + ((jc ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(shi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+          *reinterpret_cast<uint4*>(slo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          part[i] += fabsf(f[0]) * w0.x + fabsf(f[1]) * w0.y + fabsf(f[2]) * w0.z + fabsf(f[3]) * w0.w +
+                     fabsf(f[4]) * w1.x + fabsf(f[5]) * w1.y + fabsf(f[6]) * w1.z + fabsf(f[7]) * w1.w;
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[stage]);
+        if (++stage == kRxStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float v = part[i];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        if (jc == 0) s_xb[r0 + 32 * i] = v * 1.0001f + 1e-30f;
+      }
+      named_bar_sync(1, kRfConvThreads);
+      if (warp < 8) {
+        mbar_wait(tfull, tile & 1);
+        tc_fence_after();
+        const int r = (warp & 3) * 32 + lane;
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        float b1 = -INFINITY, b2 = -INFINITY;
+        int bi = 0;
+#pragma unroll 1
+        for (int c = 0; c < EG; c += 32) {
+          float a[32], b[32];
+          tmem_ld32(taddr + c, a);
+          tmem_ld32(taddr + EG + c, b);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int e = c + i;
+            const float v = a[i] + b[i];
+            if (e < E) {
+              if (v > b1) {
+                b2 = b1;
+                b1 = v;
+                bi = e;
+              } else if (v > b2) {
+                b2 = v;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);
+        const int t = row_base + r;
+        if (t < T) {
+          route[t] = bi;
+          if (E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r])) {
+            const int k = atomicAdd(count, 1);
+            list[k] = t;
+          }
+        }
+      }
+      named_bar_sync(1, kRfConvThreads);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * EG < 32 ? 32 : 2 * EG);
+  }
+#endif
+}
+
+template <int EG>
+static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
+                                  int32_t* route, int32_t* count, int32_t* list, float eps, cudaStream_t st) {
+  CUtensorMap tb, tx;
+  int rc = make_tmap_bf16(&tb, w_hl, EG, 2 * d, 2 * d, EG);
+  if (rc) return rc;
+  rc = make_tmap_f32(&tx, x, T, d, ldx, kBlockM);
+  if (rc) return rc;
+  auto kern = k_router_fused_tx<EG>;
+  const int smem = RxSmem<EG>::kBytes;
+  static_assert(RxSmem<128>::kBytes <= 232448, "router smem");
+  static bool configured = false;
+  if (!configured) {
+    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+  const int units = cdiv(T, kBlockM);
+  MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, tx, T,
+                         d, w_abs, E, route, eps, count, list));
+  return MP_OK;
+}
+
 static inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace mp
@@ -400,8 +672,15 @@ extern "C" int mp_route_top1_ex(const float* x, int ldx, int T, int d, const voi
   const RouterWs rw(ws, T, d);
   static const bool unfused = getenv("MP_ROUTER_UNFUSED") != nullptr;  // A/B switch
   if (!unfused && (Eg == 64 || Eg == 128) && ldx % 4 == 0) {
-    int rc = Eg == 128 ? launch_router_fused<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
-                       : launch_router_fused<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
+    static const bool reg_x = getenv("MP_ROUTER_REGX") != nullptr;  // A/B switch: x through registers
+    int rc;
+    if (reg_x || (reinterpret_cast<uintptr_t>(x) & 15) != 0)
+      rc = Eg == 128 ? launch_router_fused<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
+                     : launch_router_fused<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
+    else
+      rc = Eg == 128
+               ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
+               : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
     if (rc) return rc;
     MP_CUDA_TRY(launch_pdl(k_router_recheck, dim3(num_sms()), dim3(256), 0, st, x, ldx, d, w_f32, E, rw.count, rw.list, route));
     MP_CUDA_TRY(cudaGetLastError());
