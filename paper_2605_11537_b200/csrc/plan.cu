@@ -27,6 +27,8 @@ namespace cg = cooperative_groups;
 
 namespace mp {
 
+int num_sms();
+
 // counts per (layer, chunk, expert); grid (nch, L), block kChunk
 __global__ void k_chunk_hist(const int32_t* __restrict__ assign, int T, int E, int nch, int32_t* __restrict__ cc) {
   griddep_launch_dependents();
@@ -274,8 +276,11 @@ __device__ inline void emit_pieces(int32_t* pr, int32_t* pn, int p0, int np, int
 
 // Execution map per layer (src/simulator.py:185-203) + slot rows + GEMM pieces.
 // grid L, block 1024. smem: s_off[E+1] s_n[E] s_row[MS+1] s_pc[MS+1]
-__device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* __restrict__ demand, int E, int max_slots,
-                                int split_m, int32_t* __restrict__ res, int32_t* __restrict__ corrective,
+// Slot / row / piece layout of one layer into shared memory (sm: s_off[E+1] s_n[E]
+// s_row[max_slots+1] s_pc[max_slots+1]); global outputs only when `write`. demand and
+// res_in may live in global or shared memory.
+__device__ void exec_layer_core(int l, int* sm, int* red, const int32_t* demand, const int32_t* res_in, bool write,
+                                int E, int max_slots, int split_m, int32_t* res, int32_t* __restrict__ corrective,
                                 int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
                                 int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
                                 int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin, int pieces_stride,
@@ -286,10 +291,12 @@ __device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* __restr
   int* s_pc = s_row + max_slots + 1;
   const size_t b = (size_t)l * E;
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    const int n = demand[b + e], rp = res[b + e];
+    const int n = demand[b + e], rp = res_in[b + e];
     const int cnt = rp > 0 ? rp : (n > 0 ? 1 : 0);
-    corrective[b + e] = (rp == 0 && n > 0) ? 1 : 0;
-    res[b + e] = cnt;
+    if (write) {
+      corrective[b + e] = (rp == 0 && n > 0) ? 1 : 0;
+      res[b + e] = cnt;
+    }
     s_off[e] = cnt;
     s_n[e] = n;
   }
@@ -297,11 +304,11 @@ __device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* __restr
   const int ns = block_exclusive_scan(s_off, E, red);
   if (threadIdx.x == 0) {
     s_off[E] = ns;
-    num_slots[l] = ns;
+    if (write) num_slots[l] = ns;
   }
   __syncthreads();
   if (ns > max_slots) {
-    if (threadIdx.x == 0) atomicExch(err, 1);
+    if (write && threadIdx.x == 0) atomicExch(err, 1);
     return;
   }
   for (int s = threadIdx.x; s < ns; s += blockDim.x) {
@@ -324,6 +331,7 @@ __device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* __restr
     s_pc[ns] = P;
   }
   __syncthreads();
+  if (!write) return;
   int32_t* pr = piece_row + (size_t)l * pieces_stride;
   int32_t* pn = piece_rows + (size_t)l * pieces_stride;
   for (int s = threadIdx.x; s < ns; s += blockDim.x) slot_row_g[(size_t)l * (max_slots + 1) + s] = s_row[s];
@@ -343,6 +351,15 @@ __device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* __restr
   }
 }
 
+__device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* demand, int E, int max_slots, int split_m,
+                                int32_t* res, int32_t* __restrict__ corrective, int32_t* __restrict__ num_slots,
+                                int32_t* __restrict__ off_g, int32_t* __restrict__ slot_row_g,
+                                int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
+                                int32_t* __restrict__ exp_begin, int pieces_stride, int32_t* __restrict__ err) {
+  exec_layer_core(l, sm, red, demand, res, true, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
+                  piece_row, piece_rows, exp_begin, pieces_stride, err);
+}
+
 __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_slots, int split_m,
                              int32_t* __restrict__ res, int32_t* __restrict__ corrective,
                              int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
@@ -355,6 +372,104 @@ __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_
   __shared__ int red[40];
   exec_layer_body(blockIdx.x, sm, red, demand, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
                   piece_row, piece_rows, exp_begin, pieces_stride, err);
+}
+
+
+// The execution map of one layer as ONE launch (default for L == 1, E <= 256,
+// T <= 32 x 1024): grid = T / 1024 blocks of 1024 tokens.
+//   A. every block: in-block stable ranks (warp match_any + per-warp expert counts
+//      scanned over the 32 warps), its expert histogram -> bh[b][e], and a copy of the
+//      old residency; then one arrival on a grid counter.
+//   B. every block, once all have arrived: all block histograms -> its own prefix and
+//      the demand; the slot / row / piece layout of exec_layer_core in shared memory
+//      (block 0 alone writes the global outputs: residency, pieces, offsets).
+//   C. every block: rank = prefix[e] + in-block rank -> slot, row, tok_of_row from the
+//      shared-memory layout.
+// Blocks only wait for every block to finish phase A; all are co-resident
+// (T / 1024 <= 32 <= the SM count). Same stable ranks (token order within an expert) and
+// the same layout arithmetic as k_chunk_hist .. k_exec_rank.
+constexpr int kXoTokens = 1024;
+constexpr int kXoMaxBlocks = 32;
+__global__ void __launch_bounds__(kXoTokens) k_exec_one(const int32_t* __restrict__ route, int T, int E,
+                                                         int max_slots, int split_m, int32_t* res,
+                                                         int32_t* __restrict__ corrective, int32_t* __restrict__ num_slots,
+                                                         int32_t* __restrict__ off_g, int32_t* __restrict__ slot_row_g,
+                                                         int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
+                                                         int32_t* __restrict__ exp_begin, int pieces_stride,
+                                                         int32_t* err, int32_t* bh, int32_t* __restrict__ token_to_slot,
+                                                         int32_t* __restrict__ row_of_token,
+                                                         int32_t* __restrict__ tok_of_row) {
+  griddep_launch_dependents();
+  griddep_wait();
+  extern __shared__ int xo_sm[];
+  const int nb = gridDim.x, b = blockIdx.x;
+  int* s_wh = xo_sm;                   // [32 warps][E], then [nb][E] block histograms
+  int* s_res = s_wh + 32 * E;          // E: residency before this layer
+  int* s_dem = s_res + E;              // E: demand
+  int* s_pre = s_dem + E;              // E: this block's prefix
+  int* s_lay = s_pre + E;              // exec_layer_core scratch: s_off[E+1] s_n[E] s_row[ms+1] s_pc[ms+1]
+  __shared__ int red[40];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_wh[i] = 0;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_res[i] = res[i];
+  __syncthreads();
+  // ---- A
+  const int t = b * kXoTokens + threadIdx.x;
+  const int e = t < T ? __ldg(&route[t]) : -1;
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int wr = __popc(peers & ((1u << lane) - 1u));
+  if (e >= 0 && lane == __ffs(peers) - 1) s_wh[w * E + e] = __popc(peers);
+  __syncthreads();
+  for (int x = threadIdx.x; x < E; x += blockDim.x) {
+    int run = 0;
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const int c = s_wh[k * E + x];
+      s_wh[k * E + x] = run;
+      run += c;
+    }
+    bh[(size_t)b * E + x] = run;
+  }
+  __syncthreads();
+  const int inblock = e >= 0 ? s_wh[w * E + e] + wr : 0;
+  __threadfence();
+  __syncthreads();  // s_wh is reused below; every block's residency read precedes block 0's update
+  if (threadIdx.x == 0) {
+    atomicAdd(&err[1], 1);
+    int n;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(n) : "l"(&err[1]) : "memory");
+      if (n < nb) __nanosleep(32);
+    } while (n < nb);
+  }
+  __syncthreads();
+  // ---- B
+  for (int i = threadIdx.x; i < nb * E; i += blockDim.x) s_wh[i] = __ldcg(&bh[i]);
+  __syncthreads();
+  for (int x = threadIdx.x; x < E; x += blockDim.x) {
+    int run = 0, pre = 0;
+    for (int k = 0; k < nb; ++k) {
+      if (k == b) pre = run;
+      run += s_wh[k * E + x];
+    }
+    s_dem[x] = run;
+    s_pre[x] = pre;
+  }
+  __syncthreads();
+  exec_layer_core(0, s_lay, red, s_dem, s_res, b == 0, E, max_slots, split_m, res, corrective, num_slots, off_g,
+                  slot_row_g, piece_row, piece_rows, exp_begin, pieces_stride, err);
+  __syncthreads();
+  // ---- C
+  const int* s_off = s_lay;
+  const int* s_row = s_lay + 2 * E + 1;
+  if (t >= T || s_off[E] > max_slots) return;
+  const int rank = s_pre[e] + inblock;
+  const int o = s_off[e], c = s_off[e + 1] - o;
+  const int s = o + rank % c;
+  const int row = s_row[s] + rank / c;
+  token_to_slot[t] = s;
+  if (row_of_token) row_of_token[t] = row;
+  tok_of_row[row] = t;
 }
 
 __device__ void exec_rank_body(int l, int ch, int* se, const int32_t* __restrict__ route, int T, int E, int nch,
@@ -660,6 +775,17 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
     if (ce == cudaSuccess) return MP_OK;
     if (ce != cudaErrorCooperativeLaunchTooLarge) MP_CUDA_TRY(ce);
     (void)cudaGetLastError();
+  }
+  static const bool four = getenv("MP_EXEC_FOUR") != nullptr;  // A/B switch: the four-kernel form
+  const int nb = cdiv(T, kXoTokens);
+  const size_t sm_o = sizeof(int) * ((size_t)32 * E + 3 * (size_t)E) + sm_x;
+  if (!four && L == 1 && E <= 256 && nb <= kXoMaxBlocks && nb <= num_sms() && sm_o <= 200 * 1024) {
+    MP_CUDA_TRY(set_smem((const void*)k_exec_one, sm_o));
+    MP_CUDA_TRY(cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st));  // grid arrival counter
+    MP_CUDA_TRY(launch_pdl(k_exec_one, dim3(nb), dim3(kXoTokens), sm_o, st, route, T, E, max_slots, split_m, res,
+                           corrective, num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin, pieces_stride, err,
+                           cc, token_to_slot, row_of_token, tok_of_row));
+    return MP_OK;
   }
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
