@@ -76,8 +76,53 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop_evt = threading.Event()
+        self.t0 = self.t1 = None
+
+    def mark(self, begin: bool):
+        """Bracket the timed region (NVML samples outside it are dropped)."""
+        if begin:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
+    def _nvml_handle(self):
+        """NVML handle of the CUDA device (matched by PCI bus id, so CUDA_VISIBLE_DEVICES cannot mislead it)."""
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        pr = torch.cuda.get_device_properties(self.index)
+        try:
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _nvml_loop(self):
+        nv, h = self.nvml
+        reasons = nv.nvmlDeviceGetCurrentClocksEventReasons if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+            else nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        bits = [0x8, 0x40, 0x20, 0x4]  # hw_slowdown, hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop_evt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = reasons(h)
+                row = [str(sm), str(mx), "0"] + ["Active" if r & b else "Not Active" for b in bits]
+                if self.t0 is not None and self.t1 is None:  # inside the timed region only
+                    self.rows.append(row)
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
+        try:  # NVML: a sample every ~5 ms (nvidia-smi -lms cannot sample a sub-second timed region)
+            self.nvml = self._nvml_handle()
+            threading.Thread(target=self._nvml_loop, daemon=True).start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -92,6 +137,7 @@ class ClockSampler:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self):
+        self.stop_evt.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -105,7 +151,8 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i] == "Active"})
         loaded = [s for s in sm if s > 0.5 * max(mx or [1])] or sm
         med = sorted(loaded)[len(loaded) // 2] if loaded else None
-        return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+        return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 def dist_setup():
@@ -267,6 +314,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier(world)
     launches = 0
+    clocks.mark(True)
     if overlap is not None:
         overlap.run([b[0] for b in batches], args.steps, timer=(start, end))
         launches = args.steps * (overlap.launches + 1)
@@ -281,6 +329,7 @@ def run_ours(args):
                 launches += step(k, ev) + 1  # + the input staging copy
         end.record()
     torch.cuda.synchronize()
+    clocks.mark(False)
     elapsed_ms = start.elapsed_time(end)
     clk = clocks.stop()
     elapsed_ms = max_over_ranks(elapsed_ms, world)
@@ -319,6 +368,26 @@ def run_ours(args):
         except Exception:
             traffic = None
 
+    # "MoE layers only" next to end-to-end -- the predictor + plan part of the
+    # step captured alone and timed the same way; the MoE layers are the rest of the step
+    moe_only = None
+    if graph is not None:
+        g_pred = pipe.capture_call(lambda sp: pipe.predict(x, sp) + pipe.plan_and_place(sp))
+        for _ in range(3):
+            g_pred.replay()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            g_pred.replay()
+        s1.record()
+        torch.cuda.synchronize()
+        ms_pred = s0.elapsed_time(s1) / args.steps
+        ms_moe = elapsed_ms / args.steps - ms_pred
+        moe_only = {"value": T / (ms_moe * 1e-3), "unit": "tokens/s", "ms_per_step": ms_moe,
+                    "ms_predictor_and_plan": ms_pred,
+                    "how": "step time minus a separately captured and timed predictor + plan/place graph"}
+
     value = world * T * args.steps / (elapsed_ms * 1e-3)
     result = {
         "metric": METRIC,
@@ -356,6 +425,7 @@ def run_ours(args):
             "tensor_frac": flops / ((t_up + t_down) * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"],
         },
         "checks": {"routing_exact_last_step": routing_exact, "predictor_accuracy_last_step": pred_acc},
+        "moe_layers_only": moe_only,
         "cuda_graph": graph is not None or overlap is not None,
         "overlap": overlap is not None,
     }
