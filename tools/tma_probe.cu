@@ -1,0 +1,112 @@
+// Per-SM TMA ingest probe: every CTA (one per SM) streams 2-D tiles of an L2-resident
+// bf16 buffer into a STAGES-deep shared-memory ring (mbarrier tx completion), the
+// consumer releases each stage immediately. Reports bytes/s per SM and chip-wide for
+// box sizes and ring depths, to separate the GEMM core's per-SM operand ingest limit
+// from MMA / epilogue effects.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2605_11537_b200/csrc \
+//        tools/tma_probe.cu -o /tmp/tma_probe -lcuda && /tmp/tma_probe
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <vector>
+
+#include "ptx.cuh"
+
+using namespace mp;
+
+template <int STAGES>
+__global__ void __launch_bounds__(64, 1) k_probe(const __grid_constant__ CUtensorMap tm, int box_rows, int iters,
+                                                 int rows_total, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int stage_bytes = box_rows * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * stage_bytes);
+  uint64_t* empty = full + STAGES;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {  // producer
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      mbar_arrive_expect_tx(&full[stage], stage_bytes);
+      const int row = ((blockIdx.x * 7 + i) * box_rows) % rows_total;
+      tma_load_2d(smem + stage * stage_bytes, &tm, &full[stage], 0, row);
+      if (++stage == STAGES) stage = 0, phase ^= 1;
+    }
+  } else if (threadIdx.x == 32) {  // consumer
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&full[stage], phase);
+      mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) stage = 0, phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = clock64() - t0;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+int main() {
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int rows_total = 1 << 16;  // 64K rows x 128 B = 8 MB: L2-resident
+  void* buf;
+  cudaMalloc(&buf, (size_t)rows_total * 128);
+  cudaMemset(buf, 1, (size_t)rows_total * 128);
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sizeof(unsigned long long) * nsm);
+  auto enc = get_encode();
+  for (int box_rows : {64, 128, 256}) {
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int stages : {2, 4, 6}) {
+      const int sbytes = box_rows * 128;
+      const int smem = stages * sbytes + 2 * stages * 8 + 2048;
+      if (smem > 227 * 1024) continue;
+      const int iters = (64 << 20) / sbytes;  // 64 MB per CTA
+      void* kern = stages == 2 ? (void*)k_probe<2> : stages == 4 ? (void*)k_probe<4> : (void*)k_probe<6>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        if (stages == 2) k_probe<2><<<nsm, 64, smem>>>(tm, box_rows, iters, rows_total, cyc);
+        if (stages == 4) k_probe<4><<<nsm, 64, smem>>>(tm, box_rows, iters, rows_total, cyc);
+        if (stages == 6) k_probe<6><<<nsm, 64, smem>>>(tm, box_rows, iters, rows_total, cyc);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double bytes = (double)nsm * iters * sbytes;
+      std::vector<unsigned long long> h(nsm);
+      cudaMemcpy(h.data(), cyc, sizeof(unsigned long long) * nsm, cudaMemcpyDeviceToHost);
+      unsigned long long mx = 0;
+      for (auto v : h) mx = v > mx ? v : mx;
+      printf("box %3d rows (%5d B)  stages %d: %7.1f GB/s per SM, %6.2f TB/s chip, %.1f B/clk per SM (%s)\n", box_rows,
+             sbytes, stages, bytes / nsm / (ms * 1e-3) / 1e9, bytes / (ms * 1e-3) / 1e12,
+             (double)iters * sbytes / (double)mx, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
