@@ -204,7 +204,7 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
     const int cl = mc_cluster(Fp / 256);
     if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, Fp / 256, Fp, dp / 64, tiled, e, st);
   }
-  SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
+  SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled, 0};
   if (tma_store && !diag_nostore) {
     CUtensorMap tc;
     rc = make_tmap_bf16_store(&tc, hid, T, Fp, Fp);
@@ -246,7 +246,8 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
     const int cl = mc_cluster(dp / 256);
     if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, dp / 256, dp, Fp / 64, tiled, e, st);
   }
-  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
+  static const int rev = getenv("MP_GEMM2_FORWARD") ? 0 : 1;  // A/B switch: GEMM2 in GEMM1's unit order
+  SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled, rev};
   if ((flags & 16) && hdone) {  // drop each piece's H from L2 after its last slice unit
     EpiScatterAdd ed{y, dp, tok_of_row, hdone, hid, Fp, dp / bn};
     if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, ed, num_sms(), st);

@@ -354,6 +354,8 @@ struct SegSched {
   const int32_t* exp_begin;  // E + 1 entries (staged into shared memory by prepare when E < kPrepInts)
   int E, n_tiles, bn, n_per_expert, kb;
   int b_tiled;  // B pre-tiled as [E][n_tiles][kb][bn rows][64 cols]: every TMA box is one contiguous burst
+  int reverse;  // 1: walk the unit list backwards (GEMM2 consumes the hidden rows GEMM1 wrote LAST first,
+                //    while they are still in L2)
   __device__ void prepare(int* tab) {
     if (E + 1 > 1025) return;
     for (int e = threadIdx.x; e <= E; e += blockDim.x) tab[e] = exp_begin[e];
@@ -362,6 +364,7 @@ struct SegSched {
   }
   __device__ int num_units() const { return exp_begin[E] * n_tiles; }
   __device__ Unit unit(int u) const {
+    if (reverse) u = exp_begin[E] * n_tiles - 1 - u;
     int lo = 0, hi = E;  // exp_begin[lo]*n_tiles <= u < exp_begin[hi]*n_tiles
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
