@@ -53,6 +53,8 @@ def parse_args():
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
     p.add_argument("--ffn", choices=["two", "mt", "fused"], default="two")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
+    p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
+    p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")
     p.add_argument("--overlap", choices=["on", "off"], default="off",
                    help="predictor of batch i+1 on its own stream during batch i (two-actor pipeline)")
     return p.parse_args()
@@ -292,7 +294,7 @@ def run_ours(args):
     if args.overlap == "on" and not ep and not args.no_graph:
         from paper_2605_11537_b200.engine import OverlappedPipeline
 
-        overlap = OverlappedPipeline(pipe, ev)
+        overlap = OverlappedPipeline(pipe, ev, args.ffn_sms, args.pred_sms)
         overlap.run([b[0] for b in batches], 2)
         torch.cuda.synchronize()
     elif not args.no_graph and not ep:

@@ -116,6 +116,13 @@ MP_API int mp_segments_from_slots(const int32_t* token_to_slot, const int32_t* s
                                   int split_m, int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows,
                                   int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 
+/* SM partition for the two-stream schedule of the paper's pipeline (reference
+ * src/pipeline.py:70-139: the hash-table builder for batch i+1 runs while batch i is
+ * forwarded): persistent grids of the grouped expert GEMMs and of the predictor GEMMs
+ * (SRU projection, heads). 0 = all SMs (default). Host-side setting, applies to launches
+ * issued (or captured) after the call. */
+MP_API int mp_set_sm_partition(int ffn_sms, int predictor_sms);
+
 /* ------------------------------------------------------------------ K1 / generic
  * C[M x ldc] = epi(A[M x K] * B[N x K]^T) on tcgen05 (bf16 in, fp32 acc).
  * K % 64 == 0, N % 64 == 0 (pad with zero rows), 16-byte aligned rows.

@@ -46,6 +46,12 @@ int num_sms() {
   return n;
 }
 
+// SM partition for the two-stream (predictor || MoE layers) schedule: persistent grids of
+// the grouped expert GEMMs and of the predictor GEMMs; 0 = every SM.
+static int g_ffn_sms = 0, g_pred_sms = 0;
+int ffn_grid() { return g_ffn_sms > 0 ? std::min(g_ffn_sms, num_sms()) : num_sms(); }
+int pred_grid() { return g_pred_sms > 0 ? std::min(g_pred_sms, num_sms()) : num_sms(); }
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -125,7 +131,7 @@ namespace mp {
 // store_hint (TMA-store epilogue only): 0 none, 1 L2 evict_last (the output is consumed right
 // away, e.g. the SRU u/f/r read by the scan: layer 102 -> 98 us), 2 evict_first
 int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc, const float* bias,
-              int act, int sig_from, int store_hint, void* stream) {
+              int act, int sig_from, int store_hint, void* stream, int grid_cap) {
   MP_REQUIRE(M >= 1 && N >= 64 && K >= 64 && K % 64 == 0 && N % 64 == 0, MP_ERR_CONFIG,
              "mp_gemm_bf16: need K%%64==0, N%%64==0 (M=%d N=%d K=%d)", M, N, K);
   MP_REQUIRE(ldc >= N || ldc == 0, MP_ERR_CONFIG, "mp_gemm_bf16: ldc < N");
@@ -138,7 +144,8 @@ int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_
   if (rc) return rc;
   DenseSched s{M, N / bn, K / 64, bn};
   const int units = cdiv(M, kBlockM) * (N / bn);
-  const int grid = units < num_sms() ? units : num_sms();
+  const int cap = grid_cap > 0 ? std::min(grid_cap, num_sms()) : num_sms();
+  const int grid = units < cap ? units : cap;
   static const bool pair = getenv("MP_GEMM_PAIR") != nullptr;  // experiment switch: CTA-pair kernel
   if (pair && bn == 256 && c_dtype == 0 && M >= 256) {
     CUtensorMap tb2;
@@ -173,7 +180,14 @@ int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_
 
 extern "C" int mp_gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc,
                             const float* bias, int act, int sig_from, void* stream) {
-  return gemm_bf16(A, B, C, M, N, K, c_dtype, ldc, bias, act, sig_from, 0, stream);
+  return gemm_bf16(A, B, C, M, N, K, c_dtype, ldc, bias, act, sig_from, 0, stream, 0);
+}
+
+extern "C" int mp_set_sm_partition(int ffn_sms, int predictor_sms) {
+  MP_REQUIRE(ffn_sms >= 0 && predictor_sms >= 0, MP_ERR_CONFIG, "mp_set_sm_partition: negative SM count");
+  g_ffn_sms = ffn_sms;
+  g_pred_sms = predictor_sms;
+  return MP_OK;
 }
 
 namespace mp {

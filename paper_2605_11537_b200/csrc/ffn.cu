@@ -212,9 +212,9 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
     // H is re-read by GEMM2 right after: keep it in L2 (GEMM1 151 -> 142 us, GEMM2 +3.5 us)
     static const int keep = getenv("MP_H_NO_EVICT_LAST") == nullptr;  // A/B switch
     EpiStoreBf16Tma et{hid, Fp, nullptr, 1, 0, keep};
-    return launch_gemm<256, 4>(ta, tb, s, et, num_sms(), st, &tc);
+    return launch_gemm<256, 4>(ta, tb, s, et, ffn_grid(), st, &tc);
   }
-  return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
+  return launch_gemm<256, 4>(ta, tb, s, e, ffn_grid(), st);
 }
 
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
@@ -250,13 +250,13 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
   SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled, rev};
   if ((flags & 16) && hdone) {  // drop each piece's H from L2 after its last slice unit
     EpiScatterAdd ed{y, dp, tok_of_row, hdone, hid, Fp, dp / bn};
-    if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, ed, num_sms(), st);
-    if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, ed, num_sms(), st);
-    return launch_gemm<64, 8>(ta, tb, s, ed, num_sms(), st);
+    if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, ed, ffn_grid(), st);
+    if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, ed, ffn_grid(), st);
+    return launch_gemm<64, 8>(ta, tb, s, ed, ffn_grid(), st);
   }
-  if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, num_sms(), st);
-  if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, num_sms(), st);
-  return launch_gemm<64, 8>(ta, tb, s, e, num_sms(), st);
+  if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, ffn_grid(), st);
+  if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, ffn_grid(), st);
+  return launch_gemm<64, 8>(ta, tb, s, e, ffn_grid(), st);
 }
 
 #define FFN_CHECKS()                                                                                            \

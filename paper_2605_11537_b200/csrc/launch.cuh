@@ -12,7 +12,9 @@ namespace mp {
 int num_sms();
 
 int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc, const float* bias,
-              int act, int sig_from, int store_hint, void* stream);
+              int act, int sig_from, int store_hint, void* stream, int grid_cap = 0);
+int ffn_grid();   // persistent grid of the grouped expert GEMMs (mp_set_sm_partition)
+int pred_grid();  // persistent grid of the predictor GEMMs
 
 // 2-D bf16 row-major [rows x cols] tensor map, box = [box_rows x 64 cols], SWIZZLE_128B.
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,

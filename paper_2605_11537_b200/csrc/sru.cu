@@ -549,7 +549,7 @@ extern "C" int mp_sru_project(const void* x_bf16, const void* w_cat, const float
                               size_t ws_bytes, void* stream) {
   SRU_CHECKS();
   // K1: [u | f | r] = x W_cat^T + b ; sigmoid on the f and r blocks
-  return gemm_bf16(x_bf16, w_cat, SruWs(ws, T, d).ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, /*evict_last*/ 1, stream);
+  return gemm_bf16(x_bf16, w_cat, SruWs(ws, T, d).ufr, T, 3 * d, d, 0, 3 * d, b_cat, 2, d, /*evict_last*/ 1, stream, pred_grid());
 }
 
 extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, float* h_f32, void* h_bf16,
@@ -635,7 +635,7 @@ extern "C" int mp_heads_argmax(const void* h_bf16, const void* heads, int T, int
   DenseSched s{T, N / bn, d / 64, bn};
   EpiGroupArgmax e{assign, T, Eg, E, L};
   const int units = cdiv(T, kBlockM) * (N / bn);
-  const int grid = units < num_sms() ? units : num_sms();
+  const int grid = units < pred_grid() ? units : pred_grid();
   if (bn == 256 && Eg <= 128) {  // one group per column half: both epilogue warpgroups work
     EpiGroupArgmaxT<true> es{assign, T, Eg, E, L};
     return launch_gemm<256, 4>(ta, tb, s, es, grid, st);

@@ -492,13 +492,17 @@ class OverlappedPipeline:
     CUDA graph. Planning/placement stay in batch order on the consumer stream, so results
     are identical to the sequential schedule (the reference's mode_equivalence_check)."""
 
-    def __init__(self, pipe: "MoEPipeline", events=None):
+    def __init__(self, pipe: "MoEPipeline", events=None, ffn_sms: int = 0, predictor_sms: int = 0):
+        """ffn_sms / predictor_sms: persistent grids of the expert GEMMs and of the predictor
+        GEMMs (mp_set_sm_partition) so both halves find free SMs; 0 = all SMs. The consumer
+        (MoE layers) stream has the higher priority."""
         self.pipe = pipe
         T, d = pipe.cfg.tokens, pipe.dp
         dev = pipe.dev
         self.xbuf = [torch.empty(T, d, device=dev) for _ in range(2)]
         self.assign = [pipe.assign, torch.empty_like(pipe.assign)]
-        self.sp, self.sf = torch.cuda.Stream(), torch.cuda.Stream()
+        self.sp, self.sf = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+        _lib.call("mp_set_sm_partition", int(ffn_sms), int(predictor_sms))
         self.pred_ev = [torch.cuda.Event() for _ in range(2)]
         self.cons_ev = [torch.cuda.Event() for _ in range(2)]
         self.g_pred, self.g_cons = [], []
@@ -511,6 +515,7 @@ class OverlappedPipeline:
                 self.g_cons.append(pipe.capture_call(lambda sp, j=j: pipe.consume(self.xbuf[j], sp, events)))
         pipe.assign = self.assign[0]
         torch.cuda.synchronize()
+        _lib.call("mp_set_sm_partition", 0, 0)  # the captured graphs keep their grids
         self.launches = self.g_pred[0].launches + self.g_cons[0].launches
 
     def run(self, batches, n: int, timer=None) -> None:
