@@ -53,6 +53,47 @@ __global__ void __launch_bounds__(64, 1) k_probe(const __grid_constant__ CUtenso
   if (threadIdx.x == 0) cycles[blockIdx.x] = clock64() - t0;
 }
 
+template <int STAGES>
+__global__ void __launch_bounds__(64, 1) k_probe3(const __grid_constant__ CUtensorMap tm, int box_bytes, int iters,
+                                                  int blocks_total, unsigned long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * box_bytes);
+  uint64_t* empty = full + STAGES;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      mbar_arrive_expect_tx(&full[stage], box_bytes);
+      const int z = ((blockIdx.x * 7 + i) * 2) % blocks_total;
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+              smem_u32(smem + stage * box_bytes)),
+          "l"(reinterpret_cast<uint64_t>(&tm)), "r"(smem_u32(&full[stage])), "r"(0), "r"(0), "r"(z)
+          : "memory");
+      if (++stage == STAGES) stage = 0, phase ^= 1;
+    }
+  } else if (threadIdx.x == 32) {
+    uint32_t stage = 0, phase = 0;
+    for (int i = 0; i < iters; ++i) {
+      mbar_wait(&full[stage], phase);
+      mbar_arrive(&empty[stage]);
+      if (++stage == STAGES) stage = 0, phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = clock64() - t0;
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -106,6 +147,39 @@ int main() {
       printf("box %3d rows (%5d B)  stages %d: %7.1f GB/s per SM, %6.2f TB/s chip, %.1f B/clk per SM (%s)\n", box_rows,
              sbytes, stages, bytes / nsm / (ms * 1e-3) / 1e9, bytes / (ms * 1e-3) / 1e12,
              (double)iters * sbytes / (double)mx, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  // 3-D boxes {64 cols, 256 rows, 2 tiles} = 64 KB per operation (two 32 KB SW128 tiles)
+  {
+    const int tiles = rows_total / 256;
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {64, 256, (cuuint64_t)tiles};
+    cuuint64_t strides[2] = {128, 256 * 128};
+    cuuint32_t box[3] = {64, 256, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int bb = 65536;
+    for (int stages : {2, 3}) {
+      const int smem = stages * bb + 2 * stages * 8 + 2048;
+      const int iters = (64 << 20) / bb;
+      void* kern = stages == 2 ? (void*)k_probe3<2> : (void*)k_probe3<3>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a);
+        if (stages == 2) k_probe3<2><<<nsm, 64, smem>>>(tm, bb, iters, tiles, cyc);
+        if (stages == 3) k_probe3<3><<<nsm, 64, smem>>>(tm, bb, iters, tiles, cyc);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+      }
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      const double bytes = (double)nsm * iters * bb;
+      printf("3-D box 64 KB (2 x 256 rows)  stages %d: %7.1f GB/s per SM, %6.2f TB/s chip (%s)\n", stages,
+             bytes / nsm / (ms * 1e-3) / 1e9, bytes / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
