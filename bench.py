@@ -51,7 +51,7 @@ def parse_args():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
-    p.add_argument("--ffn", choices=["two", "mt", "fused"], default="two")
+    p.add_argument("--ffn", choices=["two", "mt", "fused", "pair"], default="two")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
     p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")

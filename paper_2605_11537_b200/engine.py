@@ -50,7 +50,7 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
-    ffn: str = "two"              # two (single-tile units) | mt (multi-tile units, slower: see DESIGN) |
+    ffn: str = "two"              # two (single-tile units) | mt (multi-tile units, slower: see DESIGN) | pair (CTA pairs) |
                                   # fused (experimental: one launch, H in an L2 ring)
     sru_pipeline: bool = False    # two-stream token-half SRU pipeline (measured slower: 1219 vs 1133 us)
     skew: float = 1.2
@@ -302,7 +302,11 @@ class MoEPipeline:
         # paper's baseline); the multi-tile kernel pairs 128-row tiles, so it runs on split
         # pieces (a replica is still one slot; its tiles are independent GEMM units)
         use_mt = cfg.ffn == "mt" and cfg.replication != "off" and d % 256 == 0 and E <= 1024
+        # CTA-pair (cta_group::2) grouped GEMMs: pieces of <= 128 rows, an even number per expert
+        use_pair = cfg.ffn == "pair" and d % 256 == 0
         split = 1 if (cfg.replication == "split" or cfg.ffn == "fused" or use_mt) else 0
+        if use_pair:
+            split = 3
         _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
                   ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
         n = 3  # fused split + GEMM (or pre-pass + GEMM), recheck
@@ -323,7 +327,7 @@ class MoEPipeline:
         _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[0].record(sp)
-        flags = lay.tiled | (4 if use_mt else 0)
+        flags = lay.tiled | (4 if use_mt else 0) | (2 if use_pair else 0)
         _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), flags, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:

@@ -1,7 +1,7 @@
 """Device-resident engine (MoEPipeline) on a small Switch-like workload: routing (fused
 split-bf16 router) must be the workload's exact float64 routing at every layer, and the
 residual stream must not depend on how replicas/tiles are laid out (replication on,
-split, off, and the multi-tile FFN kernel give the same bits)."""
+split, off, the multi-tile and the CTA-pair FFN kernels give the same bits)."""
 
 import pytest
 import torch
@@ -29,7 +29,7 @@ def _run(replication="on", ffn="two", sru_pipeline=True, full=False):
 def test_engine_routing_exact_and_layout_independent():
     x_on, r_on, oracle = _run("on")
     assert (r_on.long() == oracle.long()).all()
-    for rep, ffn in (("split", "two"), ("off", "two"), ("on", "mt")):
+    for rep, ffn in (("split", "two"), ("off", "two"), ("on", "mt"), ("on", "pair")):
         x, r, _ = _run(rep, ffn)
         assert torch.equal(r, r_on), (rep, ffn)
         assert torch.equal(x, x_on), (rep, ffn)

@@ -14,8 +14,13 @@ from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig  # noqa: E4
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--replication", default="on")
+    ap.add_argument("--experts", type=int, default=None)
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--capacity", type=int, default=None)
     args = ap.parse_args()
-    cfg = PipelineConfig(replication=args.replication)
+    kw = {k: v for k, v in (("num_experts", args.experts), ("num_layers", args.layers), ("capacity", args.capacity))
+          if v is not None}
+    cfg = PipelineConfig(replication=args.replication, **kw)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         pipe = MoEPipeline(cfg)
