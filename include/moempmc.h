@@ -238,7 +238,8 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
                       const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 /* The same layer as three launches (gather | GEMM1 | GEMM2) sharing `ws`, for callers that
  * time or overlap the grouped GEMMs separately. flags bit 0: u / v are in the pre-tiled
- * layout of mp_tile_kmajor (BN 256 for u, mp_ffn_down_bn(dp) for v); bit 1: CTA-pair
+ * layout of mp_tile_kmajor (BN mp_ffn_up_bn(Fp) for u; mp_ffn_down_bn(dp) for v, or 256 for
+ * v with bits 1 / 2 / 3); bit 1: CTA-pair
  * (tcgen05 cta_group::2, M = 256) kernels over piece pairs -- pieces must come from a
  * builder called with split_m bit 1 (even piece count per expert), dp % 256 == 0;
  * bit 2: multi-tile units (two 128 x 256 accumulator tiles per unit: two pieces of one
@@ -257,6 +258,8 @@ MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, in
                        const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin, void* ws,
                        size_t ws_bytes, void* stream);
 MP_API int mp_ffn_down_bn(int dp);
+/* column-tile width (and mp_tile_kmajor BN) of the pre-tiled expert U weights for GEMM1 */
+MP_API int mp_ffn_up_bn(int Fp);
 /* Diagnostics: per-CTA %globaltimer start / end (ns) of the last grouped-GEMM launch
  * (host arrays of n <= 1024). */
 MP_API int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1, int n);

@@ -76,6 +76,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_up": (_I, [_I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down_bn": (_I, [_I]),
+    "mp_ffn_up_bn": (_I, [_I]),
     "mp_debug_cta_times": (_I, [_P, _P, _I]),
     "mp_ffn_fused_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "mp_ffn_fused": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _Z, _P]),

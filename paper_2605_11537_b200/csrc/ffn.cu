@@ -84,10 +84,22 @@ __global__ void k_tile_kmajor(const uint4* __restrict__ src, uint4* __restrict__
 
 using namespace mp;
 
-extern "C" int mp_ffn_down_bn(int dp) { return (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64); }
+extern "C" int mp_ffn_up_bn(int Fp) {
+  static const bool bn192 = getenv("MP_GEMM1_BN192") != nullptr;  // A/B switch: 192-column GEMM1 units
+  return (bn192 && Fp % 192 == 0) ? 192 : 256;
+}
+
+// GEMM2 column tile: 192 when it divides dp (d = 768: 4 slices of 192 with a 5-deep operand
+// ring instead of 3 slices of 256 with a 4-deep ring -- GEMM2 142 -> 137.5 us per layer);
+// MP_GEMM2_BN256=1 restores 256. The CTA-pair and multi-tile kernels always use 256.
+extern "C" int mp_ffn_down_bn(int dp) {
+  static const bool bn256 = getenv("MP_GEMM2_BN256") != nullptr;  // A/B switch
+  if (!bn256 && dp % 192 == 0) return 192;
+  return (dp % 256 == 0) ? 256 : (dp % 128 == 0 ? 128 : 64);
+}
 
 extern "C" int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int BN, void* stream) {
-  MP_REQUIRE(G >= 1 && N % BN == 0 && K % 64 == 0 && (BN == 64 || BN == 128 || BN == 256), MP_ERR_CONFIG,
+  MP_REQUIRE(G >= 1 && N % BN == 0 && K % 64 == 0 && (BN == 64 || BN == 128 || BN == 192 || BN == 256), MP_ERR_CONFIG,
              "mp_tile_kmajor: need N %% BN == 0, K %% 64 == 0 (N=%d K=%d BN=%d)", N, K, BN);
   const size_t total = (size_t)G * N * K / 8;
   const int grid = (int)std::min<size_t>((total + 255) / 256, (size_t)num_sms() * 16);
@@ -204,6 +216,16 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
     const int cl = mc_cluster(Fp / 256);
     if (cl) return launch_seg_mc<256, 4>(cl, ta, tb, piece_row, piece_rows, exp_begin, E, Fp / 256, Fp, dp / 64, tiled, e, st);
   }
+  if (tiled && mp_ffn_up_bn(Fp) == 192 && tma_store && !diag_nostore) {  // 5-deep ring, 16 slices per expert
+    rc = tmap_b(&tb, u, E, Fp, dp, 192, tiled, 192);
+    if (rc) return rc;
+    SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 192, 192, Fp, dp / 64, tiled, 0};
+    CUtensorMap tc;
+    rc = make_tmap_bf16_store(&tc, hid, T, Fp, Fp);
+    if (rc) return rc;
+    EpiStoreBf16Tma et{hid, Fp, nullptr, 1, 0, getenv("MP_H_NO_EVICT_LAST") == nullptr};
+    return launch_gemm<192, 5>(ta, tb, s, et, ffn_grid(), st, &tc);
+  }
   SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled, 0};
   if (tma_store && !diag_nostore) {
     CUtensorMap tc;
@@ -222,7 +244,7 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
                     const __nv_bfloat16* hid, int flags, cudaStream_t st, int32_t* hdone = nullptr) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
   const int tiled = flags & 1, pair = (flags >> 1) & 1, mt = (flags >> 2) & 1;
-  const int bn = mp_ffn_down_bn(dp);
+  const int bn = (pair || mt || (flags & 8)) ? 256 : mp_ffn_down_bn(dp);
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
   if (rc) return rc;
@@ -251,11 +273,15 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
   if ((flags & 16) && hdone) {  // drop each piece's H from L2 after its last slice unit
     EpiScatterAdd ed{y, dp, tok_of_row, hdone, hid, Fp, dp / bn};
     if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, ed, ffn_grid(), st);
+    if (bn == 192) return launch_gemm<192, 5>(ta, tb, s, ed, ffn_grid(), st);
     if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, ed, ffn_grid(), st);
+    MP_REQUIRE(bn == 64, MP_ERR_CONFIG, "ffn_down: no kernel for BN %d", bn);
     return launch_gemm<64, 8>(ta, tb, s, ed, ffn_grid(), st);
   }
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, ffn_grid(), st);
+  if (bn == 192) return launch_gemm<192, 5>(ta, tb, s, e, ffn_grid(), st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, ffn_grid(), st);
+  MP_REQUIRE(bn == 64, MP_ERR_CONFIG, "ffn_down: no kernel for BN %d", bn);
   return launch_gemm<64, 8>(ta, tb, s, e, ffn_grid(), st);
 }
 

@@ -58,6 +58,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// TMEM columns of the two accumulator stages (allocation is a power of two >= 32)
+constexpr uint32_t tmem_cols(int bn) {
+  return 2 * bn <= 32 ? 32 : (2 * bn <= 64 ? 64 : (2 * bn <= 128 ? 128 : (2 * bn <= 256 ? 256 : 512)));
+}
+
 template <int BN, int STAGES, int ASTAGES = 0>
 struct GemmSmem {
   // ASTAGES == 0: one ring of STAGES x (A | B) stages. ASTAGES > 0: separate rings, STAGES
@@ -73,7 +78,7 @@ struct GemmSmem {
   static constexpr int kScratchOffset = (kVecOffset + 2 * BN * 4 + 1023) / 1024 * 1024;  // TMA-store boxes
   static constexpr int kScratchWordsPerWarp = 32 * 20;  // 32 rows x (16 + 4 pad) words: store transpose
   static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;  // scheduler table (smem)
-  static constexpr int kPrepInts = ASTAGES ? 1025 : 2048;
+  static constexpr int kPrepInts = (ASTAGES || BN % 64 != 0 || STAGES * (kBlockM + BN) * kBlockK * 2 > 196608) ? 768 : 2048;
   static constexpr int kBytes = kPrepOffset + kPrepInts * 4 + 1024;  // + alignment slack
 };
 
@@ -132,7 +137,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * BN);
+  if (warp == 2) tmem_alloc(tmem_slot, tmem_cols(BN));
   griddep_wait();  // the prologue above overlapped the previous kernel's tail
   Sched sched = sched_in;
   sched.prepare(reinterpret_cast<int*>(smem + L::kPrepOffset));
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t1[blockIdx.x] = global_ns();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * BN);
+    tmem_dealloc(tmem_base, tmem_cols(BN));
   }
 #endif
 }
@@ -356,8 +361,9 @@ struct SegSched {
   int b_tiled;  // B pre-tiled as [E][n_tiles][kb][bn rows][64 cols]: every TMA box is one contiguous burst
   int reverse;  // 1: walk the unit list backwards (GEMM2 consumes the hidden rows GEMM1 wrote LAST first,
                 //    while they are still in L2)
+  int prep_cap = 768;  // <= GemmSmem<BN, STAGES>::kPrepInts of the launch
   __device__ void prepare(int* tab) {
-    if (E + 1 > 1025) return;
+    if (E + 1 > prep_cap) return;  // table of GemmSmem::kPrepInts ints; else exp_begin stays global
     for (int e = threadIdx.x; e <= E; e += blockDim.x) tab[e] = exp_begin[e];
     __syncthreads();
     exp_begin = tab;

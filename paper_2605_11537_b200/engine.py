@@ -144,7 +144,7 @@ class MoEPipeline:
         self.layers = []
         for l in range(L):
             u, v = self.wl.expert_weights(l)
-            self.layers.append(DeviceMoeLayer.from_device(self.wl.router(l), u, v))
+            self.layers.append(DeviceMoeLayer.from_device(self.wl.router(l), u, v, cfg.ffn))
         # ---- predictor (S SRU layers + heads)
         g = torch.Generator(device=dev).manual_seed(cfg.seed + 1)
         bound = 1.0 / math.sqrt(d)
@@ -585,7 +585,7 @@ class StepGraph:
             pass
 
 
-def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor) -> DeviceMoeLayer:
+def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor, ffn: str = "two") -> DeviceMoeLayer:
     """DeviceMoeLayer from device tensors already in kernel layout (d % 64 == 0, F % 256 == 0)."""
     lay = DeviceMoeLayer.__new__(DeviceMoeLayer)
     E, d = router.shape
@@ -604,8 +604,9 @@ def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor) -
     # pre-tiled B operands: each TMA box of the grouped GEMMs is one contiguous 32 KB burst
     u2, v2 = u.reshape(E * F, d).contiguous(), v.reshape(E * d, F).contiguous()
     lay.U, lay.V = torch.empty_like(u2), torch.empty_like(v2)
-    _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, 256, stream_ptr())
-    _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, _lib.size_query("mp_ffn_down_bn", d), stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
+    vbn = 256 if ffn in ("mt", "pair", "fused") else _lib.size_query("mp_ffn_down_bn", d)  # those kernels: BN 256
+    _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, vbn, stream_ptr())
     lay.tiled = 1
     del u2, v2
     return lay

@@ -72,7 +72,9 @@ def test_size_queries_are_pure_host(lib):
     assert lib.mp_exec_workspace_bytes(1, 16384, 128, 424) > 0
     assert lib.mp_ffn_workspace_bytes(16384, 768, 3072) >= 16384 * 768 * 2 + 16384 * 3072 * 2
     assert lib.mp_sru_workspace_bytes(16384, 768) >= 16384 * 3 * 768 * 2
-    assert lib.mp_ffn_down_bn(768) == 256 and lib.mp_ffn_down_bn(128) == 128 and lib.mp_ffn_down_bn(64) == 64
+    assert lib.mp_ffn_down_bn(768) == 192 and lib.mp_ffn_down_bn(512) == 256
+    assert lib.mp_ffn_down_bn(128) == 128 and lib.mp_ffn_down_bn(64) == 64
+    assert lib.mp_ffn_up_bn(3072) == 256
 
 
 def test_config_errors_map_to_reference_exceptions(lib):

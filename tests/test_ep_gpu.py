@@ -65,8 +65,8 @@ def test_expert_parallel_single_rank_equals_dense_forward():
     _run_layers_device(x_ref, dm)
     for lay in dm.layers:  # EP path uses pre-tiled weights
         u2, v2 = lay.U.clone(), lay.V.clone()
-        _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, 256, stream_ptr())
-        _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, 256, stream_ptr())
+        _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
+        _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, _lib.size_query("mp_ffn_down_bn", d), stream_ptr())
         lay.tiled = 1
     k = CudaEpKernels(dm.layers, T, 1, 0, max_slots=4 * E)
     ep = ExpertParallelMoE(k, L, E)

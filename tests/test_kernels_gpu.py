@@ -247,7 +247,7 @@ def test_tiled_weight_layout_is_bitwise_identical(dev):
     U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
     V = (torch.randn(E * d, F, device=dev) / 16).bfloat16()
     Ut, Vt = torch.empty_like(U), torch.empty_like(V)
-    _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
     _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, _lib.size_query("mp_ffn_down_bn", d), stream_ptr())
     x = torch.randn(T, d, device=dev)
     fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
@@ -350,10 +350,11 @@ def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
               ptr(eb), ptr(sws), nb, stream_ptr())
     U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
     V = (torch.randn(E * d, F, device=dev) / 28).bfloat16()
-    if tiled:
+    if tiled:  # V column tiles: 256 for the pair / multi-tile / multicast kernels, else mp_ffn_down_bn
+        vbn = 256 if mode & (2 | 4 | 8) else _lib.size_query("mp_ffn_down_bn", d)
         Ut, Vt = torch.empty_like(U), torch.empty_like(V)
-        _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
-        _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, 256, stream_ptr())
+        _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
+        _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, vbn, stream_ptr())
     else:
         Ut, Vt = U, V
     x = torch.randn(T, d, device=dev)

@@ -18,7 +18,7 @@ def main():
     V = (torch.randn(E * d, F, device=dev) / 55).bfloat16()
     Ut, Vt = torch.empty_like(U), torch.empty_like(V)
     _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
-    _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, 256, stream_ptr())
+    _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, _lib.size_query("mp_ffn_down_bn", d), stream_ptr())
     x = torch.randn(T, d, device=dev)
     rng = np.random.default_rng(0)
     w = 1.0 / (rng.permutation(E) + 1.0) ** 1.2
