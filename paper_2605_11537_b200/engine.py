@@ -366,6 +366,8 @@ class MoEPipeline:
         self.ws_gplace = torch.empty(self.ws_gplace_n, dtype=torch.uint8, device=self.dev)
         self.ws_ghist_n = _lib.size_query("mp_histogram_workspace_bytes", cfg.num_layers, GT, cfg.num_experts)
         self.ws_ghist = torch.empty(self.ws_ghist_n, dtype=torch.uint8, device=self.dev)
+        # tests: issue the collectives (NCCL all-gathers, all-to-alls) even when world == 1
+        self.force_collectives = False
 
     def predict_sharded(self, x: torch.Tensor, sp: int) -> int:
         """Predictor over a token-sharded batch: the G ranks' token ranges are ONE sequence
@@ -403,9 +405,11 @@ class MoEPipeline:
 
         cfg, L, T, E = self.cfg, self.cfg.num_layers, self.cfg.tokens, self.cfg.num_experts
         sp = stream_ptr()
-        n = self.predict_sharded(x, sp) if self.world > 1 else self.predict(x, sp)
+        coll = self.world > 1 or self.force_collectives
+        self.ep.force_collectives = self.force_collectives
+        n = self.predict_sharded(x, sp) if coll else self.predict(x, sp)
         parts = list(self.g_assign.view(L, self.world, T).unbind(1))
-        if self.world > 1:
+        if coll:
             gathered = [torch.empty(L, T, dtype=torch.int32, device=self.dev) for _ in range(self.world)]
             dist.all_gather(gathered, self.assign, group=self.group)
             for r in range(self.world):

@@ -140,18 +140,19 @@ class ExpertParallelMoE:
         self.group = group
         self.G = dist.get_world_size(group) if dist.is_initialized() else 1
         self.L, self.E = num_layers, num_experts
+        self.force_collectives = False  # tests: NCCL calls even when G == 1
         # residency state (replicated on every rank, updated identically)
         self.res = torch.zeros(num_layers, num_experts, dtype=torch.int32, device=getattr(kernels, "dev", "cpu"))
 
     def _all_gather_counts(self, counts: torch.Tensor) -> torch.Tensor:
-        if self.G == 1:
+        if self.G == 1 and not self.force_collectives:
             return counts.view(1, -1)
         parts = [torch.empty_like(counts) for _ in range(self.G)]
         dist.all_gather(parts, counts, group=self.group)
         return torch.stack(parts)
 
     def _a2a(self, out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits) -> None:
-        if self.G == 1:
+        if self.G == 1 and not self.force_collectives:
             out.copy_(inp)
             return
         dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits, group=self.group)
