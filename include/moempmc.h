@@ -249,7 +249,10 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
  * tile loaded once and multicast to the cluster (slice count divisible by 2, 3 or 4).
  * bit 4 (mp_ffn_down, after mp_ffn_gather with the same ws): once the last slice unit of
  * a piece has consumed its hidden rows, GEMM2 drops them from L2 (discard.global.L2, no
- * write-back of dead data). Every mode gives bitwise identical results. */
+ * write-back of dead data). Every mode gives bitwise identical results.
+ * bit 5 (mp_ffn_down): store y[tok_of_row[row]] = result instead of adding it (every target
+ *   row has exactly one writer; the expert-parallel receive buffer then needs no zeroing).
+ */
 MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                          size_t ws_bytes, void* stream);
 MP_API int mp_ffn_up(int T, int dp, int Fp, int E, const void* u, int flags, const int32_t* piece_row,

@@ -50,6 +50,8 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
   int* s_off = sm;                   // E + 1
   int* s_lb = s_off + E + 1;         // max_slots + 1 : local base (hosted slots)
   int* s_pc = s_lb + max_slots + 1;  // max_slots + 1 : pieces per slot
+  int* s_gpu = s_pc + max_slots + 1; // max_slots     : GPU of each slot
+  int* s_rows = s_gpu + max_slots;   // G x max_slots : rows of (source, slot), for the per-peer scans
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int n = 0, b = 0;
     for (int g = 0; g < G; ++g) {
@@ -88,10 +90,12 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
       const int cg = C[(size_t)g * E + e];
       const int r = runs_before(acc + cg, j, c) - runs_before(acc, j, c);
       w.rows[(size_t)g * max_slots + s] = r;
+      s_rows[(size_t)g * max_slots + s] = r;
       size += r;
       acc += cg;
     }
     w.slot_gpu[s] = gpu;
+    s_gpu[s] = gpu;
     w.slot_size[s] = size;
     s_lb[s] = (gpu == rank) ? size : 0;
     s_pc[s] = (gpu == rank) ? (split ? cdiv(size, kBlockMRows) : (size > 0 ? 1 : 0)) : 0;
@@ -106,26 +110,39 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
   }
   __syncthreads();
   // sender tables (this rank) and receiver tables, one thread per peer
-  if (threadIdx.x < G) {
-    const int d = threadIdx.x;
-    int acc = 0;
-    for (int s = 0; s < S; ++s)
-      if (w.slot_gpu[s] == d) {
-        w.send_base[s] = acc;  // relative to the destination's block
-        acc += w.rows[(size_t)rank * max_slots + s];
+  {  // per peer d (one warp each, G <= 32): exclusive scans over the slots, 32 slots per step
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < G) {
+      const int d = warp;
+      int acc_s = 0, acc_r = 0;
+      for (int base = 0; base < S; base += 32) {
+        const int s = base + lane;
+        const int gpu = s < S ? s_gpu[s] : -1;
+        const int vs = gpu == d ? s_rows[(size_t)rank * max_slots + s] : 0;  // this rank sends slot s to d
+        const int vr = gpu == rank ? s_rows[(size_t)d * max_slots + s] : 0;  // d sends slot s here
+        int is = vs, ir = vr;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int ys = __shfl_up_sync(0xffffffffu, is, o), yr = __shfl_up_sync(0xffffffffu, ir, o);
+          if (lane >= o) {
+            is += ys;
+            ir += yr;
+          }
+        }
+        if (gpu == d) w.send_base[s] = acc_s + is - vs;                              // within d's block
+        if (gpu == rank) w.recv_start[(size_t)d * max_slots + s] = acc_r + ir - vr;  // within d's block
+        acc_s += __shfl_sync(0xffffffffu, is, 31);
+        acc_r += __shfl_sync(0xffffffffu, ir, 31);
       }
-    send_counts[d] = acc;
-    int acc2 = 0;
-    for (int s = 0; s < S; ++s)
-      if (w.slot_gpu[s] == rank) {
-        w.recv_start[(size_t)d * max_slots + s] = acc2;  // relative to source d's block
-        acc2 += w.rows[(size_t)d * max_slots + s];
+      if (lane == 0) {
+        send_counts[d] = acc_s;
+        recv_counts[d] = acc_r;
       }
-    recv_counts[d] = acc2;
+    }
   }
   __syncthreads();
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    const int gpu = w.slot_gpu[s];
+    const int gpu = s_gpu[s];
     int displ = 0;
     for (int g = 0; g < gpu; ++g) displ += send_counts[g];
     w.send_base[s] += displ;
@@ -133,7 +150,7 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
       int acc = s_lb[s], rdispl = 0;
       for (int g = 0; g < G; ++g) {
         w.local_start[(size_t)g * max_slots + s] = acc;
-        acc += w.rows[(size_t)g * max_slots + s];
+        acc += s_rows[(size_t)g * max_slots + s];
         w.recv_start[(size_t)g * max_slots + s] += rdispl;
         rdispl += recv_counts[g];
       }
@@ -185,19 +202,17 @@ __global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32
   }
 }
 
-// Receiver: local row of every received row, per (source, hosted slot) run. grid G.
+// Receiver: local row of every received row, per (source, hosted slot) run.
+// grid (max_slots, G): one block per (slot, source); slots beyond the plan's count exit.
 __global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ num_slots_p, int rank, EpPlanWs w,
                               int32_t* __restrict__ recv_of_local) {
   griddep_launch_dependents();
   griddep_wait();
-  const int g = blockIdx.x;
-  const int ns = *num_slots_p;
-  for (int s = 0; s < ns; ++s) {
-    if (w.slot_gpu[s] != rank) continue;
-    const int n = w.rows[(size_t)g * max_slots + s];
-    const int r0 = w.recv_start[(size_t)g * max_slots + s], l0 = w.local_start[(size_t)g * max_slots + s];
-    for (int k = threadIdx.x; k < n; k += blockDim.x) recv_of_local[l0 + k] = r0 + k;
-  }
+  const int s = blockIdx.x, g = blockIdx.y;
+  if (s >= *num_slots_p || w.slot_gpu[s] != rank) return;
+  const int n = w.rows[(size_t)g * max_slots + s];
+  const int r0 = w.recv_start[(size_t)g * max_slots + s], l0 = w.local_start[(size_t)g * max_slots + s];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) recv_of_local[l0 + k] = r0 + k;
 }
 
 // xperm[row] = buf[idx[row]] for bf16 rows; one warp per row.
@@ -278,8 +293,8 @@ extern "C" int mp_ep_plan(const int32_t* route, int T, const int32_t* C, int G, 
   const int nch = cdiv(T > 0 ? T : 1, kChunk);
   int32_t *cc, *err, *nslots;
   EpPlanWs w = carve(ws, G, E, max_slots, &cc, nch, &err, &nslots);
-  const size_t sm = sizeof(int) * ((size_t)E + 1 + 2 * ((size_t)max_slots + 1));
-  MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_ep_plan: E/max_slots too large");
+  const size_t sm = sizeof(int) * ((size_t)E + 1 + 2 * ((size_t)max_slots + 1) + (size_t)(G + 1) * max_slots);
+  MP_REQUIRE(sm <= 200 * 1024, MP_ERR_CONFIG, "mp_ep_plan: G x max_slots too large for shared memory");
   static bool configured = false;
   if (!configured) {
     MP_CUDA_TRY(cudaFuncSetAttribute(k_ep_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024)));
@@ -312,7 +327,8 @@ extern "C" int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, c
   EpPlanWs w = carve(ws, G, E, max_slots, &cc, nch, &err, &nslots);
   MP_REQUIRE(ws_bytes >= mp_ep_workspace_bytes(G, T, E, max_slots), MP_ERR_CONFIG, "mp_ep_recv_layout: workspace");
   // number of slots = off[E]
-  k_ep_recv_map<<<G, 256, 0, (cudaStream_t)stream>>>(G, max_slots, w.off + E, rank, w, recv_of_local);
+  k_ep_recv_map<<<dim3(max_slots, G), 128, 0, (cudaStream_t)stream>>>(G, max_slots, w.off + E, rank, w,
+                                                                       recv_of_local);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

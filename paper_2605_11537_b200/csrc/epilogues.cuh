@@ -227,6 +227,8 @@ struct EpiScatterAdd {
   const __nv_bfloat16* hid;   // A operand (rows x ldh)
   int ldh;
   int n_slices;
+  int store = 0;              // 1: plain stores (x[tok] = y) -- every target row has exactly one
+                              //    writer (the expert-parallel receive buffer needs no zeroing)
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
   template <int NC>
   __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float*,
@@ -256,7 +258,13 @@ struct EpiScatterAdd {
         for (int it = 0; it < 4; ++it) {
           const int row = it * 8 + (lane >> 2);
           const float4 a = *reinterpret_cast<const float4*>(scratch + row * 20 + pq * 4);
-          if (tt[it] >= 0) red_add_v4(reinterpret_cast<float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq, a);
+          if (tt[it] >= 0) {
+            float4* dst = reinterpret_cast<float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq;
+            if (store)
+              *dst = a;
+            else
+              red_add_v4(dst, a);
+          }
         }
         __syncwarp();
       }

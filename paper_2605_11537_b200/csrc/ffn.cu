@@ -252,13 +252,13 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
     MP_REQUIRE(bn == 256 && E <= kMtMaxE, MP_ERR_CONFIG, "ffn multi-tile mode: dp %% 256 == 0, E <= %d", kMtMaxE);
     rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, 128);
     if (rc) return rc;
-    EpiScatterAdd ea{y, dp, tok_of_row};
+    EpiScatterAdd ea{y, dp, tok_of_row, nullptr, nullptr, 0, 0, (flags >> 5) & 1};
     FfnMtSched s{piece_row, piece_rows, exp_begin, E, dp / 256, Fp / 64, dp, tiled, mt_single()};
     return launch_ffn_mt(ta, tb, s, ea, st);
   }
   rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
   if (rc) return rc;
-  EpiScatterAdd e{y, dp, tok_of_row, nullptr, nullptr, 0, 0};
+  EpiScatterAdd e{y, dp, tok_of_row, nullptr, nullptr, 0, 0, (flags >> 5) & 1};
   if (pair) {
     MP_REQUIRE(bn == 256, MP_ERR_CONFIG, "ffn pair mode needs dp %% 256 == 0");
     Seg2Sched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};

@@ -106,7 +106,8 @@ class CudaEpKernels:
 
     def expert_ffn(self, recvbuf: torch.Tensor, plan: EpPlan, l: int, ev=None) -> torch.Tensor:
         n = recvbuf.shape[0]
-        y = torch.zeros(n, self.d, dtype=torch.float32, device=self.dev)
+        # GEMM2 stores (flags bit 5) into the receive-order rows: each row has exactly one writer
+        y = torch.empty(n, self.d, dtype=torch.float32, device=self.dev)
         if n == 0:
             return y
         lay = self.layers[l]
@@ -122,7 +123,8 @@ class CudaEpKernels:
                   ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
         if ev is not None:
             ev[1].record(sp)
-        _lib.call("mp_ffn_down", ptr(y), n, self.d, self.F, self.E, ptr(lay.V), lay.tiled | self.ffn_flags, ptr(self.recv_of_local),
+        _lib.call("mp_ffn_down", ptr(y), n, self.d, self.F, self.E, ptr(lay.V), lay.tiled | self.ffn_flags | 32,
+                  ptr(self.recv_of_local),
                   ptr(plan.piece_row), ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
         if ev is not None:
             ev[2].record(sp)
