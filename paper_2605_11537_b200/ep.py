@@ -72,9 +72,17 @@ class CudaEpKernels:
         self.ffn_n = _lib.size_query("mp_ffn_workspace_bytes", self.cap_rows, self.d, self.F)
         self.ffn_ws = torch.empty(self.ffn_n, dtype=torch.uint8, device=dev)
         self.counts_buf = torch.empty(self.E, **i32)
-        self.sc = torch.empty(world, **i32)
-        self.rc = torch.empty(world, **i32)
-        self.nloc = torch.empty(1, **i32)
+        self.sizes = torch.empty(2 * world + 1, **i32)  # send counts | recv counts | local rows
+        self.sc, self.rc, self.nloc = self.sizes[:world], self.sizes[world:2 * world], self.sizes[2 * world:]
+        self.sizes_host = torch.empty(2 * world + 1, dtype=torch.int32, pin_memory=True)
+        self.sizes_ready = torch.cuda.Event()
+        # capacity buffers (no per-layer allocation): a rank sends at most T rows and receives
+        # at most G * T
+        self.sendbuf = torch.empty(tokens, self.d, dtype=torch.bfloat16, device=dev)
+        self.recvbuf = torch.empty(self.cap_rows, self.d, dtype=torch.bfloat16, device=dev)
+        self.ybuf = torch.empty(self.cap_rows, self.d, dtype=torch.float32, device=dev)
+        self.yback = torch.empty(tokens, self.d, dtype=torch.float32, device=dev)
+        self._packed_for = None
         self.send_pos = torch.empty(tokens, **i32)
         self.piece_row = torch.empty(self.pstride, **i32)
         self.piece_rows = torch.empty(self.pstride, **i32)
@@ -89,30 +97,55 @@ class CudaEpKernels:
                   self.hist_n, stream_ptr())
         return self.counts_buf
 
-    def plan(self, route: torch.Tensor, C: torch.Tensor, res: torch.Tensor) -> EpPlan:
+    def plan(self, route: torch.Tensor, C: torch.Tensor, res: torch.Tensor, x: torch.Tensor = None) -> EpPlan:
+        """Plan the layer; the split sizes come back to the host (one small D2H per layer: NCCL's
+        variable all-to-all needs them). With ``x`` the dispatch rows are packed into the
+        capacity send buffer BEFORE the host waits, so the pack overlaps the read-back."""
         T = route.shape[0]
+        sp = stream_ptr()
         _lib.call("mp_ep_plan", ptr(route), T, ptr(C), self.G, self.E, self.rank, self.max_slots, 1, ptr(res),
                   ptr(self.sc), ptr(self.rc), ptr(self.nloc), ptr(self.send_pos), ptr(self.piece_row),
-                  ptr(self.piece_rows), ptr(self.exp_begin), ptr(self.ws), self.ws_n, stream_ptr())
-        host = torch.cat([self.sc, self.rc, self.nloc]).cpu().tolist()  # one small D2H per layer
+                  ptr(self.piece_rows), ptr(self.exp_begin), ptr(self.ws), self.ws_n, sp)
+        self.sizes_host.copy_(self.sizes, non_blocking=True)
+        self.sizes_ready.record()
+        self._packed_for = None
+        self._layout_ready = False
+        if x is not None:
+            _lib.call("mp_ep_pack", ptr(x), T, self.d, ptr(self.send_pos), ptr(self.sendbuf), sp)
+            self._packed_for = x
+            # the receive-side row map needs only the plan: also ahead of the host wait
+            _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
+                      ptr(self.recv_of_local), ptr(self.ws), self.ws_n, sp)
+            self._layout_ready = True
+        self.sizes_ready.synchronize()
+        host = self.sizes_host.tolist()
         G = self.G
         return EpPlan(host[:G], host[G:2 * G], host[2 * G], self.send_pos[:T], self.piece_row, self.piece_rows,
                       self.exp_begin)
 
     def pack(self, x: torch.Tensor, plan: EpPlan, n_send: int) -> torch.Tensor:
-        buf = torch.empty(n_send, self.d, dtype=torch.bfloat16, device=self.dev)
-        _lib.call("mp_ep_pack", ptr(x), x.shape[0], self.d, ptr(plan.send_pos), ptr(buf), stream_ptr())
-        return buf
+        if self._packed_for is not x:
+            _lib.call("mp_ep_pack", ptr(x), x.shape[0], self.d, ptr(plan.send_pos), ptr(self.sendbuf), stream_ptr())
+        self._packed_for = None
+        return self.sendbuf[:n_send]
+
+    def recv_buffer(self, n: int) -> torch.Tensor:
+        return self.recvbuf[:n]
+
+    def back_buffer(self, n: int) -> torch.Tensor:
+        return self.yback[:n]
 
     def expert_ffn(self, recvbuf: torch.Tensor, plan: EpPlan, l: int, ev=None) -> torch.Tensor:
         n = recvbuf.shape[0]
         # GEMM2 stores (flags bit 5) into the receive-order rows: each row has exactly one writer
-        y = torch.empty(n, self.d, dtype=torch.float32, device=self.dev)
+        y = self.ybuf[:n]
         if n == 0:
             return y
         lay = self.layers[l]
-        _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
-                  ptr(self.recv_of_local), ptr(self.ws), self.ws_n, stream_ptr())
+        if not getattr(self, "_layout_ready", False):
+            _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
+                      ptr(self.recv_of_local), ptr(self.ws), self.ws_n, stream_ptr())
+        self._layout_ready = False
         # xperm region of the FFN workspace <- received rows in local (slot-major) order
         _lib.call("mp_gather_rows_bf16", ptr(recvbuf), n, self.d, ptr(self.recv_of_local), ptr(self.ffn_ws),
                   stream_ptr())
@@ -163,12 +196,16 @@ class ExpertParallelMoE:
         k = self.k
         route = k.route(x, l)
         C = self._all_gather_counts(k.counts(route))
-        plan = k.plan(route, C, self.res[l])
+        early = hasattr(k, "recv_buffer")  # device kernels: pack before the host reads the split sizes
+        plan = k.plan(route, C, self.res[l], x) if early else k.plan(route, C, self.res[l])
         sendbuf = k.pack(x, plan, sum(plan.send_counts))
-        recvbuf = torch.empty(sum(plan.recv_counts), x.shape[1], dtype=sendbuf.dtype, device=sendbuf.device)
+        n_recv = sum(plan.recv_counts)
+        recvbuf = k.recv_buffer(n_recv) if early else \
+            torch.empty(n_recv, x.shape[1], dtype=sendbuf.dtype, device=sendbuf.device)
         self._a2a(recvbuf, sendbuf, plan.recv_counts, plan.send_counts)
         y = k.expert_ffn(recvbuf, plan, l, ev) if ev is not None else k.expert_ffn(recvbuf, plan, l)
-        yback = torch.empty(sum(plan.send_counts), x.shape[1], dtype=y.dtype, device=y.device)
+        n_send = sum(plan.send_counts)
+        yback = k.back_buffer(n_send) if early else torch.empty(n_send, x.shape[1], dtype=y.dtype, device=y.device)
         self._a2a(yback, y, plan.send_counts, plan.recv_counts)
         k.combine(x, yback, plan)
         self.last_route = route
