@@ -49,6 +49,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--skew", type=float, default=1.2, help="Zipf skew of the synthetic routing")
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
     p.add_argument("--ffn", choices=["two", "mt", "fused", "pair"], default="two")
@@ -250,7 +251,7 @@ def config_dict(args, world):
         "num_layers": args.layers, "num_experts": args.experts, "d_model": 768, "d_ff": 3072,
         "tokens_per_gpu": args.tokens, "global_batch": args.tokens * world, "sru_layers": 10,
         "capacity": args.capacity, "demand_unit": args.demand_unit, "replication": args.replication,
-        "predictor": args.predictor, "zipf_skew": 1.2, "parallelism": f"ep{world}" if world > 1 else ("ep1" if args.ep else "single"),
+        "predictor": args.predictor, "zipf_skew": args.skew, "parallelism": f"ep{world}" if world > 1 else ("ep1" if args.ep else "single"),
         "l2": "inputs larger than L2 (14.5 GB of expert weights streamed per step)",
     }
 
@@ -263,7 +264,7 @@ def run_ours(args):
 
     cfg = PipelineConfig(num_layers=args.layers, num_experts=args.experts, tokens=args.tokens,
                          capacity=args.capacity, demand_unit=args.demand_unit, replication=args.replication,
-                         predictor=args.predictor, ffn=args.ffn, seed=args.seed + rank)
+                         predictor=args.predictor, ffn=args.ffn, seed=args.seed + rank, skew=args.skew)
     pipe = MoEPipeline(cfg)
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
     ep = world > 1 or args.ep
