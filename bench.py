@@ -52,7 +52,7 @@ def parse_args():
     p.add_argument("--skew", type=float, default=1.2, help="Zipf skew of the synthetic routing")
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
-    p.add_argument("--ffn", choices=["two", "mt", "fused", "pair"], default="two")
+    p.add_argument("--ffn", choices=["auto", "two", "mt", "fused", "pair"], default="auto")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
     p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")
@@ -410,9 +410,10 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {
             "kernel": ("fused grouped expert FFN (k_ffn_fused: GEMM1 relu + GEMM2 scatter-combine, H in L2 ring)"
-                       if args.ffn == "fused" else
+                       if pipe.cfg.ffn == "fused" else
                        "grouped expert GEMM pair (GEMM1 relu + GEMM2 scatter-combine"
-                       + (", multi-tile units k_ffn_mt)" if args.ffn == "mt" and args.replication != "off" else ")")),
+                       + (", multi-tile units k_ffn_mt)" if pipe.cfg.ffn == "mt" and args.replication != "off" else
+                          ", CTA-pair cta_group::2 kernels)" if pipe.cfg.ffn == "pair" else ")")),
             "bound": "hbm",
             "achieved": achieved,
             "peak": peaks["hbm_gbs"],
@@ -433,6 +434,7 @@ def run_ours(args):
         "overlap": overlap is not None,
     }
 
+    result["config"]["ffn_kernels"] = pipe.cfg.ffn  # resolved from --ffn auto
     if not args.no_e2e:
         pipe._bench_x, pipe._bench_graph = x, graph
         result["e2e"] = run_e2e(args, pipe, batches, world)

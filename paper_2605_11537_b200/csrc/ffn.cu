@@ -210,6 +210,13 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
   if (rc) return rc;
   if (pair) {
     Seg2Sched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled};
+    if (tma_store && !diag_nostore) {  // H through TMA bulk stores, as in the 1-CTA kernel
+      CUtensorMap tc;
+      rc = make_tmap_bf16_store(&tc, hid, T, Fp, Fp);
+      if (rc) return rc;
+      EpiStoreBf16Tma et{hid, Fp, nullptr, 1, 0, getenv("MP_H_NO_EVICT_LAST") == nullptr};
+      return launch_gemm2<256, 6>(ta, tb, s, et, num_sms() & ~1, st, &tc);
+    }
     return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
   }
   if (flags & 8) {  // A tile multicast across a cluster of CTAs computing consecutive slices

@@ -86,7 +86,7 @@ struct Gemm2Smem {
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBarOffset = STAGES * kStageBytes;
   static constexpr int kVecOffset = kBarOffset + (2 * STAGES + 4) * 8 + 16;
-  static constexpr int kScratchOffset = kVecOffset + 2 * BN * 4;
+  static constexpr int kScratchOffset = (kVecOffset + 2 * BN * 4 + 1023) / 1024 * 1024;  // TMA-store boxes
   static constexpr int kScratchWordsPerWarp = 32 * 20;
   static constexpr int kPrepOffset = kScratchOffset + 8 * kScratchWordsPerWarp * 4;
   static constexpr int kBytes = kPrepOffset + 1025 * 4 + 1024;
@@ -107,7 +107,7 @@ struct PairUnit {
 template <int BN, int STAGES, class Sched, class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     k_umma_gemm2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Sched sched_in,
-                 Epi epi) {
+                 Epi epi, const __grid_constant__ CUtensorMap tmC) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using L = Gemm2Smem<BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
@@ -248,13 +248,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         if (active) {
           const uint32_t taddr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN + c0;
-          epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
-                               scratch_all + (warp - 4) * L::kScratchWordsPerWarp);
+          if constexpr (TmaStoreOf<Epi>::value)
+            epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
+                                 scratch_all + (warp - 4) * L::kScratchWordsPerWarp, &tmC);
+          else
+            epi.template run<NC>(U, mt, r, taddr, c0, svec + (tile & 1) * BN + c0,
+                                 scratch_all + (warp - 4) * L::kScratchWordsPerWarp);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader0 + as * 8);
       }
+    }
+    if constexpr (TmaStoreOf<Epi>::value) {
+      if (lane == 0) bulk_wait0();  // this warp's TMA stores complete before the CTA exits
     }
   }
   tc_fence_before();

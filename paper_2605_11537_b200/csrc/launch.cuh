@@ -44,7 +44,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched
 
 template <int BN, int STAGES, class Sched, class Epi>
 int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sched, const Epi& epi, int grid,
-                 cudaStream_t st) {
+                 cudaStream_t st, const CUtensorMap* tc = nullptr) {
   auto kern = k_umma_gemm2<BN, STAGES, Sched, Epi>;
   const int smem = Gemm2Smem<BN, STAGES>::kBytes;
   static bool configured = false;
@@ -54,7 +54,8 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb, const Sched& sche
   }
   if (grid < 2) grid = 2;
   grid &= ~1;  // whole clusters
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi);
+  CUtensorMap none{};
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, sched, epi, tc ? *tc : none);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

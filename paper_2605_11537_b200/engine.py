@@ -25,6 +25,7 @@ Replication modes (SURVEY.md §7 baselines):
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import math
 from dataclasses import asdict, dataclass
 
@@ -50,7 +51,8 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
-    ffn: str = "two"              # two (single-tile units) | mt (multi-tile units, slower: see DESIGN) | pair (CTA pairs) |
+    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else two) | two (single-tile units) |
+                                  # mt (multi-tile units, slower: see DESIGN) | pair (CTA pairs) |
                                   # fused (experimental: one launch, H in an L2 ring)
     sru_pipeline: bool = False    # two-stream token-half SRU pipeline (measured slower: 1219 vs 1133 us)
     skew: float = 1.2
@@ -133,6 +135,12 @@ class MoEPipeline:
     """Weights + buffers resident in HBM; ``step`` runs one batch with zero host syncs."""
 
     def __init__(self, cfg: PipelineConfig, device: torch.device | None = None, workload: SyntheticSwitch | None = None):
+        if cfg.ffn == "auto":
+            # CTA-pair grouped GEMMs once the layer is compute-heavy (>= 1024 tokens per expert:
+            # BASELINE config 2 runs at 1,126 vs 1,007 TF/s); single-CTA units on weight-streaming
+            # layers (config 3: 128 tokens per expert, pairs are 12 % slower) -- profiles/README.md
+            pair = cfg.tokens >= 1024 * cfg.num_experts and cfg.d_model % 256 == 0
+            cfg = dataclasses.replace(cfg, ffn="pair" if pair else "two")
         self.cfg = cfg
         self.dev = device or require_device()
         dev = self.dev
