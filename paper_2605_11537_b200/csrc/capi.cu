@@ -152,9 +152,17 @@ int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_
     rc = make_tmap_bf16(&tb2, B, N, K, K, bn / 2);
     if (rc) return rc;
     Dense2Sched s2{M, N / bn, K / 64, bn};
-    EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
     const int cu = cdiv(M, 2 * kBlockM) * (N / bn);
-    return launch_gemm2<256, 6>(ta, tb2, s2, e, std::min(2 * cu, num_sms()), st);
+    const int g2 = std::min(2 * cu, cap) & ~1;
+    if (ldc > 0 && getenv("MP_STG_EPILOGUE") == nullptr) {  // TMA bulk-store epilogue
+      CUtensorMap tc;
+      rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
+      if (rc) return rc;
+      EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from, store_hint};
+      return launch_gemm2<256, 6>(ta, tb2, s2, et, g2, st, &tc);
+    }
+    EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
+    return launch_gemm2<256, 6>(ta, tb2, s2, e, g2, st);
   }
   static const bool tma_store = getenv("MP_STG_EPILOGUE") == nullptr;  // A/B switch: st.global epilogue
   if (c_dtype == 0 && tma_store && bn == 256 && ldc > 0) {  // bf16 tile through TMA bulk stores
