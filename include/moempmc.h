@@ -105,6 +105,14 @@ MP_API int mp_exec_map(const int32_t* route, int L, int T, int E, int max_slots,
                 int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
                 int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin, void* ws,
                 size_t ws_bytes, void* stream);
+/* mp_exec_map for one layer after mp_route_top1_defer: re-decides the marked tokens in
+ * float64 (x = the stream the router read, w32 = E x d fp32 router rows), writes the exact
+ * routes back into route, then builds the same execution map as mp_exec_map. */
+MP_API int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
+                               int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
+                               int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
+                               const float* x, int ldx, int d, const float* w32, void* ws, size_t ws_bytes,
+                               void* stream);
 
 /* Replica segments from an explicit token -> slot map (a reference Placement,
  * src/router_oracle.py:64-74, as consumed by moe_forward :160-175): rows are
@@ -196,6 +204,12 @@ MP_API int mp_router_weight_absmax(const float* w_f32, int E, int d, float* w_ab
 MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
                             const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
                             void* stream);
+/* mp_route_top1_ex without its fp64 re-decision launch: tokens whose top-2 gap is inside the
+ * certified bound are written as route = -1 - e (the bf16 guess); mp_exec_map_recheck
+ * re-decides them in float64 (the same arithmetic) before counting. Eg in {64, 128},
+ * ldx % 4 == 0, 16-byte aligned x. route is only exact after mp_exec_map_recheck. */
+MP_API int mp_route_top1_defer(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
+                               int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ predictor training
  * SRU training on the GPU (reference src/predictor.py:238-379), float64 like the

@@ -47,6 +47,50 @@ __global__ void k_chunk_hist(const int32_t* __restrict__ assign, int T, int E, i
   for (int e = threadIdx.x; e < E; e += blockDim.x) out[e] = hist[e];
 }
 
+// k_chunk_hist for one layer whose routing came from mp_route_top1_defer: tokens marked
+// uncertain (route < 0) are first re-decided in float64 by their warp -- the arithmetic of
+// k_router_recheck (lane-strided partial sums, xor-shuffle reduction, first maximum), so the
+// routes equal mp_route_top1_ex's -- and written back.
+__global__ void k_chunk_hist_recheck(int32_t* __restrict__ route, int T, int E, int nch, int32_t* __restrict__ cc,
+                                     const float* __restrict__ x, int ldx, int d, const float* __restrict__ w) {
+  griddep_launch_dependents();
+  griddep_wait();
+  extern __shared__ int hist[];
+  const int ch = blockIdx.x, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int t = ch * kChunk + threadIdx.x;
+  int e = t < T ? route[t] : 0;
+  unsigned m = __ballot_sync(0xffffffffu, t < T && e < 0);
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    const int tj = t - lane + j;
+    const float* xr = x + (size_t)tj * ldx;
+    double best = 0.0;
+    int bi = 0;
+    for (int ee = 0; ee < E; ++ee) {
+      const float* wr = w + (size_t)ee * d;
+      double s = 0.0;
+      for (int k = lane; k < d; k += 32) s += (double)wr[k] * (double)xr[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (ee == 0 || s > best) {
+        best = s;
+        bi = ee;
+      }
+    }
+    if (lane == j) {
+      e = bi;
+      route[t] = bi;
+    }
+  }
+  if (t < T) atomicAdd(&hist[e], 1);
+  __syncthreads();
+  int32_t* out = cc + (size_t)ch * E;
+  for (int k = threadIdx.x; k < E; k += blockDim.x) out[k] = hist[k];
+}
+
 // In place: cc[l][ch][e] <- sum_{ch' < ch} cc[l][ch'][e]; demand[l][e] <- total. Grid
 // (ceil(E / 32), L), block 32 x 32 = (expert lane, chunk group); each thread scans
 // a contiguous run of chunks for one expert (coalesced 128 B rows), group totals are
@@ -902,6 +946,47 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
                                       piece_row, piece_rows, exp_begin, pieces_stride, err));
   MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, L)), dim3(kChunk), 0, st, route, T, E, nch, max_slots, cc, off_g, slot_row, token_to_slot,
                                                row_of_token, tok_of_row));
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+// mp_exec_map (one layer) after mp_route_top1_defer: the first kernel re-decides the
+// uncertain tokens in float64 (x: the stream the router read, w32: E x d fp32 router rows)
+// and writes the exact routes back, then counts -- no separate recheck launch.
+extern "C" int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
+                                   int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots,
+                                   int32_t* row_of_token, int32_t* tok_of_row, int32_t* piece_row,
+                                   int32_t* piece_rows, int32_t* exp_begin, const float* x, int ldx, int d,
+                                   const float* w32, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(T >= 1 && E >= 1 && max_slots >= 1 && d >= 1 && ldx >= d, MP_ERR_CONFIG,
+             "mp_exec_map_recheck: bad sizes T=%d E=%d d=%d", T, E, d);
+  MP_REQUIRE(ws_bytes >= mp_exec_workspace_bytes(1, T, E, max_slots), MP_ERR_CONFIG,
+             "mp_exec_map_recheck: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nch = cdiv(T, kChunk);
+  char* p = (char*)ws;
+  int32_t* cc = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)nch * E);
+  int32_t* dem = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)E);
+  int32_t* off_g = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)(E + 1));
+  int32_t* slot_row = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)(max_slots + 1));
+  int32_t* err = (int32_t*)p;
+  const size_t sm_h = sizeof(int) * (size_t)E;
+  const size_t sm_x = sizeof(int) * ((size_t)2 * E + 1 + 2 * ((size_t)max_slots + 1));
+  MP_REQUIRE(sm_h <= 200 * 1024 && sm_x <= 200 * 1024, MP_ERR_CONFIG, "mp_exec_map_recheck: E/max_slots too large");
+  const int pieces_stride = max_slots + nch;
+  MP_CUDA_TRY(set_smem((const void*)k_chunk_hist_recheck, sm_h));
+  MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
+  MP_CUDA_TRY(launch_pdl(k_chunk_hist_recheck, dim3(nch), dim3(kChunk), sm_h, st, route, T, E, nch, cc, x, ldx, d,
+                         w32));
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), 1)), dim3(1024), 0, st, cc, nch, E, dem));
+  MP_CUDA_TRY(launch_pdl(k_exec_layer, dim3(1), dim3(1024), sm_x, st, dem, E, max_slots, split_m, res, corrective,
+                         num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin, pieces_stride, err));
+  MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, 1)), dim3(kChunk), 0, st, (const int32_t*)route, T, E, nch,
+                         max_slots, cc, off_g, slot_row, token_to_slot, row_of_token, tok_of_row));
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -358,7 +358,7 @@ template <int EG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_router_fused_tx(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int T, int d,
                       const float* __restrict__ wabs, int E, int32_t* __restrict__ route, float eps,
-                      int32_t* __restrict__ count, int32_t* __restrict__ list) {
+                      int32_t* __restrict__ count, int32_t* __restrict__ list, int defer) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using L = RxSmem<EG>;
   extern __shared__ uint8_t smem_raw[];
@@ -563,10 +563,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) mbar_arrive(tempty);
         const int t = row_base + r;
         if (t < T) {
-          route[t] = bi;
-          if (E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r])) {
-            const int k = atomicAdd(count, 1);
-            list[k] = t;
+          const bool unsure = E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r]);
+          if (defer) {  // the consumer re-decides marked tokens (mp_exec_map_recheck)
+            route[t] = unsure ? -1 - bi : bi;
+          } else {
+            route[t] = bi;
+            if (unsure) {
+              const int k = atomicAdd(count, 1);
+              list[k] = t;
+            }
           }
         }
       }
@@ -584,7 +589,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
 template <int EG>
 static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
-                                  int32_t* route, int32_t* count, int32_t* list, float eps, cudaStream_t st) {
+                                  int32_t* route, int32_t* count, int32_t* list, float eps, cudaStream_t st,
+                                  int defer = 0) {
   CUtensorMap tb, tx;
   int rc = make_tmap_bf16(&tb, w_hl, EG, 2 * d, 2 * d, EG);
   if (rc) return rc;
@@ -598,10 +604,10 @@ static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const v
     MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+  if (!defer) MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
   const int units = cdiv(T, kBlockM);
   MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, tx, T,
-                         d, w_abs, E, route, eps, count, list));
+                         d, w_abs, E, route, eps, count, list, defer));
   return MP_OK;
 }
 
@@ -688,6 +694,22 @@ extern "C" int mp_route_top1_ex(const float* x, int ldx, int T, int d, const voi
   }
   k_router_prep<<<cdiv(T * 32, 256), 256, 0, st>>>(x, ldx, T, d, w_abs, (__nv_bfloat16*)rw.xhl, rw.xb, rw.count);
   return route_gemm(x, ldx, T, d, w_hl, w_f32, E, Eg, route, rw, kRouterEps, st);
+}
+
+// mp_route_top1_ex without the fp64 re-decision launch: uncertain tokens (top-2 gap inside
+// the certified error bound) are written as route = -1 - e_bf16; mp_exec_map_recheck
+// re-decides them in float64 inside its first kernel (same arithmetic as the recheck
+// kernel) before counting. Needs the TMA-operand router (Eg in {64, 128}, ldx % 4 == 0,
+// 16-byte aligned x).
+extern "C" int mp_route_top1_defer(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
+                                   int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream) {
+  ROUTER_CHECKS();
+  MP_REQUIRE((Eg == 64 || Eg == 128) && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, MP_ERR_CONFIG,
+             "mp_route_top1_defer: needs Eg in {64, 128}, ldx %% 4 == 0, 16-byte aligned x");
+  cudaStream_t st = (cudaStream_t)stream;
+  const RouterWs rw(ws, T, d);
+  return Eg == 128 ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st, 1)
+                   : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st, 1);
 }
 
 extern "C" int mp_route_top1(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32, int E,

@@ -226,6 +226,9 @@ class MoEPipeline:
         self.launches_per_step = None
         import os
         self.h_discard = os.environ.get("MP_H_DISCARD") is not None  # opt-in: measured no gain
+        # router without its re-decision launch; the execution map's first kernel re-decides
+        # near ties in float64 (MP_ROUTER_RECHECK_LAUNCH=1: separate recheck kernel, A/B switch)
+        self.defer_recheck = os.environ.get("MP_ROUTER_RECHECK_LAUNCH") is None
 
     # ------------------------------------------------------------------ pieces of a step
     def predict(self, x: torch.Tensor, sp: int) -> int:
@@ -315,13 +318,23 @@ class MoEPipeline:
         split = 1 if (cfg.replication == "split" or cfg.ffn == "fused" or use_mt) else 0
         if use_pair:
             split = 3
-        _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
-                  ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
-        n = 3  # fused split + GEMM (or pre-pass + GEMM), recheck
-        _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
-                  ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
-                  ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]),
-                  ptr(self.ws_exec), self.ws_exec_n, sp)
+        if self.defer_recheck and lay.Eg <= 128:
+            # near-tie tokens are re-decided in float64 inside the execution map's first kernel
+            _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w_abs), E, lay.Eg,
+                      ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
+            _lib.call("mp_exec_map_recheck", ptr(self.route[l]), T, E, self.max_slots, split, ptr(self.res[l]),
+                      ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
+                      ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
+                      ptr(self.exp_begin[l]), ptr(x), d, d, ptr(lay.w32), ptr(self.ws_exec), self.ws_exec_n, sp)
+            n = 1
+        else:
+            _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
+                      ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
+            n = 2  # router, recheck
+            _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
+                      ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
+                      ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
+                      ptr(self.exp_begin[l]), ptr(self.ws_exec), self.ws_exec_n, sp)
         if cfg.ffn == "fused":
             if ev is not None:
                 ev[0].record(sp)

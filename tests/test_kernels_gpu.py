@@ -101,6 +101,63 @@ def test_router_exact(dev):
     assert (route.long() == ref).all()
 
 
+@pytest.mark.parametrize("T,E", [(4096, 12), (1000, 100), (300, 64)])
+def test_deferred_router_recheck_in_exec_map(dev, T, E):
+    """mp_route_top1_defer + mp_exec_map_recheck == exact float64 argmax routing (lowest index on
+    ties) and the same execution map as mp_route_top1_ex + mp_exec_map, with exact ties forced
+    (every token near a tie is re-decided inside the execution map's first kernel)."""
+    d = 128
+    Eg = 64 if E <= 64 else 128
+    g = torch.Generator(device=dev).manual_seed(T + E)
+    x = torch.randn(T, d, device=dev, generator=g)
+    w = torch.randn(E, d, device=dev, generator=g)
+    w[5] = w[3]  # exact tie -> lower index
+    w[E - 1] = w[0] * (1 + 2 ** -20)  # near tie
+    w_hi = w.bfloat16()
+    w_lo = (w - w_hi.float()).bfloat16()
+    whl = torch.zeros(Eg, 2 * d, device=dev, dtype=torch.bfloat16)
+    whl[:E, :d] = w_hi
+    whl[:E, d:] = w_lo
+    wabs = torch.empty(d, device=dev)
+    _lib.call("mp_router_weight_absmax", ptr(w), E, d, ptr(wabs), stream_ptr())
+    nbytes = _lib.size_query("mp_router_workspace_bytes", T, d)
+    rws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ref = (x.double() @ w.double().T).argmax(-1)
+    i32 = dict(dtype=torch.int32, device=dev)
+    max_slots = 2 * E
+    pstride = max_slots + (T + 127) // 128
+    xn = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
+    outs = []
+    for deferred in (False, True):
+        route = torch.full((T,), -7, **i32)
+        o = dict(res=torch.zeros(E, **i32), tts=torch.empty(T, **i32), corr=torch.empty(E, **i32),
+                 ns=torch.empty(1, **i32), rot=torch.empty(T, **i32), tor=torch.empty(T, **i32),
+                 prow=torch.zeros(pstride, **i32), prows=torch.zeros(pstride, **i32), eb=torch.empty(E + 1, **i32))
+        xws = torch.empty(xn, dtype=torch.uint8, device=dev)
+        tail = (ptr(o["tts"]), ptr(o["corr"]), ptr(o["ns"]), ptr(o["rot"]), ptr(o["tor"]), ptr(o["prow"]),
+                ptr(o["prows"]), ptr(o["eb"]))
+        if deferred:
+            _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(whl), ptr(wabs), E, Eg, ptr(route), ptr(rws), nbytes,
+                      stream_ptr())
+            _lib.call("mp_exec_map_recheck", ptr(route), T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(x), d, d, ptr(w),
+                      ptr(xws), xn, stream_ptr())
+        else:
+            _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(whl), ptr(w), ptr(wabs), E, Eg, ptr(route), ptr(rws),
+                      nbytes, stream_ptr())
+            _lib.call("mp_exec_map", ptr(route), 1, T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(xws), xn,
+                      stream_ptr())
+        torch.cuda.synchronize()
+        o["route"] = route
+        outs.append(o)
+    a, b = outs
+    assert (b["route"].long() == ref).all()
+    n_pieces = int(a["eb"][-1].item())
+    for k in ("route", "res", "tts", "corr", "ns", "rot", "tor", "eb"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["prow"][:n_pieces], b["prow"][:n_pieces])
+    assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
+
+
 def test_sru_layer_matches_fp64(dev):
     T, d = 700, 128
     g = torch.Generator().manual_seed(5)
