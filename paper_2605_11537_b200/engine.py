@@ -326,11 +326,11 @@ class MoEPipeline:
                       ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
                       ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                       ptr(self.exp_begin[l]), ptr(x), d, d, ptr(lay.w32), ptr(self.ws_exec), self.ws_exec_n, sp)
-            n = 0  # router + the 3 execution-map kernels are counted below as 4
+            n = 1  # router (the 4 execution-map kernels are added below)
         else:
             _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
                       ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
-            n = 2  # router, recheck
+            n = 2  # router, recheck (the 4 execution-map kernels are added below)
             _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
                       ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
                       ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
