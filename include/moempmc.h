@@ -107,12 +107,14 @@ MP_API int mp_exec_map(const int32_t* route, int L, int T, int E, int max_slots,
                 size_t ws_bytes, void* stream);
 /* mp_exec_map for one layer after mp_route_top1_defer: re-decides the marked tokens in
  * float64 (x = the stream the router read, w32 = E x d fp32 router rows), writes the exact
- * routes back into route, then builds the same execution map as mp_exec_map. */
+ * routes back into route, then builds the same execution map as mp_exec_map. With xperm
+ * (T x d bf16, e.g. the FFN workspace base; needs ldx == d in {768, 1024}) the last kernel
+ * also writes the permuted rows xperm[row] = bf16(x[tok_of_row[row]]) of mp_ffn_gather. */
 MP_API int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
                                int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
                                int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
-                               const float* x, int ldx, int d, const float* w32, void* ws, size_t ws_bytes,
-                               void* stream);
+                               const float* x, int ldx, int d, const float* w32, void* xperm, void* ws,
+                               size_t ws_bytes, void* stream);
 
 /* Replica segments from an explicit token -> slot map (a reference Placement,
  * src/router_oracle.py:64-74, as consumed by moe_forward :160-175): rows are

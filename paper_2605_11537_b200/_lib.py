@@ -47,7 +47,8 @@ SIGNATURES: dict[str, tuple] = {
     "mp_exec_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "mp_set_sm_partition": (_I, [_I, _I]),
     "mp_exec_map": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
-    "mp_exec_map_recheck": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
+    "mp_exec_map_recheck": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _Z,
+                                 _P]),
     "mp_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
     "mp_sru_workspace_bytes": (_Z, [_I, _I]),
     "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),

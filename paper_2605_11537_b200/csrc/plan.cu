@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -648,6 +649,62 @@ __global__ void k_exec_rank(const int32_t* __restrict__ route, int T, int E, int
                  row_of_token, tok_of_row);
 }
 
+// k_exec_rank (one layer) fused with the FFN permute: block = one 128-token chunk and 32
+// warps; threads < 128 compute their token's stable rank, slot and row (k_exec_rank), then
+// all 32 warps copy the chunk's rows x[t] (fp32) -> xperm[row] (bf16, round to nearest:
+// the rows of mp_ffn_gather), four rows per warp.
+template <int KQ>  // d / 4 float4 per row
+__global__ void __launch_bounds__(1024) k_exec_rank_gather(const int32_t* __restrict__ route, int T, int E, int nch,
+                                                           int max_slots, const int32_t* __restrict__ cc,
+                                                           const int32_t* __restrict__ off_g,
+                                                           const int32_t* __restrict__ slot_row_g,
+                                                           int32_t* __restrict__ token_to_slot,
+                                                           int32_t* __restrict__ row_of_token,
+                                                           int32_t* __restrict__ tok_of_row, const float* __restrict__ x,
+                                                           __nv_bfloat16* __restrict__ xperm) {
+  griddep_launch_dependents();
+  griddep_wait();
+  __shared__ int se[kChunk], srow[kChunk];
+  const int ch = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t = ch * kChunk + tid;
+  int e = -1;
+  if (tid < kChunk) {
+    e = t < T ? __ldg(&route[t]) : -1;
+    se[tid] = e;
+  }
+  __syncthreads();
+  if (tid < kChunk) {
+    int row = -1;
+    if (t < T) {
+      int r = 0;
+      for (int j = 0; j < tid; ++j) r += (se[j] == e);
+      const int rank = cc[(size_t)ch * E + e] + r;
+      const int o = off_g[e], c = off_g[e + 1] - o;
+      const int s = o + rank % c;
+      row = slot_row_g[s] + rank / c;
+      token_to_slot[t] = s;
+      if (row_of_token) row_of_token[t] = row;
+      tok_of_row[row] = t;
+    }
+    srow[tid] = row;
+  }
+  __syncthreads();
+  constexpr int N = (KQ + 31) / 32;
+  for (int k = warp; k < kChunk; k += 32) {
+    const int row = srow[k];
+    if (row < 0) continue;
+    const float4* src = reinterpret_cast<const float4*>(x + (size_t)(ch * kChunk + k) * (KQ * 4));
+    uint2* dst = reinterpret_cast<uint2*>(xperm + (size_t)row * (KQ * 4));
+    float4 v[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (lane + 32 * i < KQ) v[i] = __ldg(&src[lane + 32 * i]);
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+      if (lane + 32 * i < KQ) dst[lane + 32 * i] = make_uint2(pack_bf16x2(v[i].x, v[i].y), pack_bf16x2(v[i].z, v[i].w));
+  }
+}
+
 // The whole execution map of mp_exec_map as ONE cooperative launch (grid (nch, L),
 // block kChunk, all blocks co-resident): chunk histograms | per-(layer, expert)
 // exclusive scans over chunks (one expert per block) | slot/piece layout (block
@@ -957,7 +1014,7 @@ extern "C" int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, 
                                    int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots,
                                    int32_t* row_of_token, int32_t* tok_of_row, int32_t* piece_row,
                                    int32_t* piece_rows, int32_t* exp_begin, const float* x, int ldx, int d,
-                                   const float* w32, void* ws, size_t ws_bytes, void* stream) {
+                                   const float* w32, void* xperm, void* ws, size_t ws_bytes, void* stream) {
   MP_REQUIRE(T >= 1 && E >= 1 && max_slots >= 1 && d >= 1 && ldx >= d, MP_ERR_CONFIG,
              "mp_exec_map_recheck: bad sizes T=%d E=%d d=%d", T, E, d);
   MP_REQUIRE(ws_bytes >= mp_exec_workspace_bytes(1, T, E, max_slots), MP_ERR_CONFIG,
@@ -985,8 +1042,15 @@ extern "C" int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, 
   MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), 1)), dim3(1024), 0, st, cc, nch, E, dem));
   MP_CUDA_TRY(launch_pdl(k_exec_layer, dim3(1), dim3(1024), sm_x, st, dem, E, max_slots, split_m, res, corrective,
                          num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin, pieces_stride, err));
-  MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, 1)), dim3(kChunk), 0, st, (const int32_t*)route, T, E, nch,
-                         max_slots, cc, off_g, slot_row, token_to_slot, row_of_token, tok_of_row));
+  if (xperm != nullptr && ldx == d && (d == 768 || d == 1024)) {  // ranks + the FFN permute in one launch
+    auto kern = d == 768 ? k_exec_rank_gather<192> : k_exec_rank_gather<256>;
+    MP_CUDA_TRY(launch_pdl(kern, dim3(nch), dim3(1024), 0, st, (const int32_t*)route, T, E, nch, max_slots, cc, off_g,
+                           slot_row, token_to_slot, row_of_token, tok_of_row, x, (__nv_bfloat16*)xperm));
+  } else {
+    MP_REQUIRE(xperm == nullptr, MP_ERR_CONFIG, "mp_exec_map_recheck: the fused permute needs ldx == d in {768, 1024}");
+    MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, 1)), dim3(kChunk), 0, st, (const int32_t*)route, T, E, nch,
+                           max_slots, cc, off_g, slot_row, token_to_slot, row_of_token, tok_of_row));
+  }
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -229,6 +229,8 @@ class MoEPipeline:
         # router without its re-decision launch; the execution map's first kernel re-decides
         # near ties in float64 (MP_ROUTER_RECHECK_LAUNCH=1: separate recheck kernel, A/B switch)
         self.defer_recheck = os.environ.get("MP_ROUTER_RECHECK_LAUNCH") is None
+        # ranks + FFN permute in one kernel (MP_RANK_GATHER_OFF=1: separate gather, A/B switch)
+        self.rank_gather = os.environ.get("MP_RANK_GATHER_OFF") is None
 
     # ------------------------------------------------------------------ pieces of a step
     def predict(self, x: torch.Tensor, sp: int) -> int:
@@ -318,6 +320,9 @@ class MoEPipeline:
         split = 1 if (cfg.replication == "split" or cfg.ffn == "fused" or use_mt) else 0
         if use_pair:
             split = 3
+        # the permute into the FFN workspace rides on the execution map's last kernel when it can
+        gather_fused = (self.defer_recheck and lay.Eg <= 128 and d in (768, 1024) and cfg.ffn != "fused"
+                        and not self.h_discard and self.rank_gather)
         if self.defer_recheck and lay.Eg <= 128:
             # near-tie tokens are re-decided in float64 inside the execution map's first kernel
             _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w_abs), E, lay.Eg,
@@ -325,7 +330,8 @@ class MoEPipeline:
             _lib.call("mp_exec_map_recheck", ptr(self.route[l]), T, E, self.max_slots, split, ptr(self.res[l]),
                       ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
                       ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
-                      ptr(self.exp_begin[l]), ptr(x), d, d, ptr(lay.w32), ptr(self.ws_exec), self.ws_exec_n, sp)
+                      ptr(self.exp_begin[l]), ptr(x), d, d, ptr(lay.w32),
+                      ptr(self.ws_ffn) if gather_fused else None, ptr(self.ws_exec), self.ws_exec_n, sp)
             n = 1  # router (the 4 execution-map kernels are added below)
         else:
             _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
@@ -345,7 +351,9 @@ class MoEPipeline:
                 ev[1].record(sp)
                 ev[2].record(sp)
             return n + 4 + 1 + 1 + 1
-        _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
+        if not gather_fused:
+            _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n,
+                      sp)
         if ev is not None:
             ev[0].record(sp)
         flags = lay.tiled | (4 if use_mt else 0) | (2 if use_pair else 0)

@@ -140,7 +140,7 @@ def test_deferred_router_recheck_in_exec_map(dev, T, E):
             _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(whl), ptr(wabs), E, Eg, ptr(route), ptr(rws), nbytes,
                       stream_ptr())
             _lib.call("mp_exec_map_recheck", ptr(route), T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(x), d, d, ptr(w),
-                      ptr(xws), xn, stream_ptr())
+                      None, ptr(xws), xn, stream_ptr())
         else:
             _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(whl), ptr(w), ptr(wabs), E, Eg, ptr(route), ptr(rws),
                       nbytes, stream_ptr())
@@ -156,6 +156,42 @@ def test_deferred_router_recheck_in_exec_map(dev, T, E):
         assert torch.equal(a[k], b[k]), k
     assert torch.equal(a["prow"][:n_pieces], b["prow"][:n_pieces])
     assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
+
+
+@pytest.mark.parametrize("T,E,d", [(16384, 128, 768), (3001, 40, 1024), (200, 8, 768)])
+def test_exec_map_recheck_permute_matches_ffn_gather(dev, T, E, d):
+    """mp_exec_map_recheck with xperm (ranks + FFN permute in one kernel) == mp_exec_map_recheck
+    without it followed by mp_ffn_gather: same maps, same permuted bf16 rows."""
+    rng = np.random.default_rng(T + E)
+    p = 1.0 / (np.arange(E) + 1.0) ** 1.2
+    route0 = torch.from_numpy(rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)).to(dev)
+    x = torch.randn(T, d, device=dev)
+    w = torch.randn(E, d, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    max_slots, F = 2 * E, 256
+    pstride = max_slots + (T + 127) // 128
+    xn = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
+    fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+    outs = []
+    for fused in (False, True):
+        route = route0.clone()
+        o = dict(res=torch.zeros(E, **i32), tts=torch.empty(T, **i32), corr=torch.empty(E, **i32),
+                 ns=torch.empty(1, **i32), rot=torch.empty(T, **i32), tor=torch.empty(T, **i32),
+                 prow=torch.zeros(pstride, **i32), prows=torch.zeros(pstride, **i32), eb=torch.empty(E + 1, **i32),
+                 fws=torch.zeros(fb, dtype=torch.uint8, device=dev))
+        xws = torch.empty(xn, dtype=torch.uint8, device=dev)
+        tail = (ptr(o["tts"]), ptr(o["corr"]), ptr(o["ns"]), ptr(o["rot"]), ptr(o["tor"]), ptr(o["prow"]),
+                ptr(o["prows"]), ptr(o["eb"]))
+        _lib.call("mp_exec_map_recheck", ptr(route), T, E, max_slots, 0, ptr(o["res"]), *tail, ptr(x), d, d, ptr(w),
+                  ptr(o["fws"]) if fused else None, ptr(xws), xn, stream_ptr())
+        if not fused:
+            _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(o["tor"]), ptr(o["fws"]), fb, stream_ptr())
+        torch.cuda.synchronize()
+        outs.append(o)
+    a, b = outs
+    for k in ("res", "tts", "corr", "ns", "rot", "tor", "eb"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["fws"][: T * d * 2], b["fws"][: T * d * 2])
 
 
 def test_sru_layer_matches_fp64(dev):
