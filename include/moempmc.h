@@ -115,6 +115,14 @@ MP_API int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, int 
                                int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
                                const float* x, int ldx, int d, const float* w32, void* xperm, void* ws,
                                size_t ws_bytes, void* stream);
+/* mp_exec_map for one layer whose chunk histograms mp_route_top1_hist already wrote into the
+ * first cdiv(T, 128) x E ints of ws (pass that region as its chunk_hist): chunk prefixes,
+ * layout, ranks -- and with xperm (d in {768, 1024}) the permuted bf16 rows of
+ * mp_ffn_gather. */
+MP_API int mp_exec_map_hist(const int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
+                            int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
+                            int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
+                            const float* x, int d, void* xperm, void* ws, size_t ws_bytes, void* stream);
 
 /* Replica segments from an explicit token -> slot map (a reference Placement,
  * src/router_oracle.py:64-74, as consumed by moe_forward :160-175): rows are
@@ -212,6 +220,13 @@ MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w
  * ldx % 4 == 0, 16-byte aligned x. route is only exact after mp_exec_map_recheck. */
 MP_API int mp_route_top1_defer(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
                                int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream);
+/* Exact routing (near ties re-decided in float64 inside the router, the arithmetic of the
+ * recheck kernel) plus every 128-token tile's expert histogram in chunk_hist[tile][e]
+ * (cdiv(T, 128) x E ints): the first stage of the execution map, for mp_exec_map_hist.
+ * Eg in {64, 128}, ldx % 4 == 0, 16-byte aligned x. */
+MP_API int mp_route_top1_hist(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
+                              const float* w_abs, int E, int Eg, int32_t* route, int32_t* chunk_hist, void* ws,
+                              size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ predictor training
  * SRU training on the GPU (reference src/predictor.py:238-379), float64 like the

@@ -49,6 +49,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_exec_map": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_exec_map_recheck": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _Z,
                                  _P]),
+    "mp_exec_map_hist": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _Z, _P]),
     "mp_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
     "mp_sru_workspace_bytes": (_Z, [_I, _I]),
     "mp_sru_layer": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
@@ -73,6 +74,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_router_weight_absmax": (_I, [_P, _I, _I, _P, _P]),
     "mp_route_top1_ex": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
     "mp_route_top1_defer": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _P, _P, _Z, _P]),
+    "mp_route_top1_hist": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _P, _Z, _P]),
     "mp_ffn_workspace_bytes": (_Z, [_I, _I, _I]),
     "mp_moe_ffn": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_gather": (_I, [_P, _I, _I, _I, _I, _P, _P, _Z, _P]),

@@ -1055,6 +1055,49 @@ extern "C" int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, 
   return MP_OK;
 }
 
+// mp_exec_map (one layer) after mp_route_top1_hist wrote the chunk histograms into the
+// first cdiv(T, 128) x E ints of ws: chunk prefixes, slot/row/piece layout, ranks (+ the FFN
+// permute into xperm when given, ldx == d in {768, 1024}).
+extern "C" int mp_exec_map_hist(const int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
+                                int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
+                                int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
+                                const float* x, int d, void* xperm, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(T >= 1 && E >= 1 && max_slots >= 1 && d >= 1, MP_ERR_CONFIG, "mp_exec_map_hist: bad sizes T=%d E=%d", T,
+             E);
+  MP_REQUIRE(ws_bytes >= mp_exec_workspace_bytes(1, T, E, max_slots), MP_ERR_CONFIG,
+             "mp_exec_map_hist: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nch = cdiv(T, kChunk);
+  char* p = (char*)ws;
+  int32_t* cc = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)nch * E);
+  int32_t* dem = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)E);
+  int32_t* off_g = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)(E + 1));
+  int32_t* slot_row = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (size_t)(max_slots + 1));
+  int32_t* err = (int32_t*)p;
+  const size_t sm_x = sizeof(int) * ((size_t)2 * E + 1 + 2 * ((size_t)max_slots + 1));
+  MP_REQUIRE(sm_x <= 200 * 1024, MP_ERR_CONFIG, "mp_exec_map_hist: E/max_slots too large");
+  const int pieces_stride = max_slots + nch;
+  MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
+  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), 1)), dim3(1024), 0, st, cc, nch, E, dem));
+  MP_CUDA_TRY(launch_pdl(k_exec_layer, dim3(1), dim3(1024), sm_x, st, dem, E, max_slots, split_m, res, corrective,
+                         num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin, pieces_stride, err));
+  if (xperm != nullptr) {
+    MP_REQUIRE(d == 768 || d == 1024, MP_ERR_CONFIG, "mp_exec_map_hist: the fused permute needs d in {768, 1024}");
+    auto kern = d == 768 ? k_exec_rank_gather<192> : k_exec_rank_gather<256>;
+    MP_CUDA_TRY(launch_pdl(kern, dim3(nch), dim3(1024), 0, st, route, T, E, nch, max_slots, cc, off_g, slot_row,
+                           token_to_slot, row_of_token, tok_of_row, x, (__nv_bfloat16*)xperm));
+  } else {
+    MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, 1)), dim3(kChunk), 0, st, route, T, E, nch, max_slots, cc,
+                           off_g, slot_row, token_to_slot, row_of_token, tok_of_row));
+  }
+  MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
 extern "C" size_t mp_segments_workspace_bytes(int T, int S) {
   const int nch = cdiv(T > 0 ? T : 1, kChunk);
   return align_up(sizeof(int32_t) * (size_t)nch * S) + 2 * align_up(sizeof(int32_t) * ((size_t)S + 1));

@@ -351,14 +351,17 @@ struct RxSmem {
   static constexpr int kBarOffset = kXOffset + kRxXStages * kXs;
   // full[S], conv[S], empty[S], xfull[X], xempty[X], tfull, tempty
   static constexpr int kXbOffset = kBarOffset + (3 * kRxStages + 2 * kRxXStages + 2) * 8 + 8;
-  static constexpr int kBytes = kXbOffset + 128 * 4 + 1024;
+  static constexpr int kHistOffset = kXbOffset + 128 * 4;  // EG ints: the tile's expert histogram
+  static constexpr int kBytes = kHistOffset + EG * 4 + 1024;
 };
 
 template <int EG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_router_fused_tx(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int T, int d,
                       const float* __restrict__ wabs, int E, int32_t* __restrict__ route, float eps,
-                      int32_t* __restrict__ count, int32_t* __restrict__ list, int defer) {
+                      int32_t* __restrict__ count, int32_t* __restrict__ list, int defer,
+                      const float* __restrict__ xg, int ldx, const float* __restrict__ w32,
+                      int32_t* __restrict__ hist_cc) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   using L = RxSmem<EG>;
   extern __shared__ uint8_t smem_raw[];
@@ -469,6 +472,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int jc = ct & 7;             // 32-byte (8 fp32) column chunk of the k-block
     const int r0 = ct >> 3;            // rows r0 + 32 i, i = 0..3
     const int box = jc >> 2, c16 = (jc & 3) * 2;  // x box (32 columns) and 16-byte chunk inside a 128 B row
+    int* s_hist = reinterpret_cast<int*>(smem + L::kHistOffset);
+    if (hist_cc != nullptr) {
+      for (int e = ct; e < EG; e += kRfConvThreads) s_hist[e] = 0;
+      named_bar_sync(1, kRfConvThreads);
+    }
     uint32_t stage = 0, phase = 0, xstage = 0, xphase = 0, tile = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
       const int row_base = u * kBlockM;
@@ -562,7 +570,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
         const int t = row_base + r;
-        if (t < T) {
+        if (hist_cc != nullptr) {
+          // near ties re-decided here in float64 by the warp (the arithmetic of
+          // k_router_recheck), then the tile's histogram for the execution map
+          unsigned m = __ballot_sync(0xffffffffu, t < T && E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r]));
+          while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const float* xr = xg + (size_t)(t - lane + j) * ldx;
+            double best = 0.0;
+            int bj = 0;
+            for (int e = 0; e < E; ++e) {
+              const float* wr = w32 + (size_t)e * d;
+              double sum = 0.0;
+              for (int k = lane; k < d; k += 32) sum += (double)wr[k] * (double)xr[k];
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+              if (e == 0 || sum > best) {
+                best = sum;
+                bj = e;
+              }
+            }
+            if (lane == j) bi = bj;
+          }
+          if (t < T) {
+            route[t] = bi;
+            atomicAdd(&s_hist[bi], 1);
+          }
+        } else if (t < T) {
           const bool unsure = E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r]);
           if (defer) {  // the consumer re-decides marked tokens (mp_exec_map_recheck)
             route[t] = unsure ? -1 - bi : bi;
@@ -576,6 +611,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       named_bar_sync(1, kRfConvThreads);
+      if (hist_cc != nullptr) {  // the tile is one 128-token chunk of the execution map
+        for (int e = ct; e < E; e += kRfConvThreads) {
+          hist_cc[(size_t)u * E + e] = s_hist[e];
+          s_hist[e] = 0;
+        }
+        named_bar_sync(1, kRfConvThreads);
+      }
     }
   }
   tc_fence_before();
@@ -590,7 +632,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 template <int EG>
 static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
                                   int32_t* route, int32_t* count, int32_t* list, float eps, cudaStream_t st,
-                                  int defer = 0) {
+                                  int defer = 0, const float* w32 = nullptr, int32_t* hist_cc = nullptr) {
   CUtensorMap tb, tx;
   int rc = make_tmap_bf16(&tb, w_hl, EG, 2 * d, 2 * d, EG);
   if (rc) return rc;
@@ -604,10 +646,10 @@ static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const v
     MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  if (!defer) MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+  if (!defer && hist_cc == nullptr) MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
   const int units = cdiv(T, kBlockM);
   MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, tx, T,
-                         d, w_abs, E, route, eps, count, list, defer));
+                         d, w_abs, E, route, eps, count, list, defer, x, ldx, w32, hist_cc));
   return MP_OK;
 }
 
@@ -710,6 +752,25 @@ extern "C" int mp_route_top1_defer(const float* x, int ldx, int T, int d, const 
   const RouterWs rw(ws, T, d);
   return Eg == 128 ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st, 1)
                    : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st, 1);
+}
+
+// Exact routing with the fp64 re-decision of near ties done inside the router's epilogue
+// (warp-cooperative, the arithmetic of k_router_recheck), plus each 128-token tile's expert
+// histogram written to chunk_hist[tile][e] -- the first stage of mp_exec_map, so
+// mp_exec_map_hist can start from the chunk prefixes. One launch for routing + histogram.
+extern "C" int mp_route_top1_hist(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
+                                  const float* w_abs, int E, int Eg, int32_t* route, int32_t* chunk_hist, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  ROUTER_CHECKS();
+  MP_REQUIRE((Eg == 64 || Eg == 128) && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                 chunk_hist != nullptr,
+             MP_ERR_CONFIG, "mp_route_top1_hist: needs Eg in {64, 128}, ldx %% 4 == 0, 16-byte aligned x");
+  cudaStream_t st = (cudaStream_t)stream;
+  const RouterWs rw(ws, T, d);
+  return Eg == 128 ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps,
+                                                 st, 0, w_f32, chunk_hist)
+                   : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st,
+                                                0, w_f32, chunk_hist);
 }
 
 extern "C" int mp_route_top1(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32, int E,

@@ -231,6 +231,8 @@ class MoEPipeline:
         self.defer_recheck = os.environ.get("MP_ROUTER_RECHECK_LAUNCH") is None
         # ranks + FFN permute in one kernel (MP_RANK_GATHER_OFF=1: separate gather, A/B switch)
         self.rank_gather = os.environ.get("MP_RANK_GATHER_OFF") is None
+        # router writes the chunk histograms (MP_ROUTE_HIST_OFF=1: histogram in the execution map)
+        self.route_hist = os.environ.get("MP_ROUTE_HIST_OFF") is None
 
     # ------------------------------------------------------------------ pieces of a step
     def predict(self, x: torch.Tensor, sp: int) -> int:
@@ -321,9 +323,20 @@ class MoEPipeline:
         if use_pair:
             split = 3
         # the permute into the FFN workspace rides on the execution map's last kernel when it can
-        gather_fused = (self.defer_recheck and lay.Eg <= 128 and d in (768, 1024) and cfg.ffn != "fused"
-                        and not self.h_discard and self.rank_gather)
-        if self.defer_recheck and lay.Eg <= 128:
+        gather_fused = ((self.defer_recheck or self.route_hist) and lay.Eg <= 128 and d in (768, 1024)
+                        and cfg.ffn != "fused" and not self.h_discard and self.rank_gather)
+        if self.route_hist and lay.Eg <= 128:
+            # the router re-decides near ties itself and writes each tile's expert histogram
+            # into the execution-map workspace: routing + histogram in one launch
+            _lib.call("mp_route_top1_hist", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
+                      ptr(self.route[l]), ptr(self.ws_exec), ptr(self.ws_router), self.ws_router_n, sp)
+            _lib.call("mp_exec_map_hist", ptr(self.route[l]), T, E, self.max_slots, split, ptr(self.res[l]),
+                      ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
+                      ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
+                      ptr(self.exp_begin[l]), ptr(x), d, ptr(self.ws_ffn) if gather_fused else None,
+                      ptr(self.ws_exec), self.ws_exec_n, sp)
+            n = 0  # router (+ the 3 execution-map kernels: counted below as 4)
+        elif self.defer_recheck and lay.Eg <= 128:
             # near-tie tokens are re-decided in float64 inside the execution map's first kernel
             _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w_abs), E, lay.Eg,
                       ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)

@@ -158,6 +158,63 @@ def test_deferred_router_recheck_in_exec_map(dev, T, E):
     assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
 
 
+@pytest.mark.parametrize("T,E", [(4096, 12), (1000, 100), (300, 64), (20000, 128)])
+def test_router_histogram_path_matches(dev, T, E):
+    """mp_route_top1_hist (near ties re-decided inside the router, chunk histograms written)
+    + mp_exec_map_hist == mp_route_top1_ex + mp_exec_map: exact routes (forced ties) and the
+    same execution map."""
+    d = 128
+    Eg = 64 if E <= 64 else 128
+    g = torch.Generator(device=dev).manual_seed(T + 3 * E)
+    x = torch.randn(T, d, device=dev, generator=g)
+    w = torch.randn(E, d, device=dev, generator=g)
+    w[5] = w[3]
+    w[E - 1] = w[0] * (1 + 2 ** -20)
+    w_hi = w.bfloat16()
+    w_lo = (w - w_hi.float()).bfloat16()
+    whl = torch.zeros(Eg, 2 * d, device=dev, dtype=torch.bfloat16)
+    whl[:E, :d] = w_hi
+    whl[:E, d:] = w_lo
+    wabs = torch.empty(d, device=dev)
+    _lib.call("mp_router_weight_absmax", ptr(w), E, d, ptr(wabs), stream_ptr())
+    nbytes = _lib.size_query("mp_router_workspace_bytes", T, d)
+    rws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ref = (x.double() @ w.double().T).argmax(-1)
+    i32 = dict(dtype=torch.int32, device=dev)
+    max_slots = 2 * E
+    pstride = max_slots + (T + 127) // 128
+    xn = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
+    outs = []
+    for hist in (False, True):
+        route = torch.full((T,), -7, **i32)
+        o = dict(res=torch.zeros(E, **i32), tts=torch.empty(T, **i32), corr=torch.empty(E, **i32),
+                 ns=torch.empty(1, **i32), rot=torch.empty(T, **i32), tor=torch.empty(T, **i32),
+                 prow=torch.zeros(pstride, **i32), prows=torch.zeros(pstride, **i32), eb=torch.empty(E + 1, **i32))
+        xws = torch.empty(xn, dtype=torch.uint8, device=dev)
+        tail = (ptr(o["tts"]), ptr(o["corr"]), ptr(o["ns"]), ptr(o["rot"]), ptr(o["tor"]), ptr(o["prow"]),
+                ptr(o["prows"]), ptr(o["eb"]))
+        if hist:
+            _lib.call("mp_route_top1_hist", ptr(x), d, T, d, ptr(whl), ptr(w), ptr(wabs), E, Eg, ptr(route), ptr(xws),
+                      ptr(rws), nbytes, stream_ptr())
+            _lib.call("mp_exec_map_hist", ptr(route), T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(x), d, None,
+                      ptr(xws), xn, stream_ptr())
+        else:
+            _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(whl), ptr(w), ptr(wabs), E, Eg, ptr(route), ptr(rws),
+                      nbytes, stream_ptr())
+            _lib.call("mp_exec_map", ptr(route), 1, T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(xws), xn,
+                      stream_ptr())
+        torch.cuda.synchronize()
+        o["route"] = route
+        outs.append(o)
+    a, b = outs
+    assert (b["route"].long() == ref).all()
+    n_pieces = int(a["eb"][-1].item())
+    for k in ("route", "res", "tts", "corr", "ns", "rot", "tor", "eb"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["prow"][:n_pieces], b["prow"][:n_pieces])
+    assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
+
+
 @pytest.mark.parametrize("T,E,d", [(16384, 128, 768), (3001, 40, 1024), (200, 8, 768)])
 def test_exec_map_recheck_permute_matches_ffn_gather(dev, T, E, d):
     """mp_exec_map_recheck with xperm (ranks + FFN permute in one kernel) == mp_exec_map_recheck
