@@ -17,7 +17,7 @@ mkdir -p "$OUT"; timeout 900 ncu --set full --import-source on --clock-control n
   -k regex:k_umma_gemm --launch-skip 11 --launch-count 2 -o "$OUT/ffn_pair" python tools/one_step.py > "$OUT/ncu_ffn.log" 2>&1
 echo "ncu ffn rc=$?"
 # memory-bound kernels of the path (north star: HBM GB/s for scan, histogram, permute, router)
-for k in k_scan_fused k_gather_rows k_chunk_hist_recheck k_router_fused k_exec_layer k_exec_rank; do
+for k in k_scan_fused k_exec_rank_gather k_router_fused k_exec_layer k_chunk_prefix_cols; do
   timeout 600 ncu --set full --import-source on --clock-control none --profile-from-start off \
     -k regex:$k --launch-count 1 -o "$OUT/ncu_$k" python tools/one_step.py > "$OUT/ncu_$k.log" 2>&1
   echo "ncu $k rc=$?"
