@@ -215,6 +215,48 @@ def test_router_histogram_path_matches(dev, T, E):
     assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
 
 
+@pytest.mark.parametrize("T,E,split_m", [(16384, 128, 1), (5000, 256, 3), (129, 7, 1), (20000, 300, 0)])
+def test_exec_map_hist_from_given_chunk_histograms(dev, T, E, split_m):
+    """mp_exec_map_hist (one-block chunk prefixes + layout) on chunk histograms placed in its
+    workspace == mp_exec_map on the routes: E above one 128-expert column group, a warm
+    residency with zeros (corrective loads), CTA-pair piece padding."""
+    rng = np.random.default_rng(T + E)
+    p = 1.0 / (np.arange(E) + 1.0) ** 1.1
+    route_h = rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)
+    res0 = rng.integers(0, 3, size=E).astype(np.int32)
+    route = torch.from_numpy(route_h).to(dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    max_slots = int(res0.sum()) + E + 1
+    pstride = max_slots + (T + 127) // 128 + E
+    xn = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
+    nch = (T + 127) // 128
+    cc = np.zeros((nch, E), dtype=np.int32)
+    np.add.at(cc, (np.arange(T) // 128, route_h), 1)
+    outs = []
+    for hist in (False, True):
+        o = dict(res=torch.from_numpy(res0.copy()).to(dev), tts=torch.empty(T, **i32), corr=torch.empty(E, **i32),
+                 ns=torch.empty(1, **i32), rot=torch.empty(T, **i32), tor=torch.empty(T, **i32),
+                 prow=torch.zeros(pstride, **i32), prows=torch.zeros(pstride, **i32), eb=torch.empty(E + 1, **i32))
+        xws = torch.zeros(xn, dtype=torch.uint8, device=dev)
+        tail = (ptr(o["tts"]), ptr(o["corr"]), ptr(o["ns"]), ptr(o["rot"]), ptr(o["tor"]), ptr(o["prow"]),
+                ptr(o["prows"]), ptr(o["eb"]))
+        if hist:
+            xws[: cc.nbytes].copy_(torch.from_numpy(cc.view(np.uint8).reshape(-1)))
+            _lib.call("mp_exec_map_hist", ptr(route), T, E, max_slots, split_m, ptr(o["res"]), *tail, None, 1, None,
+                      ptr(xws), xn, stream_ptr())
+        else:
+            _lib.call("mp_exec_map", ptr(route), 1, T, E, max_slots, split_m, ptr(o["res"]), *tail, ptr(xws), xn,
+                      stream_ptr())
+        torch.cuda.synchronize()
+        outs.append(o)
+    a, b = outs
+    n_pieces = int(a["eb"][-1].item())
+    for k in ("res", "tts", "corr", "ns", "rot", "tor", "eb"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["prow"][:n_pieces], b["prow"][:n_pieces])
+    assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
+
+
 @pytest.mark.parametrize("T,E,d", [(16384, 128, 768), (3001, 40, 1024), (200, 8, 768)])
 def test_exec_map_recheck_permute_matches_ffn_gather(dev, T, E, d):
     """mp_exec_map_recheck with xperm (ranks + FFN permute in one kernel) == mp_exec_map_recheck
