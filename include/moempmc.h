@@ -345,6 +345,8 @@ MP_API int mp_replica_copy(void* dst, const void* src, size_t bytes, void* strea
  * valid inside a captured graph (recorded as external event nodes). Host plumbing. */
 MP_API int mp_graph_begin(void* stream);
 MP_API int mp_graph_end(void* stream, void** graph_exec);
+/* As mp_graph_end; *kernel_nodes = kernel nodes in the captured graph (launches per replay). */
+MP_API int mp_graph_end_counted(void* stream, void** graph_exec, int32_t* kernel_nodes);
 MP_API int mp_graph_launch(void* graph_exec, void* stream);
 MP_API int mp_graph_destroy(void* graph_exec);
 MP_API int mp_event_create(void** ev);

@@ -97,6 +97,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_l2_persist": (_I, [_P, _Z, _F, _P]),
     "mp_graph_begin": (_I, [_P]),
     "mp_graph_end": (_I, [_P, _P]),
+    "mp_graph_end_counted": (_I, [_P, _P, _P]),
     "mp_graph_launch": (_I, [_P, _P]),
     "mp_graph_destroy": (_I, [_P]),
     "mp_event_create": (_I, [_P]),

@@ -1,5 +1,6 @@
 // C-ABI plumbing: error strings, device info, TMA map encoding, the generic
 // dense tcgen05 GEMM entry point and the replica copy.
+#include <vector>
 #include <stdarg.h>
 #include <string.h>
 
@@ -240,6 +241,30 @@ extern "C" int mp_graph_end(void* stream, void** graph_exec) {
   cudaGraphDestroy(g);
   MP_CUDA_TRY(e);
   *graph_exec = (void*)ex;
+  return MP_OK;
+}
+
+// mp_graph_end that also reports how many kernel nodes the captured graph holds (the
+// launches one replay issues; memset / memcpy / event nodes are not counted).
+extern "C" int mp_graph_end_counted(void* stream, void** graph_exec, int32_t* kernel_nodes) {
+  cudaGraph_t g = nullptr;
+  MP_CUDA_TRY(cudaStreamEndCapture((cudaStream_t)stream, &g));
+  size_t n = 0;
+  cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (e == cudaSuccess && n) e = cudaGraphGetNodes(g, nodes.data(), &n);
+  int32_t k = 0;
+  for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
+    cudaGraphNodeType t;
+    e = cudaGraphNodeGetType(nodes[i], &t);
+    k += (e == cudaSuccess && t == cudaGraphNodeTypeKernel);
+  }
+  cudaGraphExec_t ex = nullptr;
+  if (e == cudaSuccess) e = cudaGraphInstantiateWithFlags(&ex, g, 0);
+  cudaGraphDestroy(g);
+  MP_CUDA_TRY(e);
+  *graph_exec = (void*)ex;
+  if (kernel_nodes) *kernel_nodes = k;
   return MP_OK;
 }
 

@@ -27,6 +27,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import math
+import os
 from dataclasses import asdict, dataclass
 
 import torch
@@ -35,6 +36,9 @@ from . import _lib
 from ._dev import ptr, require_device, round_up, stream_ptr
 from .predictor import DeviceSru
 from .router_oracle import DeviceMoeLayer, router_eg
+
+# kernels of one SRU scan (csrc/sru.cu mp_sru_scan): single pass, or the three-kernel form
+_SCAN_KERNELS = 3 if os.environ.get("MP_SRU_3PASS") else 1
 
 DISTINCT_ONLY_UNIT = 1 << 30  # ceil(n / unit) == 1 for every demanded expert
 
@@ -250,7 +254,7 @@ class MoEPipeline:
                 h32, h16 = self.h32[i % 2], self.h16[i % 2]
                 _lib.call("mp_sru_layer", ptr(cur16), ptr(cur32), ptr(W), ptr(B), T, d, None, ptr(h32), ptr(h16), None,
                           ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
-                n += 4
+                n += 1 + _SCAN_KERNELS
                 cur32, cur16 = h32, h16
         _lib.call("mp_heads_argmax", ptr(cur16), ptr(self.sru.heads), T, d, cfg.num_layers, cfg.num_experts,
                   self.sru.Eg, ptr(self.assign), sp)
@@ -290,7 +294,7 @@ class MoEPipeline:
                           ptr(h16) + k * rows16, c_last, ptr(self.nonfinite), ptr(self.ws_sru_h[k]), self.ws_sru_h_n,
                           Bs.cuda_stream)
                 ev_s[i][k].record(Bs)
-                n += 4
+                n += 1 + _SCAN_KERNELS
         A.wait_event(ev_s[-1][1])  # join
         return n
 
@@ -498,9 +502,7 @@ class MoEPipeline:
             ex = ctypes.c_void_p()
             _lib.load_library().mp_graph_end(sp, ctypes.byref(ex))
             raise
-        ex = ctypes.c_void_p()
-        _lib.call("mp_graph_end", sp, ctypes.byref(ex))
-        return StepGraph(ex, n)
+        return _end_capture(sp, n)
 
     def capture_call(self, fn) -> "StepGraph":
         """Capture ``fn(sp) -> launches`` on the current stream into a replayable graph."""
@@ -512,9 +514,7 @@ class MoEPipeline:
             ex = ctypes.c_void_p()
             _lib.load_library().mp_graph_end(sp, ctypes.byref(ex))
             raise
-        ex = ctypes.c_void_p()
-        _lib.call("mp_graph_end", sp, ctypes.byref(ex))
-        return StepGraph(ex, n)
+        return _end_capture(sp, n)
 
     def consume(self, x: torch.Tensor, sp: int, events=None) -> int:
         """Consumer half of a step: plan + place the predicted table, then the MoE layers."""
@@ -613,6 +613,16 @@ class DeviceEvent:
                 _lib.load_library().mp_event_destroy(self.h)
         except Exception:
             pass
+
+
+def _end_capture(sp: int, issued: int) -> "StepGraph":
+    """End a capture; the graph's own kernel-node count is the launches per replay (the
+    host-side tally ``issued`` must agree -- a mismatch means a stale count)."""
+    ex, k = ctypes.c_void_p(), ctypes.c_int32(0)
+    _lib.call("mp_graph_end_counted", sp, ctypes.byref(ex), ctypes.byref(k))
+    g = StepGraph(ex, int(k.value))
+    g.issued = issued
+    return g
 
 
 class StepGraph:

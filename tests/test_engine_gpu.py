@@ -119,3 +119,28 @@ def test_engine_step_matches_cpu_oracle_moe_forward():
     derr = float(np.abs((got - e0) - (ref - e0)).max() / np.abs(ref - e0).max())
     assert err < 1e-2 and derr < 1e-2, (err, derr)
     assert (pipe.route.cpu().numpy() == chosen).mean() >= 0.999
+
+
+@pytest.mark.parametrize("replication,sru_pipeline,ffn", [("on", False, "auto"), ("off", False, "auto"),
+                                                          ("on", True, "auto"), ("on", False, "pair")])
+def test_step_graph_counts_its_kernels_and_replays_the_step(replication, sru_pipeline, ffn):
+    """The captured step graph's kernel-node count (the launches bench.py reports) equals the
+    engine's own host-side tally, and one replay gives the eager step's bits."""
+    from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig
+
+    cfg = PipelineConfig(num_layers=3, num_experts=32, d_model=256, d_ff=512, tokens=4096, sru_layers=2,
+                         capacity=64, replication=replication, sru_pipeline=sru_pipeline, ffn=ffn, seed=5)
+    pipe = MoEPipeline(cfg)
+    emb, _, _ = pipe.wl.batch(cfg.tokens)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        x_eager = emb.clone()
+        pipe.step(x_eager)
+        x = emb.clone()
+        g = pipe.capture(x)
+        x.copy_(emb)
+        g.replay()
+    torch.cuda.synchronize()
+    assert g.launches == g.issued, (g.launches, g.issued)
+    assert g.launches > 0
+    assert torch.equal(x, x_eager)
