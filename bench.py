@@ -9,9 +9,18 @@ grouped expert GEMM1 (ReLU) -> grouped GEMM2 + scatter residual combine].
   python bench.py [--gpus N --steps K --warmup W] [--replication on|off|split]
   python bench.py --impl reference ...      # CPU oracle port on the host cores
 
-Prints ONE JSON line (rank 0). Under torchrun (N > 1) every rank runs its own
-replica of the pipeline on its own batch (weak scaling, no data-path
-collective yet), timed on the device and reduced with MAX over ranks.
+Prints ONE JSON line (rank 0). Under torchrun (N > 1) the ranks run the
+expert-parallel step (paper_2605_11537_b200/ep.py): ONE model built from --seed on
+every rank, each rank its own 16k-token batch (weak scaling), token dispatch /
+combine all-to-all per MoE layer; timed on the device, MAX over ranks.
+
+Beside the headline the line carries, all measured in the same run:
+  checks     float correctness of the timed step (not vacuous): per-layer FFN delta
+             and routing of sampled tokens vs a torch fp32/fp64 recompute, SRU hidden
+             states of a 1,024-token prefix vs a float64 recompute + argmax flips
+  baselines  (ii) replication off, the M-tile "split" upper bound, (i) an HF-style
+             per-expert torch loop, a random-predictor variant -- and ratios
+  grouped_gemm_config2  BASELINE config 2 (compute-bound) GEMM TF/s vs the peaks
 """
 
 from __future__ import annotations
@@ -52,7 +61,9 @@ def parse_args():
     p.add_argument("--skew", type=float, default=1.2, help="Zipf skew of the synthetic routing")
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
     p.add_argument("--l2-persist", type=float, default=1.0, help="persisting-L2 hit ratio for the residual stream")
-    p.add_argument("--ffn", choices=["auto", "two", "mt", "fused", "pair"], default="auto")
+    p.add_argument("--ffn", choices=["auto", "two", "pair"], default="auto")
+    p.add_argument("--no-baselines", action="store_true", help="skip the same-run baseline measurements")
+    p.add_argument("--no-checks", action="store_true", help="skip the float correctness checks")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
     p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")
@@ -239,6 +250,8 @@ def run_reference(args):
         "config": config_dict(args, world),
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (pure Python moesim) cannot travel to the GPU box; this arm times the numpy port "
+                "of its chain (oracle/cpu_pipeline.py, pinned to the reference's golden vectors): port-vs-GPU",
     }
     print(json.dumps(out))
     return 0
@@ -256,20 +269,195 @@ def config_dict(args, world):
     }
 
 
+def time_graph_steps(pipe, x, batches, steps, warmup=3):
+    """Capture one step graph over ``x`` and time ``steps`` replays (CUDA events on the current
+    stream); returns ms per step. Used for the same-run baselines."""
+    import torch
+
+    for k in range(warmup):
+        x.copy_(batches[k % len(batches)][0])
+        pipe.step(x)
+    graph = pipe.capture(x)
+    for k in range(2):
+        x.copy_(batches[k % len(batches)][0])
+        graph.replay()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for k in range(steps):
+        x.copy_(batches[k % len(batches)][0])
+        graph.replay()
+    s1.record()
+    torch.cuda.synchronize()
+    del graph
+    return s0.elapsed_time(s1) / steps
+
+
+def hf_loop_ms_per_step(pipe, batches, steps):
+    """Baseline (i), SURVEY 7 / PAPER.md:99-101: the HF-Transformers-style resident-all Switch MoE
+    layer -- fp32 router matmul + argmax, then a Python loop over ALL experts: boolean-mask
+    gather of the expert's tokens, two bf16 cuBLAS matmuls (relu between), scatter back, residual
+    add. Same weights (untiled bf16 copies), same batches; no predictor (HF has none), so it
+    compares with ``moe_layers_only``. Returns ms per step (12 layers)."""
+    import torch
+
+    L, E = pipe.cfg.num_layers, pipe.cfg.num_experts
+    U = [torch.stack([pipe.expert_weights_untiled(l, e)[0] for e in range(E)]) for l in range(L)]
+    V = [torch.stack([pipe.expert_weights_untiled(l, e)[1] for e in range(E)]) for l in range(L)]
+    R = [pipe.wl.router(l) for l in range(L)]
+
+    def forward(x):
+        for l in range(L):
+            e_t = (x @ R[l].T).argmax(dim=-1)
+            h = x.to(torch.bfloat16)
+            y = torch.zeros_like(h)
+            for e in range(E):
+                m = e_t == e
+                xs = h[m]
+                y[m] = torch.relu(xs @ U[l][e].T) @ V[l][e].T
+            x = x + y.float()
+        return x
+
+    x = batches[0][0].clone()
+    forward(x)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for k in range(steps):
+        forward(batches[k % len(batches)][0])
+    s1.record()
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1) / steps
+    del U, V
+    torch.cuda.empty_cache()
+    return ms
+
+
+def float_checks(pipe, batch, n_rows=256, prefix=1024, seed=0):
+    """Correctness of the benchmarked step at its own shape (untimed; plain torch / numpy
+    recomputes, not the oracle): one eager step of ``batch`` with the residual stream of
+    ``n_rows`` sampled tokens snapshotted before every MoE layer, then
+      * every layer's delta of those rows vs relu(x U_e^T) V_e^T in fp32 (weights = the bf16
+        values the kernels read; x = the fp32 stream before the layer),
+      * their routing vs the float64 argmax of the router logits,
+      * the SRU hidden states of the first ``prefix`` tokens (causal scan from c_0 = 0) vs a
+        float64 recompute, and the predicted-expert argmax flips there."""
+    import numpy as np
+    import torch
+
+    cfg, L = pipe.cfg, pipe.cfg.num_layers
+    T = cfg.tokens
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    rows = torch.randperm(T, generator=g)[:n_rows].sort().values.cuda()
+    x = batch[0].clone()
+    snaps = pipe.step_checked(x, rows)
+    torch.cuda.synchronize()
+    worst, route_ok = 0.0, True
+    for l in range(L):
+        xin, xout = snaps[l], snaps[l + 1]
+        e_t = pipe.route[l][rows].long()
+        logits = xin.double() @ pipe.wl.router(l).double().T
+        route_ok &= bool((logits.argmax(dim=-1) == e_t).all().item())
+        ref = torch.empty_like(xin)
+        for e in e_t.unique().tolist():
+            m = e_t == e
+            u, v = pipe.expert_weights_untiled(l, e)
+            ref[m] = torch.relu(xin[m] @ u.float().T) @ v.float().T
+        got = xout - xin
+        worst = max(worst, float((got - ref).abs().max() / ref.abs().max()))
+    # SRU prefix in float64: projections on the GPU, the recurrence in numpy
+    h = batch[0][:prefix].double()
+    for w, wf, wr, bf, br in pipe.sru_host:
+        W, Wf, Wr = (torch.from_numpy(a).cuda() for a in (w, wf, wr))
+        u = (h @ W.T).cpu().numpy()
+        f = torch.sigmoid((h @ Wf.T + torch.from_numpy(bf).cuda()).clamp(-60, 60)).cpu().numpy()
+        r = torch.sigmoid((h @ Wr.T + torch.from_numpy(br).cuda()).clamp(-60, 60)).cpu().numpy()
+        c = np.zeros(u.shape[1])
+        cs = np.empty_like(u)
+        gu = (1.0 - f) * u
+        for t in range(u.shape[0]):
+            c = f[t] * c + gu[t]
+            cs[t] = c
+        h = torch.from_numpy(r * np.tanh(cs) + (1.0 - r) * h.cpu().numpy()).cuda()
+    got_h = pipe.h32[(cfg.sru_layers - 1) % 2][:prefix].double()
+    sru_rel = float((got_h - h).abs().max() / h.abs().max())
+    heads = torch.from_numpy(pipe.heads_host).cuda()
+    ref_assign = torch.stack([(h @ heads[l].T).argmax(dim=-1) for l in range(L)])
+    flips = int((pipe.assign[:, :prefix].long() != ref_assign).sum().item())
+    return {
+        "ffn_maxnorm_rel": worst, "ffn_rows_per_layer": n_rows, "routing_exact_sampled": route_ok,
+        "sru_maxnorm_rel": sru_rel, "sru_prefix_tokens": prefix, "predictor_argmax_flips": flips,
+        "predictor_argmax_total": int(ref_assign.numel()), "tolerance": 1e-2,
+        "how": "one eager step of the last timed batch; torch fp32 FFN / fp64 router and SRU recomputes",
+    }
+
+
+def config2_gemm(args, peaks):
+    """BASELINE config 2: one Switch-base-8-shape layer (E = 8, d = 768, F = 3072, 16,384 tokens,
+    2,048 per expert, C = 148) -- the compute-bound grouped GEMM (--ffn auto takes the CTA-pair
+    kernels). GEMM1 + GEMM2 launch durations from events inside a replayed step graph."""
+    import dataclasses
+
+    import torch
+
+    from paper_2605_11537_b200.engine import DeviceEvent, MoEPipeline, PipelineConfig
+
+    cfg = PipelineConfig(num_layers=1, num_experts=8, tokens=16384, capacity=148, demand_unit=args.demand_unit,
+                         sru_layers=10, seed=args.seed)
+    pipe = MoEPipeline(cfg)
+    batches = [pipe.wl.batch(cfg.tokens) for _ in range(2)]
+    x = torch.empty(cfg.tokens, cfg.d_model, device="cuda")
+    for k in range(3):
+        x.copy_(batches[k % 2][0])
+        pipe.step(x)
+    ev = [[DeviceEvent() for _ in range(3)]]
+    g = pipe.capture(x, ev)
+    t1, t2 = [], []
+    for k in range(10):
+        x.copy_(batches[k % 2][0])
+        g.replay()
+        torch.cuda.synchronize()
+        if k >= 2:
+            t1.append(ev[0][0].elapsed_ms(ev[0][1]))
+            t2.append(ev[0][1].elapsed_ms(ev[0][2]))
+    ms1, ms2 = sorted(t1)[len(t1) // 2], sorted(t2)[len(t2) // 2]
+    flops = 4.0 * cfg.tokens * cfg.d_model * cfg.d_ff
+    tf = flops / ((ms1 + ms2) * 1e-3) / 1e12
+    out = {"tflops": tf, "frac_of_burst_peak": tf / peaks["bf16_tflops"],
+           "frac_of_sustained_peak": tf / peaks["bf16_tflops_sustained"], "ms_gemm1": ms1, "ms_gemm2": ms2,
+           "tokens_per_expert": cfg.tokens // cfg.num_experts, "ffn_kernels": pipe.cfg.ffn,
+           "how": "median of 8 instrumented step-graph replays (events around GEMM1 / GEMM2)"}
+    prof = ROOT / "profiles" / "config2_tensor_pipe.json"
+    if prof.exists():
+        try:
+            out["tensor_pipe_pct_ncu"] = json.loads(prof.read_text())
+            out["tensor_pipe_source"] = "profiles/config2_tensor_pipe.json (ncu --set full, not this run)"
+        except Exception:
+            pass
+    del pipe, g
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
+    import dataclasses
+
     import torch
 
     world, rank, local = dist_setup()
     from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig
 
+    # ONE model on every rank (weights, routers, predictor from --seed); per-rank batches
     cfg = PipelineConfig(num_layers=args.layers, num_experts=args.experts, tokens=args.tokens,
                          capacity=args.capacity, demand_unit=args.demand_unit, replication=args.replication,
-                         predictor=args.predictor, ffn=args.ffn, seed=args.seed + rank, skew=args.skew)
+                         predictor=args.predictor, ffn=args.ffn, seed=args.seed, skew=args.skew,
+                         batch_seed=1_000_003 * (rank + 1) + args.seed)
     pipe = MoEPipeline(cfg)
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
     ep = world > 1 or args.ep
     if ep:
         pipe.enable_expert_parallel()
+    weights_same = weights_hash_equal(pipe, world)
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]
     x = torch.empty(T, d, device="cuda")
 
@@ -345,7 +533,7 @@ def run_ours(args):
     up = [ev[l][0].elapsed_ms(ev[l][1]) for l in range(L)]
     down = [ev[l][1].elapsed_ms(ev[l][2]) for l in range(L)]
 
-    # correctness spot checks on the last step (not timed)
+    # exact routing / predictor accuracy of the last step (not timed)
     last = batches[(args.steps - 1) % len(batches)]
     routing_exact = bool((pipe.route.long() == last[2]).all().item()) if not ep else \
         bool((pipe.ep.last_route.long() == last[2][-1]).all().item())
@@ -355,19 +543,22 @@ def run_ours(args):
     t_up, t_down = sum(up) / len(up), sum(down) / len(down)
     touched = pipe.touched_experts().float().mean().item()
     w_bytes = touched * pipe.expert_weight_bytes()
-    # algorithmic bytes of one MoE layer's FFN: every touched expert's U and V once (bf16)
-    # plus the token activations it must move: gather (read fp32 x, write bf16 rows), GEMM1
-    # reads the bf16 rows, the combine reads and writes fp32 x. The hidden H is an
-    # intermediate (kept in an L2 ring by the fused kernel) and is not counted.
-    alg_bytes = w_bytes + T * (4 * d + 2 * d + 2 * d + 8 * d)
+    # algorithmic bytes of what the [GEMM1 start, GEMM2 end] bracket does per MoE layer: every
+    # touched expert's U and V once (bf16), GEMM1 reads the permuted bf16 rows (2d B/token; the
+    # permute itself runs in the execution map's rank kernel, before the bracket), GEMM2's
+    # combine reads and writes the fp32 stream (8d B/token). The hidden H (T x F bf16) is an
+    # intermediate written by GEMM1 and re-read by GEMM2 -- not algorithmic; its cost shows in
+    # the measured DRAM traffic.
+    alg_bytes = w_bytes + T * (2 * d + 8 * d)
     flops = 4.0 * T * d * cfg.d_ff
     peaks, peak_kind = load_peaks()
     achieved = alg_bytes / ((t_up + t_down) * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / "ffn_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("traffic_bytes_per_layer")
+            pj = json.loads(prof.read_text())
+            traffic, traffic_src = pj.get("traffic_bytes_per_layer"), "profiles/ffn_traffic.json: " + pj.get("source", "")
         except Exception:
             traffic = None
 
@@ -392,6 +583,7 @@ def run_ours(args):
                     "how": "step time minus a separately captured and timed predictor + plan/place graph"}
 
     value = world * T * args.steps / (elapsed_ms * 1e-3)
+    ms_step = elapsed_ms / args.steps
     result = {
         "metric": METRIC,
         "value": value,
@@ -399,7 +591,7 @@ def run_ours(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": elapsed_ms / args.steps,
+        "ms_per_step": ms_step,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -409,35 +601,44 @@ def run_ours(args):
         "clocks": clk,
         "gpu_launches": launches,
         "roofline": {
-            "kernel": ("fused grouped expert FFN (k_ffn_fused: GEMM1 relu + GEMM2 scatter-combine, H in L2 ring)"
-                       if pipe.cfg.ffn == "fused" else
-                       "grouped expert GEMM pair (GEMM1 relu + GEMM2 scatter-combine"
-                       + (", multi-tile units k_ffn_mt)" if pipe.cfg.ffn == "mt" and args.replication != "off" else
-                          ", CTA-pair cta_group::2 kernels)" if pipe.cfg.ffn == "pair" else ")")),
+            "kernel": "grouped expert GEMM pair (GEMM1 relu + GEMM2 scatter-combine"
+                      + (", CTA-pair cta_group::2 kernels)" if pipe.cfg.ffn == "pair" else ")"),
             "bound": "hbm",
             "achieved": achieved,
             "peak": peaks["hbm_gbs"],
             "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"],
             "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": peak_kind,
             "algorithmic_bytes_per_layer": alg_bytes,
+            "algorithmic_bytes_formula": "touched_experts * 4*d*F (bf16 U, V) + T * (2d + 8d) (GEMM1 reads the "
+                                         "bf16 rows; GEMM2 reads + writes the fp32 stream)",
             "touched_experts_per_layer": touched,
             "ms_gemm1": t_up,
             "ms_gemm2": t_down,
+            "timing": "per-layer CUDA events around GEMM1 / GEMM2 inside an instrumented replay of the step graph "
+                      "(mean over the layers of the last replay)",
             "tensor_tflops": flops / ((t_up + t_down) * 1e-3) / 1e12,
             "tensor_frac": flops / ((t_up + t_down) * 1e-3) / 1e12 / peaks["bf16_tflops_sustained"],
         },
-        "checks": {"routing_exact_last_step": routing_exact, "predictor_accuracy_last_step": pred_acc},
+        "checks": {"routing_exact_last_step": routing_exact, "predictor_accuracy_last_step": pred_acc,
+                   "weights_identical_on_all_ranks": weights_same},
         "moe_layers_only": moe_only,
         "cuda_graph": graph is not None or overlap is not None,
         "overlap": overlap is not None,
     }
 
     result["config"]["ffn_kernels"] = pipe.cfg.ffn  # resolved from --ffn auto
+    if not args.no_checks and not ep:
+        result["checks"].update(float_checks(pipe, last, seed=args.seed))
     if not args.no_e2e:
         pipe._bench_x, pipe._bench_graph = x, graph
         result["e2e"] = run_e2e(args, pipe, batches, world)
+    if not args.no_baselines and not ep and graph is not None:
+        del graph, graph_ev
+        result["baselines"] = run_baselines(args, pipe, x, batches, ms_step, moe_only)
+        result["grouped_gemm_config2"] = config2_gemm(args, peaks)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args)
         result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -448,6 +649,76 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def weights_hash_equal(pipe, world):
+    """Every rank must hold the same model (one --seed): float64 sums of every layer's router and
+    first/last expert weights and of the predictor, all-gathered and compared."""
+    import torch
+
+    parts = []
+    for l in (0, pipe.cfg.num_layers - 1):
+        lay = pipe.layers[l]
+        parts += [lay.w32.double().sum(), lay.U[:4096].double().sum(), lay.V[-4096:].double().sum()]
+    parts.append(pipe.sru.heads.double().sum())
+    h = torch.stack(parts)
+    if world == 1:
+        return True
+    import torch.distributed as dist
+
+    hs = [torch.empty_like(h) for _ in range(world)]
+    dist.all_gather(hs, h)
+    return all(bool(torch.equal(hs[0], o)) for o in hs[1:])
+
+
+def run_baselines(args, pipe, x, batches, ms_on, moe_only):
+    """SURVEY 7 baselines on the same model, batches and box, right after the headline:
+      (ii) replication off  -- distinct-only caps, one serial unit per expert (the paper's
+                               non-replicated GPU baseline on the same kernels)
+      split                 -- every 128-row tile its own unit (upper bound of the plan)
+      (i)  HF-style loop    -- per-expert torch loop over all experts
+      random predictor      -- random heads: the plan forecasts nothing, corrective replicas
+    ratios are headline / baseline (tokens/s)."""
+    import dataclasses
+
+    import torch
+
+    T = pipe.cfg.tokens
+    steps = max(5, min(args.steps, 20))
+    base_cfg = pipe.cfg
+    out = {"steps_each": steps}
+    for name, change in (("replication_off", dict(replication="off")), ("split", dict(replication="split"))):
+        pipe.cfg = dataclasses.replace(base_cfg, **change)
+        pipe.res.zero_()
+        ms = time_graph_steps(pipe, x, batches, steps)
+        out[name] = {"value": T / (ms * 1e-3), "ms_per_step": ms, "speedup_of_headline": ms / ms_on}
+    pipe.cfg = base_cfg
+    # random predictor: the same SRU, random heads
+    heads_keep = pipe.sru.heads.clone()
+    g = torch.Generator(device="cuda").manual_seed(args.seed + 99)
+    pipe.sru.heads.copy_(((torch.rand(heads_keep.shape, device="cuda", generator=g) * 2 - 1)
+                          / pipe.cfg.d_model ** 0.5).to(heads_keep.dtype))
+    pipe.res.zero_()
+    ms = time_graph_steps(pipe, x, batches, steps)
+    acc = float((pipe.assign.long() == batches[(steps - 1) % len(batches)][2]).float().mean().item())
+    out["random_predictor"] = {"value": T / (ms * 1e-3), "ms_per_step": ms, "predictor_accuracy": acc,
+                               "corrective_replicas_last_step": int(pipe.corrective.sum().item()),
+                               "headline_over_this": ms / ms_on}
+    pipe.sru.heads.copy_(heads_keep)
+    pipe.res.zero_()
+    ms_hf = hf_loop_ms_per_step(pipe, batches, 3)
+    out["hf_loop"] = {"value": T / (ms_hf * 1e-3), "ms_per_step": ms_hf, "steps": 3,
+                      "what": "MoE layers only (router + per-expert mask/gather/2 matmuls/scatter, bf16 cuBLAS)"}
+    if moe_only is not None:
+        ms_off_moe = out["replication_off"]["ms_per_step"] - moe_only["ms_predictor_and_plan"]
+        out["ratios_moe_layers_only"] = {
+            "on_over_off": ms_off_moe / moe_only["ms_per_step"],
+            "on_over_hf_loop": ms_hf / moe_only["ms_per_step"],
+            "how": "MoE-layer time = step time minus the predictor + plan graph (same for on and off)"}
+    out["ratios_whole_step"] = {"on_over_off": out["replication_off"]["ms_per_step"] / ms_on,
+                                "on_over_hf_loop_moe": ms_hf / ms_on,
+                                "target": ">= 3x the non-replicated GPU baseline (north star)"}
+    return out
 
 
 def run_e2e(args, pipe, batches, world):
@@ -509,8 +780,9 @@ def run_e2e(args, pipe, batches, world):
     return {"value": world * T * args.steps / (ms * 1e-3), "unit": "tokens/s",
             "h2d_bytes_per_step": T * d * 4, "d2h_bytes_per_step": T * d * 4,
             "ms_per_step": ms / args.steps,
-            "api": "MoEPipeline.step over pinned host batches (H2D/D2H double-buffered through device staging "
-                   "buffers on copy streams)"}
+            "api": "MoEPipeline step graph (MoEPipeline.capture, replayed) over pinned host batches: H2D of the "
+                   "embeddings and D2H of the output stream every step, double-buffered through device staging "
+                   "buffers on copy streams"}
 
 
 def main():

@@ -105,16 +105,6 @@ MP_API int mp_exec_map(const int32_t* route, int L, int T, int E, int max_slots,
                 int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
                 int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin, void* ws,
                 size_t ws_bytes, void* stream);
-/* mp_exec_map for one layer after mp_route_top1_defer: re-decides the marked tokens in
- * float64 (x = the stream the router read, w32 = E x d fp32 router rows), writes the exact
- * routes back into route, then builds the same execution map as mp_exec_map. With xperm
- * (T x d bf16, e.g. the FFN workspace base; needs ldx == d in {768, 1024}) the last kernel
- * also writes the permuted rows xperm[row] = bf16(x[tok_of_row[row]]) of mp_ffn_gather. */
-MP_API int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
-                               int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots, int32_t* row_of_token,
-                               int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
-                               const float* x, int ldx, int d, const float* w32, void* xperm, void* ws,
-                               size_t ws_bytes, void* stream);
 /* mp_exec_map for one layer whose chunk histograms mp_route_top1_hist already wrote into the
  * first cdiv(T, 128) x E ints of ws (pass that region as its chunk_hist): chunk prefixes,
  * layout, ranks -- and with xperm (d in {768, 1024}) the permuted bf16 rows of
@@ -214,12 +204,6 @@ MP_API int mp_router_weight_absmax(const float* w_f32, int E, int d, float* w_ab
 MP_API int mp_route_top1_ex(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32,
                             const float* w_abs, int E, int Eg, int32_t* route, void* ws, size_t ws_bytes,
                             void* stream);
-/* mp_route_top1_ex without its fp64 re-decision launch: tokens whose top-2 gap is inside the
- * certified bound are written as route = -1 - e (the bf16 guess); mp_exec_map_recheck
- * re-decides them in float64 (the same arithmetic) before counting. Eg in {64, 128},
- * ldx % 4 == 0, 16-byte aligned x. route is only exact after mp_exec_map_recheck. */
-MP_API int mp_route_top1_defer(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
-                               int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream);
 /* Exact routing (near ties re-decided in float64 inside the router, the arithmetic of the
  * recheck kernel) plus every 128-token tile's expert histogram in chunk_hist[tile][e]
  * (cdiv(T, 128) x E ints): the first stage of the execution map, for mp_exec_map_hist.
@@ -269,20 +253,14 @@ MP_API int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, co
                       const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 /* The same layer as three launches (gather | GEMM1 | GEMM2) sharing `ws`, for callers that
  * time or overlap the grouped GEMMs separately. flags bit 0: u / v are in the pre-tiled
- * layout of mp_tile_kmajor (BN mp_ffn_up_bn(Fp) for u; mp_ffn_down_bn(dp) for v, or 256 for
- * v with bits 1 / 2 / 3); bit 1: CTA-pair
- * (tcgen05 cta_group::2, M = 256) kernels over piece pairs -- pieces must come from a
- * builder called with split_m bit 1 (even piece count per expert), dp % 256 == 0;
- * bit 2: multi-tile units (two 128 x 256 accumulator tiles per unit: two pieces of one
- * expert share each weight k-block, or one piece feeds two weight slices) -- pieces of
- * <= 128 rows (split_m bit 0), Fp % 256 == 0 (up) / dp % 256 == 0 (down), E <= 1024;
- * bit 3: clusters of 2-4 CTAs computing consecutive weight slices of one piece, the A
- * tile loaded once and multicast to the cluster (slice count divisible by 2, 3 or 4).
- * bit 4 (mp_ffn_down, after mp_ffn_gather with the same ws): once the last slice unit of
- * a piece has consumed its hidden rows, GEMM2 drops them from L2 (discard.global.L2, no
- * write-back of dead data). Every mode gives bitwise identical results.
- * bit 5 (mp_ffn_down): store y[tok_of_row[row]] = result instead of adding it (every target
- *   row has exactly one writer; the expert-parallel receive buffer then needs no zeroing).
+ * layout of mp_tile_kmajor (BN mp_ffn_up_bn(Fp) for u; mp_ffn_down_bn(dp) for v, or 256 with
+ * bit 1 or bit 6); bit 1: CTA-pair (tcgen05 cta_group::2, M = 256) kernels over piece pairs --
+ * pieces must come from a builder called with split_m bit 1 (even piece count per expert),
+ * dp % 256 == 0; bit 5 (mp_ffn_down): store y[tok_of_row[row]] = result instead of adding it
+ * (every target row has exactly one writer; the expert-parallel receive buffer then needs
+ * no zeroing); bit 6 (mp_ffn_down, single-CTA kernel): v is tiled with 256-column slices
+ * (the CTA-pair layout), so the same weights serve both kernels. Every mode gives bitwise
+ * identical results.
  */
 MP_API int mp_ffn_gather(const float* x, int T, int dp, int Fp, int E, const int32_t* tok_of_row, void* ws,
                          size_t ws_bytes, void* stream);
@@ -297,16 +275,6 @@ MP_API int mp_ffn_up_bn(int Fp);
 /* Diagnostics: per-CTA %globaltimer start / end (ns) of the last grouped-GEMM launch
  * (host arrays of n <= 1024). */
 MP_API int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1, int n);
-/* One MoE layer's FFN as ONE persistent launch (after a gather): GEMM1 and GEMM2 units
- * of every piece interleaved, the hidden activations living in an L2-resident ring of
- * 128-row slots (never a T x F HBM buffer), device-side completion counters ordering
- * GEMM2 after GEMM1 and slot reuse after GEMM2. Needs pre-tiled weights (BN 256 for both),
- * pieces of <= 128 rows (split_m bit 0), dp % 256 == 0, Fp % 256 == 0; x updated in place.
- * max_pieces >= the piece-array capacity used by the builder. */
-MP_API size_t mp_ffn_fused_workspace_bytes(int T, int dp, int Fp, int max_pieces);
-MP_API int mp_ffn_fused(float* x, int T, int dp, int Fp, int E, const void* u_tiled, const void* v_tiled,
-                        const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
-                        const int32_t* exp_begin, int max_pieces, void* ws, size_t ws_bytes, void* stream);
 /* Weight layout transform for the grouped GEMM B operand:
  * dst[g][n / BN][k / 64][n % BN][k % 64] = src[g * N + n][k]   (bf16, G groups of N x K). */
 MP_API int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int BN, void* stream);

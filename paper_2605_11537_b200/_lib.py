@@ -47,8 +47,6 @@ SIGNATURES: dict[str, tuple] = {
     "mp_exec_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "mp_set_sm_partition": (_I, [_I, _I]),
     "mp_exec_map": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
-    "mp_exec_map_recheck": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _Z,
-                                 _P]),
     "mp_exec_map_hist": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _P, _P, _Z, _P]),
     "mp_gemm_bf16": (_I, [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P]),
     "mp_sru_workspace_bytes": (_Z, [_I, _I]),
@@ -73,7 +71,6 @@ SIGNATURES: dict[str, tuple] = {
     "mp_route_top1": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _F, _P, _P, _Z, _P]),
     "mp_router_weight_absmax": (_I, [_P, _I, _I, _P, _P]),
     "mp_route_top1_ex": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _Z, _P]),
-    "mp_route_top1_defer": (_I, [_P, _I, _I, _I, _P, _P, _I, _I, _P, _P, _Z, _P]),
     "mp_route_top1_hist": (_I, [_P, _I, _I, _I, _P, _P, _P, _I, _I, _P, _P, _P, _Z, _P]),
     "mp_ffn_workspace_bytes": (_Z, [_I, _I, _I]),
     "mp_moe_ffn": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
@@ -83,8 +80,6 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_down_bn": (_I, [_I]),
     "mp_ffn_up_bn": (_I, [_I]),
     "mp_debug_cta_times": (_I, [_P, _P, _I]),
-    "mp_ffn_fused_workspace_bytes": (_Z, [_I, _I, _I, _I]),
-    "mp_ffn_fused": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _Z, _P]),
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
     "mp_ep_workspace_bytes": (_Z, [_I, _I, _I, _I]),

@@ -66,11 +66,6 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-bool pdl_enabled() {  // opt-in: measured 5.51 vs 5.34 ms/step with PDL edges in the step graph
-  static const bool on = getenv("MP_PDL") != nullptr;
-  return on;
-}
-
 int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
                    uint32_t box_rows) {
   auto enc = get_encode();
@@ -147,26 +142,7 @@ int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_
   const int units = cdiv(M, kBlockM) * (N / bn);
   const int cap = grid_cap > 0 ? std::min(grid_cap, num_sms()) : num_sms();
   const int grid = units < cap ? units : cap;
-  static const bool pair = getenv("MP_GEMM_PAIR") != nullptr;  // experiment switch: CTA-pair kernel
-  if (pair && bn == 256 && c_dtype == 0 && M >= 256) {
-    CUtensorMap tb2;
-    rc = make_tmap_bf16(&tb2, B, N, K, K, bn / 2);
-    if (rc) return rc;
-    Dense2Sched s2{M, N / bn, K / 64, bn};
-    const int cu = cdiv(M, 2 * kBlockM) * (N / bn);
-    const int g2 = std::min(2 * cu, cap) & ~1;
-    if (ldc > 0 && getenv("MP_STG_EPILOGUE") == nullptr) {  // TMA bulk-store epilogue
-      CUtensorMap tc;
-      rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
-      if (rc) return rc;
-      EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from, store_hint};
-      return launch_gemm2<256, 6>(ta, tb2, s2, et, g2, st, &tc);
-    }
-    EpiStoreBf16 e{(__nv_bfloat16*)C, ldc, bias, act, sig_from};
-    return launch_gemm2<256, 6>(ta, tb2, s2, e, g2, st);
-  }
-  static const bool tma_store = getenv("MP_STG_EPILOGUE") == nullptr;  // A/B switch: st.global epilogue
-  if (c_dtype == 0 && tma_store && bn == 256 && ldc > 0) {  // bf16 tile through TMA bulk stores
+  if (c_dtype == 0 && bn == 256 && ldc > 0) {  // bf16 tile through TMA bulk stores
     CUtensorMap tc;
     rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
     if (rc) return rc;

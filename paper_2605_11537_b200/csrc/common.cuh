@@ -112,12 +112,10 @@ struct RouterWs {
   }
 };
 
-// Kernel launch with programmatic stream serialization (PDL) allowed: inside a CUDA
-// graph this becomes a programmatic edge, so the kernel's launch and prologue overlap
-// the previous kernel's tail; every kernel calls griddep_wait() before touching data
-// a predecessor produced. Opt-in with MP_PDL=1: in the whole-step CUDA graph the
-// programmatic edges measured slower (5.51 vs 5.34 ms/step), so plain edges are default.
-bool pdl_enabled();
+// Kernel launch through cudaLaunchKernelEx. Kernels still bracket their dependent reads
+// with griddep_wait() so programmatic edges could be enabled per launch; in the whole-step
+// CUDA graph programmatic edges measured slower (5.51 vs 5.34 ms/step, round 1), so none
+// are requested.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -126,11 +124,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -221,12 +221,6 @@ struct EpiScatterAdd {
   float* x;  // T x ldx fp32 residual stream (updated in place)
   int ldx;
   const int32_t* tok_of_row;
-  // optional: drop the A rows (GEMM1's hidden activations) from L2 once all n_slices
-  // units of a piece have consumed them -- dead data that would otherwise be written back
-  int32_t* done;              // per first-row counters (zeroed by the gather), or null
-  const __nv_bfloat16* hid;   // A operand (rows x ldh)
-  int ldh;
-  int n_slices;
   int store = 0;              // 1: plain stores (x[tok] = y) -- every target row has exactly one
                               //    writer (the expert-parallel receive buffer needs no zeroing)
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
@@ -269,17 +263,6 @@ struct EpiScatterAdd {
         __syncwarp();
       }
     });
-    if (done != nullptr && mt == (U.rows - 1) / kBlockM) {  // last M tile of the unit
-      __shared__ int last;
-      named_bar_sync(3, 32 * kEpiWarps);  // every epilogue warp is past this unit's MMA results
-      if (threadIdx.x == 128) last = atomicAdd(&done[U.a_row], 1) == n_slices - 1;
-      named_bar_sync(3, 32 * kEpiWarps);
-      if (last) {
-        const char* p0 = reinterpret_cast<const char*>(hid + (size_t)U.a_row * ldh);
-        const size_t nl = (size_t)U.rows * ldh * 2 / 128;
-        for (size_t i = threadIdx.x - 128; i < nl; i += 32 * kEpiWarps) l2_discard(p0 + i * 128);
-      }
-    }
   }
 };
 

@@ -16,7 +16,6 @@
 // built deterministically (no atomics decide order): per-128-token chunk
 // counts -> per-expert exclusive scan over chunks -> in-chunk rank by a
 // shared-memory broadcast compare.
-#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -24,7 +23,6 @@
 #include "common.cuh"
 #include "ptx.cuh"
 
-namespace cg = cooperative_groups;
 
 namespace mp {
 
@@ -48,49 +46,6 @@ __global__ void k_chunk_hist(const int32_t* __restrict__ assign, int T, int E, i
   for (int e = threadIdx.x; e < E; e += blockDim.x) out[e] = hist[e];
 }
 
-// k_chunk_hist for one layer whose routing came from mp_route_top1_defer: tokens marked
-// uncertain (route < 0) are first re-decided in float64 by their warp -- the arithmetic of
-// k_router_recheck (lane-strided partial sums, xor-shuffle reduction, first maximum), so the
-// routes equal mp_route_top1_ex's -- and written back.
-__global__ void k_chunk_hist_recheck(int32_t* __restrict__ route, int T, int E, int nch, int32_t* __restrict__ cc,
-                                     const float* __restrict__ x, int ldx, int d, const float* __restrict__ w) {
-  griddep_launch_dependents();
-  griddep_wait();
-  extern __shared__ int hist[];
-  const int ch = blockIdx.x, lane = threadIdx.x & 31;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
-  __syncthreads();
-  const int t = ch * kChunk + threadIdx.x;
-  int e = t < T ? route[t] : 0;
-  unsigned m = __ballot_sync(0xffffffffu, t < T && e < 0);
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    const int tj = t - lane + j;
-    const float* xr = x + (size_t)tj * ldx;
-    double best = 0.0;
-    int bi = 0;
-    for (int ee = 0; ee < E; ++ee) {
-      const float* wr = w + (size_t)ee * d;
-      double s = 0.0;
-      for (int k = lane; k < d; k += 32) s += (double)wr[k] * (double)xr[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (ee == 0 || s > best) {
-        best = s;
-        bi = ee;
-      }
-    }
-    if (lane == j) {
-      e = bi;
-      route[t] = bi;
-    }
-  }
-  if (t < T) atomicAdd(&hist[e], 1);
-  __syncthreads();
-  int32_t* out = cc + (size_t)ch * E;
-  for (int k = threadIdx.x; k < E; k += blockDim.x) out[k] = hist[k];
-}
 
 // In place: cc[l][ch][e] <- sum_{ch' < ch} cc[l][ch'][e]; demand[l][e] <- total. Grid
 // (ceil(E / 32), L), block 32 x 32 = (expert lane, chunk group); each thread scans
@@ -522,104 +477,6 @@ __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_
 }
 
 
-// The execution map of one layer as ONE launch (default for L == 1, E <= 256,
-// T <= 32 x 1024): grid = T / 1024 blocks of 1024 tokens.
-//   A. every block: in-block stable ranks (warp match_any + per-warp expert counts
-//      scanned over the 32 warps), its expert histogram -> bh[b][e], and a copy of the
-//      old residency; then one arrival on a grid counter.
-//   B. every block, once all have arrived: all block histograms -> its own prefix and
-//      the demand; the slot / row / piece layout of exec_layer_core in shared memory
-//      (block 0 alone writes the global outputs: residency, pieces, offsets).
-//   C. every block: rank = prefix[e] + in-block rank -> slot, row, tok_of_row from the
-//      shared-memory layout.
-// Blocks only wait for every block to finish phase A; all are co-resident
-// (T / 1024 <= 32 <= the SM count). Same stable ranks (token order within an expert) and
-// the same layout arithmetic as k_chunk_hist .. k_exec_rank.
-constexpr int kXoTokens = 1024;
-constexpr int kXoMaxBlocks = 32;
-__global__ void __launch_bounds__(kXoTokens) k_exec_one(const int32_t* __restrict__ route, int T, int E,
-                                                         int max_slots, int split_m, int32_t* res,
-                                                         int32_t* __restrict__ corrective, int32_t* __restrict__ num_slots,
-                                                         int32_t* __restrict__ off_g, int32_t* __restrict__ slot_row_g,
-                                                         int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
-                                                         int32_t* __restrict__ exp_begin, int pieces_stride,
-                                                         int32_t* err, int32_t* bh, int32_t* __restrict__ token_to_slot,
-                                                         int32_t* __restrict__ row_of_token,
-                                                         int32_t* __restrict__ tok_of_row) {
-  griddep_launch_dependents();
-  griddep_wait();
-  extern __shared__ int xo_sm[];
-  const int nb = gridDim.x, b = blockIdx.x;
-  int* s_wh = xo_sm;                   // [32 warps][E], then [nb][E] block histograms
-  int* s_res = s_wh + 32 * E;          // E: residency before this layer
-  int* s_dem = s_res + E;              // E: demand
-  int* s_pre = s_dem + E;              // E: this block's prefix
-  int* s_lay = s_pre + E;              // exec_layer_core scratch: s_off[E+1] s_n[E] s_row[ms+1] s_pc[ms+1]
-  __shared__ int red[40];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) s_wh[i] = 0;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) s_res[i] = res[i];
-  __syncthreads();
-  // ---- A
-  const int t = b * kXoTokens + threadIdx.x;
-  const int e = t < T ? __ldg(&route[t]) : -1;
-  const unsigned peers = __match_any_sync(0xffffffffu, e);
-  const int wr = __popc(peers & ((1u << lane) - 1u));
-  if (e >= 0 && lane == __ffs(peers) - 1) s_wh[w * E + e] = __popc(peers);
-  __syncthreads();
-  for (int x = threadIdx.x; x < E; x += blockDim.x) {
-    int run = 0;
-#pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-      const int c = s_wh[k * E + x];
-      s_wh[k * E + x] = run;
-      run += c;
-    }
-    bh[(size_t)b * E + x] = run;
-  }
-  __syncthreads();
-  const int inblock = e >= 0 ? s_wh[w * E + e] + wr : 0;
-  __threadfence();
-  __syncthreads();  // s_wh is reused below; every block's residency read precedes block 0's update
-  if (threadIdx.x == 0) {
-    atomicAdd(&err[1], 1);
-    int n;
-    do {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(n) : "l"(&err[1]) : "memory");
-      if (n < nb) __nanosleep(32);
-    } while (n < nb);
-  }
-  __syncthreads();
-  // ---- B
-  for (int i = threadIdx.x; i < nb * E; i += blockDim.x) s_wh[i] = __ldcg(&bh[i]);
-  __syncthreads();
-  for (int x = threadIdx.x; x < E; x += blockDim.x) {
-    int run = 0, pre = 0;
-    for (int k = 0; k < nb; ++k) {
-      if (k == b) pre = run;
-      run += s_wh[k * E + x];
-    }
-    s_dem[x] = run;
-    s_pre[x] = pre;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32)
-    exec_layer_warp(s_lay, s_dem, s_res, b == 0, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
-                    piece_row, piece_rows, exp_begin, err);
-  __syncthreads();
-  // ---- C
-  const int* s_off = s_lay;
-  const int* s_row = s_lay + 2 * E + 1;
-  if (t >= T || s_off[E] > max_slots) return;
-  const int rank = s_pre[e] + inblock;
-  const int o = s_off[e], c = s_off[e + 1] - o;
-  const int s = o + rank % c;
-  const int row = s_row[s] + rank / c;
-  token_to_slot[t] = s;
-  if (row_of_token) row_of_token[t] = row;
-  tok_of_row[row] = t;
-}
-
 __device__ void exec_rank_body(int l, int ch, int* se, const int32_t* __restrict__ route, int T, int E, int nch,
                                int max_slots, const int32_t* __restrict__ cc, const int32_t* __restrict__ off_g,
                                const int32_t* __restrict__ slot_row_g, int32_t* __restrict__ token_to_slot,
@@ -705,56 +562,6 @@ __global__ void __launch_bounds__(1024) k_exec_rank_gather(const int32_t* __rest
   }
 }
 
-// The whole execution map of mp_exec_map as ONE cooperative launch (grid (nch, L),
-// block kChunk, all blocks co-resident): chunk histograms | per-(layer, expert)
-// exclusive scans over chunks (one expert per block) | slot/piece layout (block
-// (0, l)) | stable ranks, separated by grid-wide barriers. Same arithmetic as the
-// four-kernel form, one launch instead of four.
-__global__ void k_exec_fused(const int32_t* __restrict__ route, int T, int E, int nch, int max_slots, int split_m,
-                             int32_t* __restrict__ cc, int32_t* __restrict__ demand, int32_t* __restrict__ res,
-                             int32_t* __restrict__ corrective, int32_t* __restrict__ num_slots,
-                             int32_t* __restrict__ off_g, int32_t* __restrict__ slot_row_g,
-                             int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
-                             int32_t* __restrict__ exp_begin, int pieces_stride, int32_t* __restrict__ err,
-                             int32_t* __restrict__ token_to_slot, int32_t* __restrict__ row_of_token,
-                             int32_t* __restrict__ tok_of_row) {
-  griddep_launch_dependents();
-  griddep_wait();
-  extern __shared__ int sm[];
-  __shared__ int red[40];
-  cg::grid_group grid = cg::this_grid();
-  const int l = blockIdx.y, ch = blockIdx.x;
-  // 1. chunk histogram
-  for (int e = threadIdx.x; e < E; e += blockDim.x) sm[e] = 0;
-  __syncthreads();
-  {
-    const int t = ch * kChunk + threadIdx.x;
-    if (t < T) atomicAdd(&sm[__ldg(&route[(size_t)l * T + t])], 1);
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) cc[((size_t)l * nch + ch) * E + e] = sm[e];
-  grid.sync();
-  // 2. per-expert exclusive scan over chunks (experts ch, ch + nch, ... of layer l)
-  for (int e = ch; e < E; e += nch) {
-    int32_t* col = cc + (size_t)l * nch * E + e;
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) sm[c] = col[(size_t)c * E];
-    __syncthreads();
-    const int total = block_exclusive_scan(sm, nch, red);
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) col[(size_t)c * E] = sm[c];
-    if (threadIdx.x == 0) demand[(size_t)l * E + e] = total;
-    __syncthreads();
-  }
-  grid.sync();
-  // 3. slots, rows and GEMM pieces of layer l
-  if (ch == 0)
-    exec_layer_body(l, sm, red, demand, E, max_slots, split_m, res, corrective, num_slots, off_g, slot_row_g,
-                    piece_row, piece_rows, exp_begin, pieces_stride, err);
-  grid.sync();
-  // 4. stable ranks -> slot, row, permutation
-  if (num_slots[l] <= max_slots)
-    exec_rank_body(l, ch, sm, route, T, E, nch, max_slots, cc, off_g, slot_row_g, token_to_slot, row_of_token,
-                   tok_of_row);
-}
 
 // Segments from an explicit token -> slot map. grid 1, block 1024.
 // size[s] (from the chunk histogram) -> slot_row (scan) -> pieces (scan).
@@ -957,44 +764,6 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
   const size_t sm_x = sizeof(int) * ((size_t)2 * E + 1 + 2 * ((size_t)max_slots + 1));
   MP_REQUIRE(sm_h <= 200 * 1024 && sm_x <= 200 * 1024, MP_ERR_CONFIG, "mp_exec_map: E/max_slots too large");
   const int pieces_stride = max_slots + cdiv(T, kChunk);
-  // MP_EXEC_FUSED=1: one cooperative launch instead of four (measured equal in a CUDA graph,
-  // so the plain four-kernel form stays the default); falls back when the grid cannot be co-resident
-  static const bool fused = getenv("MP_EXEC_FUSED") != nullptr;
-  if (fused) {
-    const size_t sm_f = std::max(std::max(sm_h, sm_x), sizeof(int) * (size_t)std::max(nch, kChunk));
-    MP_CUDA_TRY(set_smem((const void*)k_exec_fused, sm_f));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(nch, L);
-    cfg.blockDim = dim3(kChunk);
-    cfg.dynamicSmemBytes = sm_f;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    const cudaError_t ce = cudaLaunchKernelEx(&cfg, k_exec_fused, route, T, E, nch, max_slots, split_m, cc, dem, res,
-                                              corrective, num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin,
-                                              pieces_stride, err, token_to_slot, row_of_token, tok_of_row);
-    if (ce == cudaSuccess) return MP_OK;
-    if (ce != cudaErrorCooperativeLaunchTooLarge) MP_CUDA_TRY(ce);
-    (void)cudaGetLastError();
-  }
-  // MP_EXEC_ONE=1: the single-launch form (k_exec_one). Measured in the step graph it is
-  // equal to the four-kernel form (3.152 vs 3.159 M tokens/s, 4 runs each; its memset node and
-  // grid arrival cost what the saved launches gain), so the four kernels -- no inter-block
-  // waiting at all -- stay the default.
-  static const bool four = getenv("MP_EXEC_ONE") == nullptr;
-  const int nb = cdiv(T, kXoTokens);
-  const size_t sm_o = sizeof(int) * ((size_t)32 * E + 3 * (size_t)E) + sm_x;
-  if (!four && L == 1 && E <= 256 && nb <= kXoMaxBlocks && nb <= num_sms() && sm_o <= 200 * 1024) {
-    MP_CUDA_TRY(set_smem((const void*)k_exec_one, sm_o));
-    MP_CUDA_TRY(cudaMemsetAsync(err + 1, 0, sizeof(int32_t), st));  // grid arrival counter
-    MP_CUDA_TRY(launch_pdl(k_exec_one, dim3(nb), dim3(kXoTokens), sm_o, st, route, T, E, max_slots, split_m, res,
-                           corrective, num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin, pieces_stride, err,
-                           cc, token_to_slot, row_of_token, tok_of_row));
-    return MP_OK;
-  }
   MP_CUDA_TRY(set_smem((const void*)k_chunk_hist, sm_h));
   MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
   MP_CUDA_TRY(launch_pdl(k_chunk_hist, dim3(dim3(nch, L)), dim3(kChunk), sm_h, st, route, T, E, nch, cc));
@@ -1007,53 +776,6 @@ extern "C" int mp_exec_map(const int32_t* route, int L, int T, int E, int max_sl
   return MP_OK;
 }
 
-// mp_exec_map (one layer) after mp_route_top1_defer: the first kernel re-decides the
-// uncertain tokens in float64 (x: the stream the router read, w32: E x d fp32 router rows)
-// and writes the exact routes back, then counts -- no separate recheck launch.
-extern "C" int mp_exec_map_recheck(int32_t* route, int T, int E, int max_slots, int split_m, int32_t* res,
-                                   int32_t* token_to_slot, int32_t* corrective, int32_t* num_slots,
-                                   int32_t* row_of_token, int32_t* tok_of_row, int32_t* piece_row,
-                                   int32_t* piece_rows, int32_t* exp_begin, const float* x, int ldx, int d,
-                                   const float* w32, void* xperm, void* ws, size_t ws_bytes, void* stream) {
-  MP_REQUIRE(T >= 1 && E >= 1 && max_slots >= 1 && d >= 1 && ldx >= d, MP_ERR_CONFIG,
-             "mp_exec_map_recheck: bad sizes T=%d E=%d d=%d", T, E, d);
-  MP_REQUIRE(ws_bytes >= mp_exec_workspace_bytes(1, T, E, max_slots), MP_ERR_CONFIG,
-             "mp_exec_map_recheck: workspace too small");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int nch = cdiv(T, kChunk);
-  char* p = (char*)ws;
-  int32_t* cc = (int32_t*)p;
-  p += align_up(sizeof(int32_t) * (size_t)nch * E);
-  int32_t* dem = (int32_t*)p;
-  p += align_up(sizeof(int32_t) * (size_t)E);
-  int32_t* off_g = (int32_t*)p;
-  p += align_up(sizeof(int32_t) * (size_t)(E + 1));
-  int32_t* slot_row = (int32_t*)p;
-  p += align_up(sizeof(int32_t) * (size_t)(max_slots + 1));
-  int32_t* err = (int32_t*)p;
-  const size_t sm_h = sizeof(int) * (size_t)E;
-  const size_t sm_x = sizeof(int) * ((size_t)2 * E + 1 + 2 * ((size_t)max_slots + 1));
-  MP_REQUIRE(sm_h <= 200 * 1024 && sm_x <= 200 * 1024, MP_ERR_CONFIG, "mp_exec_map_recheck: E/max_slots too large");
-  const int pieces_stride = max_slots + nch;
-  MP_CUDA_TRY(set_smem((const void*)k_chunk_hist_recheck, sm_h));
-  MP_CUDA_TRY(set_smem((const void*)k_exec_layer, sm_x));
-  MP_CUDA_TRY(launch_pdl(k_chunk_hist_recheck, dim3(nch), dim3(kChunk), sm_h, st, route, T, E, nch, cc, x, ldx, d,
-                         w32));
-  MP_CUDA_TRY(launch_pdl(k_chunk_prefix_cols, dim3(dim3(cdiv(E, 32), 1)), dim3(1024), 0, st, cc, nch, E, dem));
-  MP_CUDA_TRY(launch_pdl(k_exec_layer, dim3(1), dim3(1024), sm_x, st, dem, E, max_slots, split_m, res, corrective,
-                         num_slots, off_g, slot_row, piece_row, piece_rows, exp_begin, pieces_stride, err));
-  if (xperm != nullptr && ldx == d && (d == 768 || d == 1024)) {  // ranks + the FFN permute in one launch
-    auto kern = d == 768 ? k_exec_rank_gather<192> : k_exec_rank_gather<256>;
-    MP_CUDA_TRY(launch_pdl(kern, dim3(nch), dim3(1024), 0, st, (const int32_t*)route, T, E, nch, max_slots, cc, off_g,
-                           slot_row, token_to_slot, row_of_token, tok_of_row, x, (__nv_bfloat16*)xperm));
-  } else {
-    MP_REQUIRE(xperm == nullptr, MP_ERR_CONFIG, "mp_exec_map_recheck: the fused permute needs ldx == d in {768, 1024}");
-    MP_CUDA_TRY(launch_pdl(k_exec_rank, dim3(dim3(nch, 1)), dim3(kChunk), 0, st, (const int32_t*)route, T, E, nch,
-                           max_slots, cc, off_g, slot_row, token_to_slot, row_of_token, tok_of_row));
-  }
-  MP_CUDA_TRY(cudaGetLastError());
-  return MP_OK;
-}
 
 // mp_exec_map (one layer) after mp_route_top1_hist wrote the chunk histograms into the
 // first cdiv(T, 128) x E ints of ws: chunk prefixes, slot/row/piece layout, ranks (+ the FFN

@@ -81,10 +81,6 @@ __device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const 
                "r"(smem_u32(smem_src)), "r"(c0), "r"(c1), "l"(policy)
                : "memory");
 }
-// Drop one 128-byte L2 line without writing it back (its contents are dead).
-__device__ __forceinline__ void l2_discard(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // the shared-memory sources of all committed bulk stores have been read
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }

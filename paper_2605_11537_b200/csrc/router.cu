@@ -8,8 +8,6 @@
 // the fp32 inputs) by a warp-per-token kernel. The bound per logit is
 //   |err| <= 2^-12 * sum_k |x_k| * max_e |w_ek|
 // (split residuals ~3*2^-17 plus worst-case fp32 accumulation of 3d terms).
-#include <cstdlib>
-
 #include "epilogues.cuh"
 #include "launch.cuh"
 
@@ -74,271 +72,18 @@ __global__ void k_router_recheck(const float* __restrict__ x, int ldx, int d, co
 }
 
 
-// ---------------------------------------------------------------------------
+constexpr int kRfConvThreads = 256;  // convert + epilogue threads (warps 4..11)
+
 // Fused router (Eg <= 128): the split of x into bf16 hi/lo and the bound scale
-// sum_k |x_k| * wabs_k are computed INSIDE the GEMM by the 8 epilogue warps,
-// which read x (fp32, L2-resident residual stream) straight from global memory
-// and write the two SWIZZLE_128B K-major operand tiles into shared memory; no
-// T x 2d split buffer goes through HBM and there is no pre-pass launch.
-// Per k-block (64 columns):
+// sum_k |x_k| * wabs_k are computed INSIDE the GEMM. A producer warp (warp 3) streams x
+// fp32 k-blocks (two 128 x 32 SWIZZLE_128B boxes) into a 3-deep shared-memory ring; the 8
+// epilogue warps convert them into the two SWIZZLE_128B K-major operand tiles (no T x 2d
+// split buffer goes through HBM, no pre-pass launch). Per k-block (64 columns):
 //   acc[:, 0:Eg)   += x_hi . w_hi^T + x_lo . w_hi^T     (N = Eg MMA on the hi rows)
 //   acc[:, Eg:2Eg) += x_hi . w_lo^T                     (part of one N = 2Eg MMA)
 // with B = [w_hi ; w_lo] stacked as 2Eg rows of one tile; logit = acc[e] + acc[Eg + e].
-// Roles: warp 0 TMA (B), warp 1 MMA, warp 2 TMEM, warps 4..11 convert + epilogue.
-constexpr int kRfStages = 3;
-constexpr int kRfConvThreads = 256;
-
-template <int EG>
-struct RfSmem {
-  static constexpr int kB = 2 * EG * 128;          // [w_hi ; w_lo] k-block tile
-  static constexpr int kA = 128 * 128;             // one 128 x 64 bf16 tile
-  static constexpr int kStage = kB + 2 * kA;       // B | x_hi | x_lo
-  static constexpr int kBarOffset = kRfStages * kStage;
-  // full[S] (B tx), conv[S] (8 warps), empty[S] (MMA commit), tfull, tempty
-  static constexpr int kXbOffset = kBarOffset + (3 * kRfStages + 2) * 8 + 8;
-  static constexpr int kBytes = kXbOffset + 128 * 4 + 1024;
-};
-
-template <int EG>
-__global__ void __launch_bounds__(kGemmThreads, 1)
-    k_router_fused(const __grid_constant__ CUtensorMap tmB, const float* __restrict__ x, int ldx, int T, int d,
-                   const float* __restrict__ wabs, int E, int32_t* __restrict__ route, float eps,
-                   int32_t* __restrict__ count, int32_t* __restrict__ list) {
-#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
-  using L = RfSmem<EG>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
-  uint64_t* conv = full + kRfStages;
-  uint64_t* empty = conv + kRfStages;
-  uint64_t* tfull = empty + kRfStages;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-  float* s_xb = reinterpret_cast<float*>(smem + L::kXbOffset);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = d / 64;
-  const int units = (T + kBlockM - 1) / kBlockM;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmB);
-    for (int s = 0; s < kRfStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], kRfConvThreads / 32);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 4);  // the 4 warps of epilogue warpgroup 0
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * EG < 32 ? 32 : 2 * EG);
-  griddep_wait();  // x is the previous layer's output
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ B producer
-      uint32_t stage = 0, phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sb = smem + stage * L::kStage;
-          mbar_arrive_expect_tx(&full[stage], L::kB);
-          tma_load_2d(sb, &tmB, &full[stage], kb * 64, 0);                // w_hi rows
-          tma_load_2d(sb + EG * 128, &tmB, &full[stage], d + kb * 64, 0);  // w_lo rows
-          if (++stage == kRfStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      constexpr uint32_t id_all = idesc_bf16_f32(kBlockM, 2 * EG);
-      constexpr uint32_t id_hi = idesc_bf16_f32(kBlockM, EG);
-      uint32_t stage = 0, phase = 0, tile = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
-        mbar_wait(tempty, (tile & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          mbar_wait(&conv[stage], phase);
-          tc_fence_after();
-          uint8_t* sb = smem + stage * L::kStage;
-          const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sb));
-          const uint64_t dhi = sw128_kmajor_desc(smem_u32(sb + L::kB));
-          const uint64_t dlo = sw128_kmajor_desc(smem_u32(sb + L::kB + L::kA));
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            umma_bf16(tmem_base, dhi + 2 * k, bdesc + 2 * k, id_all, (kb | k) != 0);
-            umma_bf16(tmem_base, dlo + 2 * k, bdesc + 2 * k, id_hi, 1);
-          }
-          umma_commit(&empty[stage]);
-          if (++stage == kRfStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        umma_commit(tfull);
-      }
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ convert + epilogue
-    const int ct = threadIdx.x - 128;  // 0..255
-    const int jc = ct & 7;             // 16-byte column chunk of the k-block (8 bf16)
-    const int r0 = ct >> 3;            // rows r0 + 32 i, i = 0..3
-    uint32_t stage = 0, phase = 0, tile = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
-      const int row_base = u * kBlockM;
-      float part[4] = {0.f, 0.f, 0.f, 0.f};
-      float4 cur[4][2];
-      auto load = [&](int kb, float4 (&v)[4][2]) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int t = row_base + r0 + 32 * i;
-          if (t < T) {
-            const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * ldx + kb * 64 + 8 * jc);
-            v[i][0] = __ldg(src);
-            v[i][1] = __ldg(src + 1);
-          } else {
-            v[i][0] = v[i][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-      };
-      load(0, cur);
-      for (int kb = 0; kb < nkb; ++kb) {
-        float4 nxt[4][2];
-        if (kb + 1 < nkb) load(kb + 1, nxt);
-        const float4 w0 = __ldg(reinterpret_cast<const float4*>(wabs + kb * 64 + 8 * jc));
-        const float4 w1 = __ldg(reinterpret_cast<const float4*>(wabs + kb * 64 + 8 * jc + 4));
-        mbar_wait(&empty[stage], phase ^ 1);  // MMA done with this stage's operand tiles
-        uint8_t* shi = smem + stage * L::kStage + L::kB;
-        uint8_t* slo = shi + L::kA;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = r0 + 32 * i;
-          const float f[8] = {cur[i][0].x, cur[i][0].y, cur[i][0].z, cur[i][0].w,
-                              cur[i][1].x, cur[i][1].y, cur[i][1].z, cur[i][1].w};
-          uint32_t hw[4], lw[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
-            const float2 hf = __bfloat1622float2(h);
-            const __nv_bfloat162 lo = __floats2bfloat162_rn(f[2 * q] - hf.x, f[2 * q + 1] - hf.y);
-            hw[q] = *reinterpret_cast<const uint32_t*>(&h);
-            lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
-          }
-          // SWIZZLE_128B K-major: row r at r * 128 B, 16-byte chunk jc stored at chunk jc ^ (r & 7)
-          const int off = r * 128 + ((jc ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(shi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          *reinterpret_cast<uint4*>(slo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-          part[i] += fabsf(f[0]) * w0.x + fabsf(f[1]) * w0.y + fabsf(f[2]) * w0.z + fabsf(f[3]) * w0.w +
-                     fabsf(f[4]) * w1.x + fabsf(f[5]) * w1.y + fabsf(f[6]) * w1.z + fabsf(f[7]) * w1.w;
-        }
-        fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[stage]);
-        if (++stage == kRfStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-        if (kb + 1 < nkb) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            cur[i][0] = nxt[i][0];
-            cur[i][1] = nxt[i][1];
-          }
-        }
-      }
-      // bound scale per row: the 8 lanes of a row hold disjoint column chunks
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        float v = part[i];
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        if (jc == 0) s_xb[r0 + 32 * i] = v * 1.0001f + 1e-30f;
-      }
-      named_bar_sync(1, kRfConvThreads);
-      if (warp < 8) {  // warpgroup 0: TMEM lanes 0..127 = tile rows; top-1 + certification
-        mbar_wait(tfull, tile & 1);
-        tc_fence_after();
-        const int r = (warp & 3) * 32 + lane;
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-        float b1 = -INFINITY, b2 = -INFINITY;
-        int bi = 0;
-#pragma unroll 1
-        for (int c = 0; c < EG; c += 32) {
-          float a[32], b[32];
-          tmem_ld32(taddr + c, a);
-          tmem_ld32(taddr + EG + c, b);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int e = c + i;
-            const float v = a[i] + b[i];
-            if (e < E) {
-              if (v > b1) {
-                b2 = b1;
-                b1 = v;
-                bi = e;
-              } else if (v > b2) {
-                b2 = v;
-              }
-            }
-          }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
-        const int t = row_base + r;
-        if (t < T) {
-          route[t] = bi;
-          if (E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r])) {
-            const int k = atomicAdd(count, 1);
-            list[k] = t;
-          }
-        }
-      }
-      named_bar_sync(1, kRfConvThreads);  // s_xb reuse by the next tile
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * EG < 32 ? 32 : 2 * EG);
-  }
-#endif
-}
-
-template <int EG>
-static int launch_router_fused(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
-                               int32_t* route, int32_t* count, int32_t* list, float eps, cudaStream_t st) {
-  CUtensorMap tb;
-  int rc = make_tmap_bf16(&tb, w_hl, EG, 2 * d, 2 * d, EG);
-  if (rc) return rc;
-  auto kern = k_router_fused<EG>;
-  const int smem = RfSmem<EG>::kBytes;
-  static bool configured = false;
-  if (!configured) {
-    MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
-  MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
-  const int units = cdiv(T, kBlockM);
-  MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, x, ldx,
-                         T, d, w_abs, E, route, eps, count, list));
-  return MP_OK;
-}
-
-
-// k_router_fused with x staged by TMA: a fourth role (warp 3) streams x fp32 k-blocks
-// (two 128 x 32 SWIZZLE_128B boxes) into a 3-deep shared-memory ring, so the
-// converters read x from shared memory instead of holding global loads in registers
-// (the register form is latency-bound: 18 % warps active, x at 2.2 TB/s). The operand
-// ring is 2 deep (measured equal to 3 deep for the register form). EG <= 128.
+// Roles: warp 0 TMA (B), warp 3 TMA (x), warp 1 MMA, warp 2 TMEM, warps 4..11 convert +
+// epilogue. The operand ring is 2 deep.
 constexpr int kRxStages = 2;
 constexpr int kRxXStages = 3;
 template <int EG>
@@ -359,7 +104,7 @@ template <int EG>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_router_fused_tx(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int T, int d,
                       const float* __restrict__ wabs, int E, int32_t* __restrict__ route, float eps,
-                      int32_t* __restrict__ count, int32_t* __restrict__ list, int defer,
+                      int32_t* __restrict__ count, int32_t* __restrict__ list,
                       const float* __restrict__ xg, int ldx, const float* __restrict__ w32,
                       int32_t* __restrict__ hist_cc) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
@@ -598,15 +343,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             atomicAdd(&s_hist[bi], 1);
           }
         } else if (t < T) {
-          const bool unsure = E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r]);
-          if (defer) {  // the consumer re-decides marked tokens (mp_exec_map_recheck)
-            route[t] = unsure ? -1 - bi : bi;
-          } else {
-            route[t] = bi;
-            if (unsure) {
-              const int k = atomicAdd(count, 1);
-              list[k] = t;
-            }
+          route[t] = bi;
+          if (E > 1 && !(b1 - b2 > 2.f * eps * s_xb[r])) {  // queued for k_router_recheck
+            const int k = atomicAdd(count, 1);
+            list[k] = t;
           }
         }
       }
@@ -632,7 +372,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 template <int EG>
 static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
                                   int32_t* route, int32_t* count, int32_t* list, float eps, cudaStream_t st,
-                                  int defer = 0, const float* w32 = nullptr, int32_t* hist_cc = nullptr) {
+                                  const float* w32 = nullptr, int32_t* hist_cc = nullptr) {
   CUtensorMap tb, tx;
   int rc = make_tmap_bf16(&tb, w_hl, EG, 2 * d, 2 * d, EG);
   if (rc) return rc;
@@ -646,10 +386,10 @@ static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const v
     MP_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  if (!defer && hist_cc == nullptr) MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+  if (hist_cc == nullptr) MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
   const int units = cdiv(T, kBlockM);
   MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, tx, T,
-                         d, w_abs, E, route, eps, count, list, defer, x, ldx, w32, hist_cc));
+                         d, w_abs, E, route, eps, count, list, x, ldx, w32, hist_cc));
   return MP_OK;
 }
 
@@ -718,40 +458,18 @@ extern "C" int mp_route_top1_ex(const float* x, int ldx, int T, int d, const voi
   ROUTER_CHECKS();
   cudaStream_t st = (cudaStream_t)stream;
   const RouterWs rw(ws, T, d);
-  static const bool unfused = getenv("MP_ROUTER_UNFUSED") != nullptr;  // A/B switch
-  if (!unfused && (Eg == 64 || Eg == 128) && ldx % 4 == 0) {
-    static const bool reg_x = getenv("MP_ROUTER_REGX") != nullptr;  // A/B switch: x through registers
-    int rc;
-    if (reg_x || (reinterpret_cast<uintptr_t>(x) & 15) != 0)
-      rc = Eg == 128 ? launch_router_fused<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
-                     : launch_router_fused<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
-    else
-      rc = Eg == 128
-               ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
-               : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
+  if ((Eg == 64 || Eg == 128) && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const int rc = Eg == 128
+                       ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st)
+                       : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st);
     if (rc) return rc;
     MP_CUDA_TRY(launch_pdl(k_router_recheck, dim3(num_sms()), dim3(256), 0, st, x, ldx, d, w_f32, E, rw.count, rw.list, route));
     MP_CUDA_TRY(cudaGetLastError());
     return MP_OK;
   }
+  // any other layout (Eg = 256, unaligned rows): split pre-pass + split-bf16 GEMM + recheck
   k_router_prep<<<cdiv(T * 32, 256), 256, 0, st>>>(x, ldx, T, d, w_abs, (__nv_bfloat16*)rw.xhl, rw.xb, rw.count);
   return route_gemm(x, ldx, T, d, w_hl, w_f32, E, Eg, route, rw, kRouterEps, st);
-}
-
-// mp_route_top1_ex without the fp64 re-decision launch: uncertain tokens (top-2 gap inside
-// the certified error bound) are written as route = -1 - e_bf16; mp_exec_map_recheck
-// re-decides them in float64 inside its first kernel (same arithmetic as the recheck
-// kernel) before counting. Needs the TMA-operand router (Eg in {64, 128}, ldx % 4 == 0,
-// 16-byte aligned x).
-extern "C" int mp_route_top1_defer(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_abs, int E,
-                                   int Eg, int32_t* route, void* ws, size_t ws_bytes, void* stream) {
-  ROUTER_CHECKS();
-  MP_REQUIRE((Eg == 64 || Eg == 128) && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0, MP_ERR_CONFIG,
-             "mp_route_top1_defer: needs Eg in {64, 128}, ldx %% 4 == 0, 16-byte aligned x");
-  cudaStream_t st = (cudaStream_t)stream;
-  const RouterWs rw(ws, T, d);
-  return Eg == 128 ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st, 1)
-                   : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st, 1);
 }
 
 // Exact routing with the fp64 re-decision of near ties done inside the router's epilogue
@@ -768,9 +486,9 @@ extern "C" int mp_route_top1_hist(const float* x, int ldx, int T, int d, const v
   cudaStream_t st = (cudaStream_t)stream;
   const RouterWs rw(ws, T, d);
   return Eg == 128 ? launch_router_fused_tx<128>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps,
-                                                 st, 0, w_f32, chunk_hist)
+                                                 st, w_f32, chunk_hist)
                    : launch_router_fused_tx<64>(x, ldx, T, d, w_hl, w_abs, E, route, rw.count, rw.list, kRouterEps, st,
-                                                0, w_f32, chunk_hist);
+                                                w_f32, chunk_hist);
 }
 
 extern "C" int mp_route_top1(const float* x, int ldx, int T, int d, const void* w_hl, const float* w_f32, int E,

@@ -557,21 +557,11 @@ extern "C" int mp_sru_scan(const float* x_f32, int T, int d, const float* c0, fl
   SRU_CHECKS();
   cudaStream_t st = (cudaStream_t)stream;
   const SruWs w(ws, T, d);
-  const int nch = cdiv(T, kScanChunk);
-  static const bool three_pass = getenv("MP_SRU_3PASS") != nullptr;  // A/B switch: the three-kernel form
-  if (!three_pass) {
-    const int nblk = cdiv(T, kSpTokens), nstr = cdiv(d, 128);
-    MP_CUDA_TRY(cudaMemsetAsync(w.sp_flags, 0, sizeof(int) * ((size_t)nstr * nblk + 1), st));
-    MP_CUDA_TRY(launch_pdl(k_scan_fused, dim3(nstr * nblk), dim3(32 * kSpWarps), 0, st, w.ufr, x_f32, T, d, c0, h_f32,
-                           (__nv_bfloat16*)h_bf16, c_last, nonfinite, w.sp_flags, w.aggA, w.carry, nblk));
-    return MP_OK;
-  }
-  // K2: chunk aggregates | carries (from c0) | replay + highway
-  const dim3 gq(cdiv(d / 4, 64), nch);
-  MP_CUDA_TRY(launch_pdl(k_scan_aggregate, dim3(gq), dim3(64), 0, st, w.ufr, T, d, w.aggA, w.aggB));
-  MP_CUDA_TRY(launch_pdl(k_scan_carry, dim3(cdiv(d, 32)), dim3(32 * kCarryGroups), 0, st, w.aggA, w.aggB, nch, d, c0, w.carry, nullptr));
-  MP_CUDA_TRY(launch_pdl(k_scan_output, dim3(gq), dim3(64), 0, st, w.ufr, x_f32, T, d, w.carry, h_f32, (__nv_bfloat16*)h_bf16, c_last, nonfinite));
-  MP_CUDA_TRY(cudaGetLastError());
+  // K2: one launch -- chunk maps, decoupled look-back carries, replay + highway
+  const int nblk = cdiv(T, kSpTokens), nstr = cdiv(d, 128);
+  MP_CUDA_TRY(cudaMemsetAsync(w.sp_flags, 0, sizeof(int) * ((size_t)nstr * nblk + 1), st));
+  MP_CUDA_TRY(launch_pdl(k_scan_fused, dim3(nstr * nblk), dim3(32 * kSpWarps), 0, st, w.ufr, x_f32, T, d, c0, h_f32,
+                         (__nv_bfloat16*)h_bf16, c_last, nonfinite, w.sp_flags, w.aggA, w.carry, nblk));
   return MP_OK;
 }
 

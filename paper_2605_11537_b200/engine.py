@@ -27,7 +27,6 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import math
-import os
 from dataclasses import asdict, dataclass
 
 import torch
@@ -36,9 +35,6 @@ from . import _lib
 from ._dev import ptr, require_device, round_up, stream_ptr
 from .predictor import DeviceSru
 from .router_oracle import DeviceMoeLayer, router_eg
-
-# kernels of one SRU scan (csrc/sru.cu mp_sru_scan): single pass, or the three-kernel form
-_SCAN_KERNELS = 3 if os.environ.get("MP_SRU_3PASS") else 1
 
 DISTINCT_ONLY_UNIT = 1 << 30  # ceil(n / unit) == 1 for every demanded expert
 
@@ -55,13 +51,12 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
-    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else two) | two (single-tile units) |
-                                  # mt (multi-tile units, slower: see DESIGN) | pair (CTA pairs) |
-                                  # fused (experimental: one launch, H in an L2 ring)
-    sru_pipeline: bool = False    # two-stream token-half SRU pipeline (measured slower: 1219 vs 1133 us)
+    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else two) | two (single-CTA
+                                  # grouped GEMMs) | pair (CTA-pair cta_group::2 grouped GEMMs)
     skew: float = 1.2
     noise: float = 0.1
-    seed: int = 0
+    seed: int = 0                 # model: routers, experts, predictor (identical on every rank)
+    batch_seed: int | None = None  # synthetic batches (per rank under EP); None: derived from seed
 
     def as_dict(self):
         return asdict(self)
@@ -81,7 +76,9 @@ class SyntheticSwitch:
         self.cfg = cfg
         self.dev = device
         g = torch.Generator(device=device).manual_seed(cfg.seed)
-        self.g = g
+        self.g = g  # model draws (same on every rank)
+        bseed = cfg.batch_seed if cfg.batch_seed is not None else cfg.seed * 1000003 + 17
+        self.gb = torch.Generator(device=device).manual_seed(bseed)  # batch draws
         E, d, L = cfg.num_experts, cfg.d_model, cfg.num_layers
         self.k = max(1, d // 2)
         c = torch.randn(E, self.k, device=device, generator=g, dtype=torch.float64)
@@ -116,14 +113,14 @@ class SyntheticSwitch:
 
     def batch(self, T: int):
         """(embeddings (T, d) fp32, layer-0 experts (T,), oracle routing (L, T))."""
-        e0 = torch.multinomial(self.probs, T, replacement=True, generator=self.g)
+        e0 = torch.multinomial(self.probs, T, replacement=True, generator=self.gb)
         base = self.centroids[e0]
         emb = torch.empty_like(base)
         pending = torch.arange(T, device=self.dev)
         rout = self.centroids[:, : self.k].double()
         for _ in range(100):
             cand = base[pending] + self.cfg.noise * torch.randn(len(pending), self.cfg.d_model, device=self.dev,
-                                                                generator=self.g)
+                                                                generator=self.gb)
             logits = cand[:, : self.k].double() @ rout.T
             own = logits.gather(1, e0[pending, None]).squeeze(1)
             logits.scatter_(1, e0[pending, None], -math.inf)
@@ -174,7 +171,10 @@ class MoEPipeline:
             heads = torch.stack([self.wl.router(l) for l in range(L)]).double()
         else:
             heads = draw(L, E, d)
-        self.sru = DeviceSru([tuple(t.cpu().numpy() for t in lay) for lay in sru], heads.cpu().numpy(), dev)
+        # host float64 copies: the checks in tests/ and bench.py recompute the predictor from them
+        self.sru_host = [tuple(t.cpu().numpy() for t in lay) for lay in sru]
+        self.heads_host = heads.cpu().numpy()
+        self.sru = DeviceSru(self.sru_host, self.heads_host, dev)
         # ---- buffers
         i32 = dict(dtype=torch.int32, device=dev)
         self.assign = torch.empty(L, T, **i32)
@@ -207,13 +207,6 @@ class MoEPipeline:
 
         self.ws_sru_n = _lib.size_query("mp_sru_workspace_bytes", T, d)
         self.ws_sru = ws(self.ws_sru_n)
-        # two-stream SRU pipeline over token halves (see _sru_pipelined)
-        self.sru_halves = cfg.sru_pipeline and T % 256 == 0 and T >= 512
-        if self.sru_halves:
-            self.ws_sru_h_n = _lib.size_query("mp_sru_workspace_bytes", T // 2, d)
-            self.ws_sru_h = [ws(self.ws_sru_h_n) for _ in range(2)]
-            self.sru_carry = torch.zeros(d, device=dev)
-            self.sru_stream = torch.cuda.Stream(device=dev)
         self.ws_hist_n = _lib.size_query("mp_histogram_workspace_bytes", L, T, E)
         self.ws_hist = ws(self.ws_hist_n)
         self.ws_place_n = _lib.size_query("mp_place_workspace_bytes", L, T, E)
@@ -225,18 +218,7 @@ class MoEPipeline:
         self.ws_ffn_n = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
         self.ws_ffn = ws(self.ws_ffn_n)
         self.pstride = pstride
-        self.ws_fused_n = _lib.size_query("mp_ffn_fused_workspace_bytes", T, d, F, pstride)
-        self.ws_fused = ws(self.ws_fused_n) if cfg.ffn == "fused" else None
         self.launches_per_step = None
-        import os
-        self.h_discard = os.environ.get("MP_H_DISCARD") is not None  # opt-in: measured no gain
-        # router without its re-decision launch; the execution map's first kernel re-decides
-        # near ties in float64 (MP_ROUTER_RECHECK_LAUNCH=1: separate recheck kernel, A/B switch)
-        self.defer_recheck = os.environ.get("MP_ROUTER_RECHECK_LAUNCH") is None
-        # ranks + FFN permute in one kernel (MP_RANK_GATHER_OFF=1: separate gather, A/B switch)
-        self.rank_gather = os.environ.get("MP_RANK_GATHER_OFF") is None
-        # router writes the chunk histograms (MP_ROUTE_HIST_OFF=1: histogram in the execution map)
-        self.route_hist = os.environ.get("MP_ROUTE_HIST_OFF") is None
 
     # ------------------------------------------------------------------ pieces of a step
     def predict(self, x: torch.Tensor, sp: int) -> int:
@@ -245,58 +227,16 @@ class MoEPipeline:
         n = 0
         _lib.call("mp_f32_to_bf16", ptr(x), ptr(self.x16), T * d, sp)
         n += 1
-        if self.sru_halves:
-            n += self._sru_pipelined(x, sp)
-            cur16 = self.h16[(len(self.sru.w_cat) - 1) % 2]
-        else:
-            cur32, cur16 = x, self.x16
-            for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
-                h32, h16 = self.h32[i % 2], self.h16[i % 2]
-                _lib.call("mp_sru_layer", ptr(cur16), ptr(cur32), ptr(W), ptr(B), T, d, None, ptr(h32), ptr(h16), None,
-                          ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
-                n += 1 + _SCAN_KERNELS
-                cur32, cur16 = h32, h16
+        cur32, cur16 = x, self.x16
+        for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
+            h32, h16 = self.h32[i % 2], self.h16[i % 2]
+            _lib.call("mp_sru_layer", ptr(cur16), ptr(cur32), ptr(W), ptr(B), T, d, None, ptr(h32), ptr(h16), None,
+                      ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
+            n += 2  # projection GEMM + single-pass scan
+            cur32, cur16 = h32, h16
         _lib.call("mp_heads_argmax", ptr(cur16), ptr(self.sru.heads), T, d, cfg.num_layers, cfg.num_experts,
                   self.sru.Eg, ptr(self.assign), sp)
         return n + 1
-
-    def _sru_pipelined(self, x: torch.Tensor, sp: int) -> int:
-        """SRU stack with the batch split into two token halves on two streams: the scan
-        (memory-bound) of one half overlaps the projection GEMM (tensor-bound) of the other,
-        and layer i+1's projection of a half starts as soon as layer i's scan of that half is
-        done. The scan of the second half starts from the first half's final carry, so the
-        result is the sequential recurrence (same kernels, same arithmetic)."""
-        T, d, T2 = self.cfg.tokens, self.dp, self.cfg.tokens // 2
-        A = torch.cuda.ExternalStream(sp)
-        Bs = self.sru_stream
-        fork = torch.cuda.Event()
-        fork.record(A)
-        Bs.wait_event(fork)
-        ev_g = [[torch.cuda.Event() for _ in range(2)] for _ in range(len(self.sru.w_cat))]
-        ev_s = [[torch.cuda.Event() for _ in range(2)] for _ in range(len(self.sru.w_cat))]
-        self._sru_events = (fork, ev_g, ev_s)  # keep alive while the graph is captured
-        rows16, rows32 = T2 * d * 2, T2 * d * 4
-        n = 0
-        for i, (W, B) in enumerate(zip(self.sru.w_cat, self.sru.b_cat)):
-            in16 = self.x16 if i == 0 else self.h16[(i - 1) % 2]
-            in32 = x if i == 0 else self.h32[(i - 1) % 2]
-            h32, h16 = self.h32[i % 2], self.h16[i % 2]
-            for k in range(2):
-                if i > 0:
-                    A.wait_event(ev_s[i - 1][k])
-                _lib.call("mp_sru_project", ptr(in16) + k * rows16, ptr(W), ptr(B), T2, d, ptr(self.ws_sru_h[k]),
-                          self.ws_sru_h_n, sp)
-                ev_g[i][k].record(A)
-                Bs.wait_event(ev_g[i][k])
-                c0 = None if k == 0 else ptr(self.sru_carry)
-                c_last = ptr(self.sru_carry) if k == 0 else None
-                _lib.call("mp_sru_scan", ptr(in32) + k * rows32, T2, d, c0, ptr(h32) + k * rows32,
-                          ptr(h16) + k * rows16, c_last, ptr(self.nonfinite), ptr(self.ws_sru_h[k]), self.ws_sru_h_n,
-                          Bs.cuda_stream)
-                ev_s[i][k].record(Bs)
-                n += 1 + _SCAN_KERNELS
-        A.wait_event(ev_s[-1][1])  # join
-        return n
 
     def plan_and_place(self, sp: int) -> int:
         """Alg. 1: demand histogram -> capped plan -> residency + token walk for all layers."""
@@ -312,26 +252,21 @@ class MoEPipeline:
         return 2 + 1 + 4
 
     def layer(self, l: int, x: torch.Tensor, sp: int, ev=None) -> int:
-        """One MoE layer in place on the residual stream x."""
+        """One MoE layer in place on the residual stream x. Returns #kernel launches.
+
+        ev: optional 3 events recorded around GEMM1 / GEMM2 (roofline timing)."""
         cfg, T, E, d, F = self.cfg, self.cfg.tokens, self.cfg.num_experts, self.dp, self.Fp
         lay = self.layers[l]
-        # the fused FFN needs <= 128-row pieces: replicas longer than a tile are split into
-        # consecutive M tiles of the SAME replica (a replica is still one slot)
-        # replication "off" keeps one serial unit per expert (one server per expert, the
-        # paper's baseline); the multi-tile kernel pairs 128-row tiles, so it runs on split
-        # pieces (a replica is still one slot; its tiles are independent GEMM units)
-        use_mt = cfg.ffn == "mt" and cfg.replication != "off" and d % 256 == 0 and E <= 1024
-        # CTA-pair (cta_group::2) grouped GEMMs: pieces of <= 128 rows, an even number per expert
         use_pair = cfg.ffn == "pair" and d % 256 == 0
-        split = 1 if (cfg.replication == "split" or cfg.ffn == "fused" or use_mt) else 0
-        if use_pair:
-            split = 3
-        # the permute into the FFN workspace rides on the execution map's last kernel when it can
-        gather_fused = ((self.defer_recheck or self.route_hist) and lay.Eg <= 128 and d in (768, 1024)
-                        and cfg.ffn != "fused" and not self.h_discard and self.rank_gather)
-        if self.route_hist and lay.Eg <= 128:
-            # the router re-decides near ties itself and writes each tile's expert histogram
-            # into the execution-map workspace: routing + histogram in one launch
+        # replication "off" keeps one serial unit per replica (one server per expert, the paper's
+        # baseline); "split" makes every 128-row tile its own unit; the CTA-pair kernels need
+        # <= 128-row pieces padded to an even count per expert (split_m = 3)
+        split = 3 if use_pair else (1 if cfg.replication == "split" else 0)
+        # the permute into the FFN workspace rides on the execution map's rank kernel
+        gather_fused = d in (768, 1024)
+        if lay.Eg <= 128:
+            # the router re-decides near ties itself (float64) and writes each 128-token tile's
+            # expert histogram into the execution-map workspace: routing + histogram in one launch
             _lib.call("mp_route_top1_hist", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
                       ptr(self.route[l]), ptr(self.ws_exec), ptr(self.ws_router), self.ws_router_n, sp)
             _lib.call("mp_exec_map_hist", ptr(self.route[l]), T, E, self.max_slots, split, ptr(self.res[l]),
@@ -339,52 +274,33 @@ class MoEPipeline:
                       ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                       ptr(self.exp_begin[l]), ptr(x), d, ptr(self.ws_ffn) if gather_fused else None,
                       ptr(self.ws_exec), self.ws_exec_n, sp)
-            n = 0  # router (+ the 3 execution-map kernels: counted below as 4)
-        elif self.defer_recheck and lay.Eg <= 128:
-            # near-tie tokens are re-decided in float64 inside the execution map's first kernel
-            _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w_abs), E, lay.Eg,
-                      ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
-            _lib.call("mp_exec_map_recheck", ptr(self.route[l]), T, E, self.max_slots, split, ptr(self.res[l]),
-                      ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
-                      ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
-                      ptr(self.exp_begin[l]), ptr(x), d, d, ptr(lay.w32),
-                      ptr(self.ws_ffn) if gather_fused else None, ptr(self.ws_exec), self.ws_exec_n, sp)
-            n = 1  # router (the 4 execution-map kernels are added below)
-        else:
+            n = 1 + 3  # router | chunk prefixes, slot layout, ranks (+ permute)
+        else:  # E > 128: split pre-pass + split-bf16 GEMM + recheck, then the four-kernel map
             _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
                       ptr(self.route[l]), ptr(self.ws_router), self.ws_router_n, sp)
-            n = 2  # router, recheck (the 4 execution-map kernels are added below)
             _lib.call("mp_exec_map", ptr(self.route[l]), 1, T, E, self.max_slots, split, ptr(self.res[l]),
                       ptr(self.exec_slot[l]), ptr(self.corrective[l]), ptr(self.exec_slots[l:l + 1]), None,
                       ptr(self.tok_of_row[l]), ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                       ptr(self.exp_begin[l]), ptr(self.ws_exec), self.ws_exec_n, sp)
-        if cfg.ffn == "fused":
-            if ev is not None:
-                ev[0].record(sp)
-            _lib.call("mp_ffn_fused", ptr(x), T, d, F, E, ptr(lay.U), ptr(lay.V), ptr(self.tok_of_row[l]),
-                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), self.pstride,
-                      ptr(self.ws_fused), self.ws_fused_n, sp)
-            if ev is not None:
-                ev[1].record(sp)
-                ev[2].record(sp)
-            return n + 4 + 1 + 1 + 1
+            n = 3 + 4
+            gather_fused = False
         if not gather_fused:
             _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n,
                       sp)
+            n += 1
         if ev is not None:
             ev[0].record(sp)
-        flags = lay.tiled | (4 if use_mt else 0) | (2 if use_pair else 0)
+        flags = lay.tiled | (2 if use_pair else 0)
         _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), flags, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
         if ev is not None:
             ev[1].record(sp)
-        # bit 4: GEMM2 drops each piece's H from L2 once consumed (counters zeroed by the gather)
-        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags | (16 if self.h_discard else 0),
-                  ptr(self.tok_of_row[l]), ptr(self.piece_row[l]),
-                  ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
+        _lib.call("mp_ffn_down", ptr(x), T, d, F, E, ptr(lay.V), flags, ptr(self.tok_of_row[l]),
+                  ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn),
+                  self.ws_ffn_n, sp)
         if ev is not None:
             ev[2].record(sp)
-        return n + 4 + 1 + 1 + 1
+        return n + 2
 
     # ------------------------------------------------------------------ expert parallelism
     def enable_expert_parallel(self, group=None) -> None:
@@ -440,7 +356,7 @@ class MoEPipeline:
             _lib.call("mp_sru_fold_carry", ptr(self.sru_tots), self.rank, d, None, ptr(self.sru_carry_in), sp)
             _lib.call("mp_sru_scan_finish", ptr(cur32), T, d, ptr(self.sru_carry_in), ptr(h32), ptr(h16), None,
                       ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
-            n += 6
+            n += 6  # GEMM | aggregate, carry | fold | carry, replay
             cur32, cur16 = h32, h16
         _lib.call("mp_heads_argmax", ptr(cur16), ptr(self.sru.heads), T, d, cfg.num_layers, cfg.num_experts,
                   self.sru.Eg, ptr(self.assign), sp)
@@ -489,6 +405,29 @@ class MoEPipeline:
             n += self.layer(l, x, sp, events[l] if events is not None else None)
         self.launches_per_step = n
         return n
+
+    def step_checked(self, x: torch.Tensor, rows: torch.Tensor) -> list[torch.Tensor]:
+        """Eager single-device step that also snapshots the residual-stream rows ``rows`` before
+        every MoE layer and after the last one (L + 1 tensors), for correctness checks taken
+        outside any timed region (bench.py, tests)."""
+        sp = stream_ptr()
+        self.predict(x, sp)
+        self.plan_and_place(sp)
+        snaps = []
+        for l in range(self.cfg.num_layers):
+            snaps.append(x[rows].clone())
+            self.layer(l, x, sp)
+        snaps.append(x[rows].clone())
+        return snaps
+
+    def expert_weights_untiled(self, l: int, e: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """(U_e (F, d), V_e (d, F)) bf16 of layer l, expert e, back in the reference layout
+        (router_oracle.py:26-27) from the pre-tiled device copy."""
+        lay = self.layers[l]
+        d, F = lay.dp, lay.Fp
+        u = lay.U.view(lay.E, F // 256, d // 64, 256, 64)[e].permute(0, 2, 1, 3).reshape(F, d)
+        v = lay.V.view(lay.E, d // lay.vbn, F // 64, lay.vbn, 64)[e].permute(0, 2, 1, 3).reshape(d, F)
+        return u, v
 
     # ------------------------------------------------------------------ CUDA graph
     def capture(self, x: torch.Tensor, events=None) -> "StepGraph":
@@ -661,9 +600,10 @@ def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor, f
     u2, v2 = u.reshape(E * F, d).contiguous(), v.reshape(E * d, F).contiguous()
     lay.U, lay.V = torch.empty_like(u2), torch.empty_like(v2)
     _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
-    vbn = 256 if ffn in ("mt", "pair", "fused") else _lib.size_query("mp_ffn_down_bn", d)  # those kernels: BN 256
+    vbn = 256 if ffn == "pair" else _lib.size_query("mp_ffn_down_bn", d)  # the CTA-pair kernels read BN 256
     _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, vbn, stream_ptr())
     lay.tiled = 1
+    lay.vbn = vbn
     del u2, v2
     return lay
 

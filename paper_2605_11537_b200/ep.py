@@ -68,7 +68,6 @@ class CudaEpKernels:
         self.ws = torch.empty(self.ws_n, dtype=torch.uint8, device=dev)
         self.hist_n = _lib.size_query("mp_histogram_workspace_bytes", 1, tokens, self.E)
         self.hist_ws = torch.empty(max(self.hist_n, 256), dtype=torch.uint8, device=dev)
-        self.ffn_flags = 0  # single-tile grouped GEMMs (bit 2, multi-tile units, measured slower)
         self.ffn_n = _lib.size_query("mp_ffn_workspace_bytes", self.cap_rows, self.d, self.F)
         self.ffn_ws = torch.empty(self.ffn_n, dtype=torch.uint8, device=dev)
         self.counts_buf = torch.empty(self.E, **i32)
@@ -152,11 +151,14 @@ class CudaEpKernels:
         sp = stream_ptr()
         if ev is not None:
             ev[0].record(sp)
-        _lib.call("mp_ffn_up", n, self.d, self.F, self.E, ptr(lay.U), lay.tiled | self.ffn_flags, ptr(plan.piece_row),
+        # single-CTA grouped GEMMs over the EP pieces (split_m = 1); a V tiled for the CTA-pair
+        # kernels (256-column slices) is read with 256-column units (flags bit 6)
+        vflag = 64 if lay.tiled and getattr(lay, "vbn", 0) == 256 else 0
+        _lib.call("mp_ffn_up", n, self.d, self.F, self.E, ptr(lay.U), lay.tiled, ptr(plan.piece_row),
                   ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
         if ev is not None:
             ev[1].record(sp)
-        _lib.call("mp_ffn_down", ptr(y), n, self.d, self.F, self.E, ptr(lay.V), lay.tiled | self.ffn_flags | 32,
+        _lib.call("mp_ffn_down", ptr(y), n, self.d, self.F, self.E, ptr(lay.V), lay.tiled | 32 | vflag,
                   ptr(self.recv_of_local),
                   ptr(plan.piece_row), ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
         if ev is not None:

@@ -32,3 +32,13 @@ def test_bench_prints_one_contract_line():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert d["checks"]["routing_exact_last_step"] is True
+    c = d["checks"]
+    assert c["routing_exact_sampled"] is True and c["weights_identical_on_all_ranks"] is True
+    assert c["ffn_maxnorm_rel"] <= c["tolerance"] and c["sru_maxnorm_rel"] <= c["tolerance"]
+    b = d["baselines"]
+    for k in ("replication_off", "split", "random_predictor", "hf_loop", "ratios_whole_step"):
+        assert k in b, k
+    assert d["grouped_gemm_config2"]["tflops"] > 0
+    alg = d["roofline"]["algorithmic_bytes_per_layer"]
+    t = (d["roofline"]["ms_gemm1"] + d["roofline"]["ms_gemm2"]) * 1e-3
+    assert abs(alg / t / 1e9 - d["roofline"]["achieved"]) <= 1e-6 * d["roofline"]["achieved"]

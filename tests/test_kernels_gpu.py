@@ -101,63 +101,6 @@ def test_router_exact(dev):
     assert (route.long() == ref).all()
 
 
-@pytest.mark.parametrize("T,E", [(4096, 12), (1000, 100), (300, 64)])
-def test_deferred_router_recheck_in_exec_map(dev, T, E):
-    """mp_route_top1_defer + mp_exec_map_recheck == exact float64 argmax routing (lowest index on
-    ties) and the same execution map as mp_route_top1_ex + mp_exec_map, with exact ties forced
-    (every token near a tie is re-decided inside the execution map's first kernel)."""
-    d = 128
-    Eg = 64 if E <= 64 else 128
-    g = torch.Generator(device=dev).manual_seed(T + E)
-    x = torch.randn(T, d, device=dev, generator=g)
-    w = torch.randn(E, d, device=dev, generator=g)
-    w[5] = w[3]  # exact tie -> lower index
-    w[E - 1] = w[0] * (1 + 2 ** -20)  # near tie
-    w_hi = w.bfloat16()
-    w_lo = (w - w_hi.float()).bfloat16()
-    whl = torch.zeros(Eg, 2 * d, device=dev, dtype=torch.bfloat16)
-    whl[:E, :d] = w_hi
-    whl[:E, d:] = w_lo
-    wabs = torch.empty(d, device=dev)
-    _lib.call("mp_router_weight_absmax", ptr(w), E, d, ptr(wabs), stream_ptr())
-    nbytes = _lib.size_query("mp_router_workspace_bytes", T, d)
-    rws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    ref = (x.double() @ w.double().T).argmax(-1)
-    i32 = dict(dtype=torch.int32, device=dev)
-    max_slots = 2 * E
-    pstride = max_slots + (T + 127) // 128
-    xn = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
-    outs = []
-    for deferred in (False, True):
-        route = torch.full((T,), -7, **i32)
-        o = dict(res=torch.zeros(E, **i32), tts=torch.empty(T, **i32), corr=torch.empty(E, **i32),
-                 ns=torch.empty(1, **i32), rot=torch.empty(T, **i32), tor=torch.empty(T, **i32),
-                 prow=torch.zeros(pstride, **i32), prows=torch.zeros(pstride, **i32), eb=torch.empty(E + 1, **i32))
-        xws = torch.empty(xn, dtype=torch.uint8, device=dev)
-        tail = (ptr(o["tts"]), ptr(o["corr"]), ptr(o["ns"]), ptr(o["rot"]), ptr(o["tor"]), ptr(o["prow"]),
-                ptr(o["prows"]), ptr(o["eb"]))
-        if deferred:
-            _lib.call("mp_route_top1_defer", ptr(x), d, T, d, ptr(whl), ptr(wabs), E, Eg, ptr(route), ptr(rws), nbytes,
-                      stream_ptr())
-            _lib.call("mp_exec_map_recheck", ptr(route), T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(x), d, d, ptr(w),
-                      None, ptr(xws), xn, stream_ptr())
-        else:
-            _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(whl), ptr(w), ptr(wabs), E, Eg, ptr(route), ptr(rws),
-                      nbytes, stream_ptr())
-            _lib.call("mp_exec_map", ptr(route), 1, T, E, max_slots, 1, ptr(o["res"]), *tail, ptr(xws), xn,
-                      stream_ptr())
-        torch.cuda.synchronize()
-        o["route"] = route
-        outs.append(o)
-    a, b = outs
-    assert (b["route"].long() == ref).all()
-    n_pieces = int(a["eb"][-1].item())
-    for k in ("route", "res", "tts", "corr", "ns", "rot", "tor", "eb"):
-        assert torch.equal(a[k], b[k]), k
-    assert torch.equal(a["prow"][:n_pieces], b["prow"][:n_pieces])
-    assert torch.equal(a["prows"][:n_pieces], b["prows"][:n_pieces])
-
-
 @pytest.mark.parametrize("T,E", [(4096, 12), (1000, 100), (300, 64), (20000, 128)])
 def test_router_histogram_path_matches(dev, T, E):
     """mp_route_top1_hist (near ties re-decided inside the router, chunk histograms written)
@@ -258,30 +201,33 @@ def test_exec_map_hist_from_given_chunk_histograms(dev, T, E, split_m):
 
 
 @pytest.mark.parametrize("T,E,d", [(16384, 128, 768), (3001, 40, 1024), (200, 8, 768)])
-def test_exec_map_recheck_permute_matches_ffn_gather(dev, T, E, d):
-    """mp_exec_map_recheck with xperm (ranks + FFN permute in one kernel) == mp_exec_map_recheck
+def test_exec_map_rank_permute_matches_ffn_gather(dev, T, E, d):
+    """mp_exec_map_hist with xperm (ranks + FFN permute in one kernel) == mp_exec_map_hist
     without it followed by mp_ffn_gather: same maps, same permuted bf16 rows."""
     rng = np.random.default_rng(T + E)
     p = 1.0 / (np.arange(E) + 1.0) ** 1.2
-    route0 = torch.from_numpy(rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)).to(dev)
+    route_h = rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)
+    route = torch.from_numpy(route_h).to(dev)
     x = torch.randn(T, d, device=dev)
-    w = torch.randn(E, d, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
     max_slots, F = 2 * E, 256
     pstride = max_slots + (T + 127) // 128
     xn = _lib.size_query("mp_exec_workspace_bytes", 1, T, E, max_slots)
     fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
+    nch = (T + 127) // 128
+    cc = np.zeros((nch, E), dtype=np.int32)
+    np.add.at(cc, (np.arange(T) // 128, route_h), 1)
     outs = []
     for fused in (False, True):
-        route = route0.clone()
         o = dict(res=torch.zeros(E, **i32), tts=torch.empty(T, **i32), corr=torch.empty(E, **i32),
                  ns=torch.empty(1, **i32), rot=torch.empty(T, **i32), tor=torch.empty(T, **i32),
                  prow=torch.zeros(pstride, **i32), prows=torch.zeros(pstride, **i32), eb=torch.empty(E + 1, **i32),
                  fws=torch.zeros(fb, dtype=torch.uint8, device=dev))
-        xws = torch.empty(xn, dtype=torch.uint8, device=dev)
+        xws = torch.zeros(xn, dtype=torch.uint8, device=dev)
+        xws[: cc.nbytes].copy_(torch.from_numpy(cc.view(np.uint8).reshape(-1)))
         tail = (ptr(o["tts"]), ptr(o["corr"]), ptr(o["ns"]), ptr(o["rot"]), ptr(o["tor"]), ptr(o["prow"]),
                 ptr(o["prows"]), ptr(o["eb"]))
-        _lib.call("mp_exec_map_recheck", ptr(route), T, E, max_slots, 0, ptr(o["res"]), *tail, ptr(x), d, d, ptr(w),
+        _lib.call("mp_exec_map_hist", ptr(route), T, E, max_slots, 0, ptr(o["res"]), *tail, ptr(x), d,
                   ptr(o["fws"]) if fused else None, ptr(xws), xn, stream_ptr())
         if not fused:
             _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(o["tor"]), ptr(o["fws"]), fb, stream_ptr())
@@ -502,30 +448,17 @@ def test_cta_pair_ffn_matches_single_cta(dev, split):
     assert torch.equal(y1, y2)
 
 
-@pytest.mark.parametrize("skew,d,F,tiled", [(0.0, 256, 768, 1), (1.2, 512, 512, 1), (3.0, 768, 1280, 0),
-                                             (1.2, 256, 256, 0), (8.0, 512, 768, 1)])
-def test_multi_tile_ffn_matches_single_tile(dev, skew, d, F, tiled):
-    _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 4)
-
-
-@pytest.mark.parametrize("skew,d,F,tiled", [(0.0, 768, 768, 1), (1.2, 512, 1024, 1), (3.0, 768, 1280, 0),
-                                             (1.2, 256, 512, 1), (8.0, 768, 3072, 1)])
-def test_multicast_cluster_ffn_matches_single_cta(dev, skew, d, F, tiled):
-    """A tile multicast across a cluster of CTAs (one per weight slice) == the single-CTA
-    kernels, bit for bit (cluster sizes 2/3/4 chosen by the slice counts)."""
-    _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 8)
-
-
-@pytest.mark.parametrize("skew,d,F,tiled", [(1.2, 768, 3072, 1), (3.0, 512, 768, 0), (0.0, 256, 512, 1)])
-def test_hidden_discard_keeps_results(dev, skew, d, F, tiled):
-    """flags bit 4: GEMM2 discards each piece's hidden rows from L2 after its last slice unit;
-    the results must not change (no unit may read H after the discard)."""
-    _check_ffn_mode_bitwise(dev, skew, d, F, tiled, 16)
+@pytest.mark.parametrize("skew,d,F", [(0.0, 256, 768), (1.2, 512, 512), (1.2, 768, 3072), (8.0, 768, 1280)])
+def test_single_cta_gemm2_reads_pair_tiled_v(dev, skew, d, F):
+    """flags bit 6: the single-CTA GEMM2 reading V tiled in 256-column slices (the CTA-pair
+    layout; expert parallelism reuses the weights of a pair-mode pipeline) == the reference
+    layout, bit for bit."""
+    _check_ffn_mode_bitwise(dev, skew, d, F, 1, 64)
 
 
 def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
-    """Multi-tile units (two accumulator tiles sharing A or B) == the single-tile kernels, bit for bit:
-    odd and even piece counts per expert, odd slice counts, empty experts, both weight layouts."""
+    """mp_ffn_gather / up / down with ``mode`` flags == mp_moe_ffn on the reference layout, bit for
+    bit: odd and even piece counts per expert, empty experts."""
     rng = np.random.default_rng(int(skew * 10) + d + F)
     T, E = 5000, 21
     p = 1.0 / (np.arange(E) + 1.0) ** skew
@@ -542,8 +475,8 @@ def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
               ptr(eb), ptr(sws), nb, stream_ptr())
     U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
     V = (torch.randn(E * d, F, device=dev) / 28).bfloat16()
-    if tiled:  # V column tiles: 256 for the pair / multi-tile / multicast kernels, else mp_ffn_down_bn
-        vbn = 256 if mode & (2 | 4 | 8) else _lib.size_query("mp_ffn_down_bn", d)
+    if tiled:  # V column tiles: 256 with bit 6, else mp_ffn_down_bn
+        vbn = 256 if mode & 64 else _lib.size_query("mp_ffn_down_bn", d)
         Ut, Vt = torch.empty_like(U), torch.empty_like(V)
         _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
         _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, vbn, stream_ptr())
@@ -560,7 +493,7 @@ def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
     y2 = x.clone()
     ws.zero_()
     _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(tor), ptr(ws), fb, stream_ptr())
-    _lib.call("mp_ffn_up", T, d, F, E, ptr(Ut), tiled | mode, ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb,
+    _lib.call("mp_ffn_up", T, d, F, E, ptr(Ut), tiled | (mode & 2), ptr(prow), ptr(prows), ptr(eb), ptr(ws), fb,
               stream_ptr())
     h2 = ws[h0:h0 + T * F * 2].clone()
     _lib.call("mp_ffn_down", ptr(y2), T, d, F, E, ptr(Vt), tiled | mode, ptr(tor), ptr(prow), ptr(prows), ptr(eb),
@@ -568,41 +501,3 @@ def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
     torch.cuda.synchronize()
     assert torch.equal(h1, h2)
     assert torch.equal(y1, y2)
-
-
-@pytest.mark.parametrize("skew", [0.0, 1.2, 3.0])
-def test_fused_interleaved_ffn_matches_two_launch(dev, skew):
-    """Fused GEMM1/GEMM2 launch with the L2 ring for H == the two-launch path, bit for bit."""
-    rng = np.random.default_rng(int(skew * 10) + 1)
-    T, E, d, F = 6000, 24, 256, 768
-    p = 1.0 / (np.arange(E) + 1.0) ** skew
-    route = torch.from_numpy(rng.choice(E, size=T, p=p / p.sum()).astype(np.int32)).to(dev)
-    slot_expert = torch.arange(E, dtype=torch.int32, device=dev)
-    i32 = dict(dtype=torch.int32, device=dev)
-    nb = _lib.size_query("mp_segments_workspace_bytes", T, E)
-    sws = torch.empty(nb, dtype=torch.uint8, device=dev)
-    pn = E + (T + 127) // 128
-    tor = torch.empty(T, **i32)
-    prow, prows, eb = torch.empty(pn, **i32), torch.empty(pn, **i32), torch.empty(E + 1, **i32)
-    _lib.call("mp_segments_from_slots", ptr(route), ptr(slot_expert), T, E, E, 1, ptr(tor), ptr(prow), ptr(prows),
-              ptr(eb), ptr(sws), nb, stream_ptr())
-    U = (torch.randn(E * F, d, device=dev) / 16).bfloat16()
-    V = (torch.randn(E * d, F, device=dev) / 28).bfloat16()
-    Ut, Vt = torch.empty_like(U), torch.empty_like(V)
-    _lib.call("mp_tile_kmajor", ptr(U), ptr(Ut), E, F, d, 256, stream_ptr())
-    _lib.call("mp_tile_kmajor", ptr(V), ptr(Vt), E, d, F, 256, stream_ptr())
-    x = torch.randn(T, d, device=dev)
-    y1 = x.clone()
-    fb = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
-    ws = torch.empty(fb, dtype=torch.uint8, device=dev)
-    _lib.call("mp_moe_ffn", ptr(x), ptr(y1), T, d, F, E, ptr(U), ptr(V), ptr(tor), ptr(prow), ptr(prows), ptr(eb),
-              ptr(ws), fb, stream_ptr())
-    y2 = x.clone()
-    fz = _lib.size_query("mp_ffn_fused_workspace_bytes", T, d, F, pn)
-    wz = torch.empty(fz, dtype=torch.uint8, device=dev)
-    for _ in range(2):  # second run reuses the counters/ring (reset inside)
-        y2.copy_(x)
-        _lib.call("mp_ffn_fused", ptr(y2), T, d, F, E, ptr(Ut), ptr(Vt), ptr(tor), ptr(prow), ptr(prows), ptr(eb), pn,
-                  ptr(wz), fz, stream_ptr())
-        torch.cuda.synchronize()
-        assert torch.equal(y1, y2)

@@ -11,8 +11,6 @@ run --experts 100 --tokens 5000 --layers 3
 run --experts 64 --tokens 3000 --layers 2 --replication off
 run --experts 200 --tokens 777 --layers 2 --capacity 250 --replication split
 run --experts 8 --tokens 100 --layers 1 --capacity 8
-run --experts 128 --tokens 16384 --layers 2 --ffn mt
-run --experts 128 --tokens 16384 --layers 2 --ffn fused
 run --experts 128 --tokens 16384 --layers 2 --ffn pair
 run --experts 128 --tokens 40000 --layers 2
 run --experts 128 --tokens 16384 --layers 2 --overlap on
