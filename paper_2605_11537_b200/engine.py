@@ -51,8 +51,9 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
-    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else two) | two (single-CTA
-                                  # grouped GEMMs) | pair (CTA-pair cta_group::2 grouped GEMMs)
+    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else fused) | fused (one kernel:
+                                  # GEMM1 -> relu -> GEMM2 + combine, hidden on chip) | two (single-CTA
+                                  # grouped GEMM pair) | pair (CTA-pair cta_group::2 grouped GEMMs)
     skew: float = 1.2
     noise: float = 0.1
     seed: int = 0                 # model: routers, experts, predictor (identical on every rank)
@@ -141,7 +142,8 @@ class MoEPipeline:
             # BASELINE config 2 runs at 1,126 vs 1,007 TF/s); single-CTA units on weight-streaming
             # layers (config 3: 128 tokens per expert, pairs are 12 % slower) -- profiles/README.md
             pair = cfg.tokens >= 1024 * cfg.num_experts and cfg.d_model % 256 == 0
-            cfg = dataclasses.replace(cfg, ffn="pair" if pair else "two")
+            fused = _lib.size_query("mp_ffn_fused_tile", cfg.d_model) > 0 and cfg.d_ff % 128 == 0
+            cfg = dataclasses.replace(cfg, ffn="pair" if pair else ("fused" if fused else "two"))
         self.cfg = cfg
         self.dev = device or require_device()
         dev = self.dev
@@ -216,7 +218,7 @@ class MoEPipeline:
         self.ws_router_n = _lib.size_query("mp_router_workspace_bytes", T, d)
         self.ws_router = ws(self.ws_router_n)
         self.ws_ffn_n = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
-        self.ws_ffn = ws(self.ws_ffn_n)
+        self.ws_ffn = torch.zeros(self.ws_ffn_n, dtype=torch.uint8, device=dev)  # fused FFN ticket starts at 0
         self.pstride = pstride
         self.launches_per_step = None
 
@@ -290,6 +292,14 @@ class MoEPipeline:
             n += 1
         if ev is not None:
             ev[0].record(sp)
+        if cfg.ffn == "fused":
+            _lib.call("mp_ffn_fused", ptr(x), T, d, F, E, ptr(lay.U), ptr(lay.V), 0, ptr(self.tok_of_row[l]),
+                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn),
+                      self.ws_ffn_n, sp)
+            if ev is not None:
+                ev[1].record(sp)
+                ev[2].record(sp)
+            return n + 1
         flags = lay.tiled | (2 if use_pair else 0)
         _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), flags, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
@@ -425,7 +435,8 @@ class MoEPipeline:
         (router_oracle.py:26-27) from the pre-tiled device copy."""
         lay = self.layers[l]
         d, F = lay.dp, lay.Fp
-        u = lay.U.view(lay.E, F // 256, d // 64, 256, 64)[e].permute(0, 2, 1, 3).reshape(F, d)
+        ubn = lay.ubn
+        u = lay.U.view(lay.E, F // ubn, d // 64, ubn, 64)[e].permute(0, 2, 1, 3).reshape(F, d)
         v = lay.V.view(lay.E, d // lay.vbn, F // 64, lay.vbn, 64)[e].permute(0, 2, 1, 3).reshape(d, F)
         return u, v
 
@@ -599,11 +610,14 @@ def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor, f
     # pre-tiled B operands: each TMA box of the grouped GEMMs is one contiguous 32 KB burst
     u2, v2 = u.reshape(E * F, d).contiguous(), v.reshape(E * d, F).contiguous()
     lay.U, lay.V = torch.empty_like(u2), torch.empty_like(v2)
-    _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
-    vbn = 256 if ffn == "pair" else _lib.size_query("mp_ffn_down_bn", d)  # the CTA-pair kernels read BN 256
+    # the fused FFN reads 128-row boxes of both; the CTA-pair kernels read V in 256-column slices
+    ubn = 128 if ffn == "fused" else _lib.size_query("mp_ffn_up_bn", F)
+    vbn = 128 if ffn == "fused" else (256 if ffn == "pair" else _lib.size_query("mp_ffn_down_bn", d))
+    _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, ubn, stream_ptr())
     _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, vbn, stream_ptr())
     lay.tiled = 1
-    lay.vbn = vbn
+    lay.ubn, lay.vbn = ubn, vbn
+    lay.ffn = ffn
     del u2, v2
     return lay
 

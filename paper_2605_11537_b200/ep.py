@@ -69,7 +69,7 @@ class CudaEpKernels:
         self.hist_n = _lib.size_query("mp_histogram_workspace_bytes", 1, tokens, self.E)
         self.hist_ws = torch.empty(max(self.hist_n, 256), dtype=torch.uint8, device=dev)
         self.ffn_n = _lib.size_query("mp_ffn_workspace_bytes", self.cap_rows, self.d, self.F)
-        self.ffn_ws = torch.empty(self.ffn_n, dtype=torch.uint8, device=dev)
+        self.ffn_ws = torch.zeros(self.ffn_n, dtype=torch.uint8, device=dev)  # fused FFN ticket starts at 0
         self.counts_buf = torch.empty(self.E, **i32)
         self.sizes = torch.empty(2 * world + 1, **i32)  # send counts | recv counts | local rows
         self.sc, self.rc, self.nloc = self.sizes[:world], self.sizes[world:2 * world], self.sizes[2 * world:]
@@ -151,6 +151,14 @@ class CudaEpKernels:
         sp = stream_ptr()
         if ev is not None:
             ev[0].record(sp)
+        if getattr(lay, "ffn", "") == "fused":  # one kernel; stores into the receive-order rows
+            _lib.call("mp_ffn_fused", ptr(y), n, self.d, self.F, self.E, ptr(lay.U), ptr(lay.V), 32,
+                      ptr(self.recv_of_local), ptr(plan.piece_row), ptr(plan.piece_rows), ptr(plan.exp_begin),
+                      ptr(self.ffn_ws), self.ffn_n, sp)
+            if ev is not None:
+                ev[1].record(sp)
+                ev[2].record(sp)
+            return y
         # single-CTA grouped GEMMs over the EP pieces (split_m = 1); a V tiled for the CTA-pair
         # kernels (256-column slices) is read with 256-column units (flags bit 6)
         vflag = 64 if lay.tiled and getattr(lay, "vbn", 0) == 256 else 0
