@@ -272,23 +272,6 @@ MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, in
 MP_API int mp_ffn_down_bn(int dp);
 /* column-tile width (and mp_tile_kmajor BN) of the pre-tiled expert U weights for GEMM1 */
 MP_API int mp_ffn_up_bn(int Fp);
-/* The whole expert FFN of a layer in ONE persistent tcgen05 kernel with the hidden activation
- * kept on chip (router_oracle.py:101-111 + 127-134): per replica slot (piece), NT-token tiles
- * (NT = mp_ffn_fused_tile(dp)) run GEMM1 (U_e chunk as the 128-row M operand, tokens as N),
- * relu -> bf16 into shared memory, GEMM2 accumulating y^T in TMEM over the d_ff chunks, then
- * y[tok_of_row[row]] += result (flags bit 5: = result). Requires dp % 128 == 0, dp <= 768,
- * Fp % 128 == 0; u / v pre-tiled by mp_tile_kmajor with BN = 128 (u: G=E, N=Fp, K=dp;
- * v: G=E, N=dp, K=Fp); xperm (the first region of ws) filled by mp_ffn_gather or the
- * execution map's rank kernel. Slots are handed out by a self-resetting ticket in the last
- * 256 bytes of ws: zero the workspace once before the first call. */
-MP_API int mp_ffn_fused(float* y, int T, int dp, int Fp, int E, const void* u, const void* v, int flags,
-                        const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
-                        const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
-/* token tile of mp_ffn_fused for model width dp (0: unsupported width) */
-MP_API int mp_ffn_fused_tile(int dp);
-/* Diagnostics: per-CTA wait cycles by role of the last mp_ffn_fused launch made with the
- * environment variable MP_FUSED_DEBUG set (out[cta * 16 + k], n <= 16384 entries). */
-MP_API int mp_debug_fused_waits(unsigned long long* out, int n);
 /* Diagnostics: per-CTA %globaltimer start / end (ns) of the last grouped-GEMM launch
  * (host arrays of n <= 1024). */
 MP_API int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1, int n);
@@ -298,11 +281,14 @@ MP_API int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, int B
 
 /* ------------------------------------------------------------------ C1/C2: expert parallelism
  * (SURVEY.md §8(e)). G ranks, tokens sharded by position, all expert weights resident on
- * every GPU, replica j of expert e on GPU (e*G/E + j) mod G. Per layer, after the caller
- * all-gathers per-rank expert counts C (G x E int32, from mp_histogram_ws):
+ * every GPU, the slot list cut into G blocks of equal rows (a slot runs on the GPU its row
+ * midpoint falls in). Per layer, after the caller all-gathers per-rank expert counts C
+ * (G x E int32, from mp_histogram_ws):
  *   mp_ep_plan         same residency/corrective update and global stable ranks as the
  *                      single-device execution map; send/recv row counts per peer; this
- *                      rank's send position per token; local pieces of hosted replicas
+ *                      rank's send position per token; local pieces of hosted replicas.
+ *                      More slots than max_slots (>= G * capacity + E): num_local_rows = -1
+ *                      and zero counts, so the caller raises before any collective
  *   mp_ep_pack         bf16 rows into the send buffer (destination-major)
  *   (caller: variable all-to-all of the rows, e.g. NCCL)
  *   mp_ep_recv_layout  local row (slot-major, global token order) of every received row

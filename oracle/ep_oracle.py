@@ -34,10 +34,13 @@ def ep_plan(route, C, res, rank, split=True):
     slot_e = np.repeat(np.arange(E), cnt)
     slot_j = np.arange(S) - off[slot_e]
     slot_c = cnt[slot_e]
-    slot_gpu = (slot_e * G // E + slot_j) % G
     acc = np.concatenate([np.zeros((1, E), np.int64), np.cumsum(C, 0)])  # (G+1, E)
     rows = np.stack([_F(acc[g + 1][slot_e], slot_j, slot_c) - _F(acc[g][slot_e], slot_j, slot_c) for g in range(G)])
     size = rows.sum(0)
+    # slot list cut into G blocks of equal rows (the slot's row midpoint decides its GPU)
+    before = np.concatenate([[0], np.cumsum(size)[:-1]]) if S else np.zeros(0, np.int64)
+    total = int(size.sum())
+    slot_gpu = np.minimum(G - 1, ((2 * before + size) * G) // (2 * total)) if total > 0 else np.zeros(S, np.int64)
     # sender
     send_counts = np.array([rows[rank][slot_gpu == dd].sum() for dd in range(G)], dtype=np.int64)
     send_displ = np.concatenate([[0], np.cumsum(send_counts)])

@@ -79,9 +79,6 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_down": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down_bn": (_I, [_I]),
     "mp_ffn_up_bn": (_I, [_I]),
-    "mp_ffn_fused": (_I, [_P, _I, _I, _I, _I, _P, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
-    "mp_ffn_fused_tile": (_I, [_I]),
-    "mp_debug_fused_waits": (_I, [_P, _I]),
     "mp_debug_cta_times": (_I, [_P, _P, _I]),
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "mp_replica_copy": (_I, [_P, _P, _Z, _P]),

@@ -7,8 +7,11 @@
 //     cnt_e = res_e, or one corrective replica; slot (e, j) for j < cnt_e;
 //   * a token's GLOBAL stable rank = its local rank + sum_{g < rank} C[g][e], so
 //     slot(t) = off[e] + grank mod cnt_e is bit-identical to one device;
-//   * replica (e, j) runs on GPU (home(e) + j) mod G, home(e) = e * G / E (all
-//     expert weights are resident on every GPU; placement spreads hot replicas);
+//   * replica -> GPU: the slot list (expert-major, ordinal-minor) is cut into G blocks of
+//     equal rows -- slot s runs on GPU floor((rows before s + size_s / 2) * G / total rows).
+//     Every GPU gets ~total/G rows and a hot expert's replicas stay on as few (consecutive)
+//     GPUs as its rows need, so each expert's weights are streamed by as few GPUs as possible
+//     (all expert weights are resident on every GPU);
 //   * rows(g, s) = #tokens of rank g on slot s, in closed form:
 //     #{y in [B_g, B_g + C_g) : y = j mod c} = F(B_g + C_g) - F(B_g),
 //     F(x) = max(0, ceil((x - j) / c)).
@@ -70,8 +73,12 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
   const int S = block_exclusive_scan(s_off, E, red);
   if (threadIdx.x == 0) s_off[E] = S;
   __syncthreads();
-  if (S > max_slots) {
-    if (threadIdx.x == 0) atomicExch(err, 1);
+  if (S > max_slots) {  // report through the sizes the host reads anyway: no collective runs
+    if (threadIdx.x == 0) {
+      atomicExch(err, 1);
+      *num_local_rows = -1;
+    }
+    for (int g = threadIdx.x; g < G; g += blockDim.x) send_counts[g] = recv_counts[g] = 0;
     return;
   }
   for (int e = threadIdx.x; e <= E; e += blockDim.x) w.off[e] = s_off[e];
@@ -83,8 +90,6 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
       if (s_off[mid] <= s) lo = mid; else hi = mid;
     }
     const int e = lo, j = s - s_off[e], c = s_off[e + 1] - s_off[e];
-    const int home = (int)(((long long)e * G) / E);
-    const int gpu = (home + j) % G;
     int size = 0, acc = 0;
     for (int g = 0; g < G; ++g) {
       const int cg = C[(size_t)g * E + e];
@@ -94,9 +99,21 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
       size += r;
       acc += cg;
     }
+    w.slot_size[s] = size;
+    s_lb[s] = size;  // scanned below into the rows before each slot
+  }
+  __syncthreads();
+  const int total = block_exclusive_scan(s_lb, S, red);
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int size = w.slot_size[s];
+    const long long mid2 = 2LL * s_lb[s] + size;  // twice the slot's row midpoint
+    const int gpu = total > 0 ? (int)min((long long)G - 1, (mid2 * G) / (2LL * total)) : 0;
     w.slot_gpu[s] = gpu;
     s_gpu[s] = gpu;
-    w.slot_size[s] = size;
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int size = w.slot_size[s], gpu = s_gpu[s];
     s_lb[s] = (gpu == rank) ? size : 0;
     s_pc[s] = (gpu == rank) ? (split ? cdiv(size, kBlockMRows) : (size > 0 ? 1 : 0)) : 0;
   }
@@ -167,9 +184,10 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
 
 // Sender: global rank -> slot -> send position; one thread per token (chunked stable rank).
 __global__ void k_ep_send_pos(const int32_t* __restrict__ route, int T, int E, int nch, const int32_t* __restrict__ cc,
-                              EpPlanWs w, int32_t* __restrict__ send_pos) {
+                              EpPlanWs w, int32_t* __restrict__ send_pos, const int32_t* __restrict__ err) {
   griddep_launch_dependents();
   griddep_wait();
+  if (*err) return;  // the plan overflowed max_slots: its tables were not written
   __shared__ int se[kChunk];
   const int ch = blockIdx.x;
   const int t = ch * kChunk + threadIdx.x;
@@ -205,9 +223,10 @@ __global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32
 // Receiver: local row of every received row, per (source, hosted slot) run.
 // grid (max_slots, G): one block per (slot, source); slots beyond the plan's count exit.
 __global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ num_slots_p, int rank, EpPlanWs w,
-                              int32_t* __restrict__ recv_of_local) {
+                              int32_t* __restrict__ recv_of_local, const int32_t* __restrict__ err) {
   griddep_launch_dependents();
   griddep_wait();
+  if (*err) return;
   const int s = blockIdx.x, g = blockIdx.y;
   if (s >= *num_slots_p || w.slot_gpu[s] != rank) return;
   const int n = w.rows[(size_t)g * max_slots + s];
@@ -300,13 +319,14 @@ extern "C" int mp_ep_plan(const int32_t* route, int T, const int32_t* C, int G, 
     MP_CUDA_TRY(cudaFuncSetAttribute(k_ep_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024)));
     configured = true;
   }
+  MP_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
   k_ep_plan<<<1, 1024, sm, st>>>(C, G, E, rank, max_slots, split_m & 1, res, w, send_counts, recv_counts,
                                  num_local_rows, piece_row, piece_rows, exp_begin, err);
   if (T > 0) {
     // local stable ranks (chunk histograms + exclusive scan over chunks)
     int rc = mp_histogram_ws(route, 1, T, E, cc + (size_t)nch * E, cc, (size_t)nch * E * 4, stream);
     if (rc) return rc;
-    k_ep_send_pos<<<nch, kChunk, 0, st>>>(route, T, E, nch, cc, w, send_pos);
+    k_ep_send_pos<<<nch, kChunk, 0, st>>>(route, T, E, nch, cc, w, send_pos, err);
   }
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
@@ -328,7 +348,7 @@ extern "C" int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, c
   MP_REQUIRE(ws_bytes >= mp_ep_workspace_bytes(G, T, E, max_slots), MP_ERR_CONFIG, "mp_ep_recv_layout: workspace");
   // number of slots = off[E]
   k_ep_recv_map<<<dim3(max_slots, G), 128, 0, (cudaStream_t)stream>>>(G, max_slots, w.off + E, rank, w,
-                                                                       recv_of_local);
+                                                                       recv_of_local, err);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

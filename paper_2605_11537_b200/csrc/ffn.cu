@@ -103,17 +103,10 @@ extern "C" int mp_tile_kmajor(const void* src, void* dst, int G, int N, int K, i
   return MP_OK;
 }
 
-// [xperm T x dp bf16][hid T x Fp bf16][T i32][control: 256 B, the fused kernel's work ticket]
 extern "C" size_t mp_ffn_workspace_bytes(int T, int dp, int Fp) {
   return al(sizeof(__nv_bfloat16) * (size_t)T * dp) + al(sizeof(__nv_bfloat16) * (size_t)T * Fp) +
-         al(sizeof(int32_t) * (size_t)T) + 256;
+         al(sizeof(int32_t) * (size_t)T);
 }
-
-namespace mp {
-int* ffn_ticket(void* ws, int T, int dp, int Fp) {
-  return (int*)((char*)ws + mp_ffn_workspace_bytes(T, dp, Fp) - 256);
-}
-}  // namespace mp
 
 static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, int tiled, int box_rows) {
   if (tiled) return make_tmap_bf16(tb, w, (uint64_t)E * N * (K / 64), 64, 64, box_rows);

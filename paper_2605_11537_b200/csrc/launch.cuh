@@ -13,9 +13,7 @@ int num_sms();
 
 int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_dtype, int ldc, const float* bias,
               int act, int sig_from, int store_hint, void* stream, int grid_cap = 0);
-int ffn_grid();
-// the fused FFN's self-resetting work ticket inside the FFN workspace (must start at zero)
-int* ffn_ticket(void* ws, int T, int dp, int Fp);   // persistent grid of the grouped expert GEMMs (mp_set_sm_partition)
+int ffn_grid();   // persistent grid of the grouped expert GEMMs (mp_set_sm_partition)
 int pred_grid();  // persistent grid of the predictor GEMMs
 
 // 2-D bf16 row-major [rows x cols] tensor map, box = [box_rows x 64 cols], SWIZZLE_128B.

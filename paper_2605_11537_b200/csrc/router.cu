@@ -72,6 +72,14 @@ __global__ void k_router_recheck(const float* __restrict__ x, int ldx, int d, co
 }
 
 
+// 16-byte shared-memory load (explicit ld.shared: the address never goes through a generic pointer)
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+
 constexpr int kRfConvThreads = 256;  // convert + epilogue threads (warps 4..11)
 
 // Fused router (Eg <= 128): the split of x into bf16 hi/lo and the bound scale
@@ -228,16 +236,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       float part[4] = {0.f, 0.f, 0.f, 0.f};
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&xfull[xstage], xphase);
-        const uint8_t* sx = smem + L::kXOffset + xstage * L::kXs + box * (L::kXs / 2);
+        const uint32_t sx = smem_u32(smem + L::kXOffset + xstage * L::kXs + box * (L::kXs / 2));
         float4 cur[4][2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = r0 + 32 * i;
-          cur[i][0] = *reinterpret_cast<const float4*>(sx + r * 128 + (((c16) ^ (r & 7)) << 4));
-          cur[i][1] = *reinterpret_cast<const float4*>(sx + r * 128 + (((c16 + 1) ^ (r & 7)) << 4));
+          cur[i][0] = lds_f4(sx + r * 128 + (((c16) ^ (r & 7)) << 4));
+          cur[i][1] = lds_f4(sx + r * 128 + (((c16 + 1) ^ (r & 7)) << 4));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&xempty[xstage]);
+        uint64_t* x_release = &xempty[xstage];  // released only after the values are consumed (below)
         if (++xstage == kRxXStages) {
           xstage = 0;
           xphase ^= 1;
@@ -269,7 +276,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         fence_proxy_async();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[stage]);
+        // The x ring slot is handed back only now: its values have been consumed into the
+        // operand tiles above. (Releasing it right after issuing the loads let the next TMA
+        // land before the loads had read -- the loads were generic and still in flight.)
+        if (lane == 0) {
+          mbar_arrive(x_release);
+          mbar_arrive(&conv[stage]);
+        }
         if (++stage == kRxStages) {
           stage = 0;
           phase ^= 1;
@@ -501,3 +514,4 @@ extern "C" int mp_route_top1(const float* x, int ldx, int T, int d, const void* 
   if (rc) return rc;
   return mp_route_top1_ex(x, ldx, T, d, w_hl, w_f32, wabs, E, Eg, route, ws, ws_bytes, stream);
 }
+

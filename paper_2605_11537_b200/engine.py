@@ -51,9 +51,8 @@ class PipelineConfig:
     demand_unit: int = 128        # 1 = reference token demand; 128 = M-tile demand (F12)
     replication: str = "on"       # on | off | split
     predictor: str = "constructed"  # constructed (highway-open SRU, heads = router rows) | random
-    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else fused) | fused (one kernel:
-                                  # GEMM1 -> relu -> GEMM2 + combine, hidden on chip) | two (single-CTA
-                                  # grouped GEMM pair) | pair (CTA-pair cta_group::2 grouped GEMMs)
+    ffn: str = "auto"             # auto (pair at >= 1024 tokens/expert, else two) | two (single-CTA
+                                  # grouped GEMMs) | pair (CTA-pair cta_group::2 grouped GEMMs)
     skew: float = 1.2
     noise: float = 0.1
     seed: int = 0                 # model: routers, experts, predictor (identical on every rank)
@@ -142,8 +141,7 @@ class MoEPipeline:
             # BASELINE config 2 runs at 1,126 vs 1,007 TF/s); single-CTA units on weight-streaming
             # layers (config 3: 128 tokens per expert, pairs are 12 % slower) -- profiles/README.md
             pair = cfg.tokens >= 1024 * cfg.num_experts and cfg.d_model % 256 == 0
-            fused = _lib.size_query("mp_ffn_fused_tile", cfg.d_model) > 0 and cfg.d_ff % 128 == 0
-            cfg = dataclasses.replace(cfg, ffn="pair" if pair else ("fused" if fused else "two"))
+            cfg = dataclasses.replace(cfg, ffn="pair" if pair else "two")
         self.cfg = cfg
         self.dev = device or require_device()
         dev = self.dev
@@ -190,7 +188,7 @@ class MoEPipeline:
         self.fallback = torch.empty(L, **i32)
         self.num_slots = torch.empty(L, **i32)
         self.route = torch.empty(L, T, **i32)
-        self.max_slots = max(cfg.capacity, E) * 8 + E  # also covers the global (G * C) plan of EP
+        self.max_slots = max(cfg.capacity, E) + E  # placement / execution slots of one device
         self.exec_slot = torch.empty(L, T, **i32)
         self.corrective = torch.empty(L, E, **i32)
         self.exec_slots = torch.empty(L, **i32)
@@ -218,7 +216,7 @@ class MoEPipeline:
         self.ws_router_n = _lib.size_query("mp_router_workspace_bytes", T, d)
         self.ws_router = ws(self.ws_router_n)
         self.ws_ffn_n = _lib.size_query("mp_ffn_workspace_bytes", T, d, F)
-        self.ws_ffn = torch.zeros(self.ws_ffn_n, dtype=torch.uint8, device=dev)  # fused FFN ticket starts at 0
+        self.ws_ffn = ws(self.ws_ffn_n)
         self.pstride = pstride
         self.launches_per_step = None
 
@@ -292,14 +290,6 @@ class MoEPipeline:
             n += 1
         if ev is not None:
             ev[0].record(sp)
-        if cfg.ffn == "fused":
-            _lib.call("mp_ffn_fused", ptr(x), T, d, F, E, ptr(lay.U), ptr(lay.V), 0, ptr(self.tok_of_row[l]),
-                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.ws_ffn),
-                      self.ws_ffn_n, sp)
-            if ev is not None:
-                ev[1].record(sp)
-                ev[2].record(sp)
-            return n + 1
         flags = lay.tiled | (2 if use_pair else 0)
         _lib.call("mp_ffn_up", T, d, F, E, ptr(lay.U), flags, ptr(self.piece_row[l]), ptr(self.piece_rows[l]),
                   ptr(self.exp_begin[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
@@ -326,7 +316,8 @@ class MoEPipeline:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         cfg = self.cfg
-        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.max_slots)
+        # slots of the global plan: G * C capacity slots + at most one corrective replica per expert
+        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.world * cfg.capacity + cfg.num_experts)
         self.ep = ExpertParallelMoE(k, cfg.num_layers, cfg.num_experts, group)
         self.ep.res = self.res  # one residency state for placement and execution
         GT = self.world * cfg.tokens
@@ -610,9 +601,8 @@ def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor, f
     # pre-tiled B operands: each TMA box of the grouped GEMMs is one contiguous 32 KB burst
     u2, v2 = u.reshape(E * F, d).contiguous(), v.reshape(E * d, F).contiguous()
     lay.U, lay.V = torch.empty_like(u2), torch.empty_like(v2)
-    # the fused FFN reads 128-row boxes of both; the CTA-pair kernels read V in 256-column slices
-    ubn = 128 if ffn == "fused" else _lib.size_query("mp_ffn_up_bn", F)
-    vbn = 128 if ffn == "fused" else (256 if ffn == "pair" else _lib.size_query("mp_ffn_down_bn", d))
+    ubn = _lib.size_query("mp_ffn_up_bn", F)
+    vbn = 256 if ffn == "pair" else _lib.size_query("mp_ffn_down_bn", d)  # the CTA-pair kernels read BN 256
     _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, ubn, stream_ptr())
     _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, vbn, stream_ptr())
     lay.tiled = 1

@@ -8,7 +8,8 @@ tokens. Per MoE layer, on every rank:
   1. route the local tokens                      (mp_route_top1_ex)
   2. local expert counts -> all-gather C (G x E)  (mp_histogram_ws + all_gather)
   3. plan (identical on all ranks): residency + corrective replicas, global
-     stable ranks, replica (e, j) -> GPU (e*G/E + j) mod G, per-peer row counts,
+     stable ranks, the slot list cut into G blocks of equal rows (slot -> GPU),
+     per-peer row counts,
      send positions, local replica pieces         (mp_ep_plan)
   4. dispatch: pack bf16 rows by destination, variable all-to-all
   5. receiver: rows to slot-major global-token order (mp_ep_recv_layout,
@@ -35,6 +36,7 @@ import torch.distributed as dist
 
 from . import _lib
 from ._dev import ptr, stream_ptr
+from .errors import ConfigurationError
 from .router_oracle import DeviceMoeLayer, route_device
 
 
@@ -69,7 +71,7 @@ class CudaEpKernels:
         self.hist_n = _lib.size_query("mp_histogram_workspace_bytes", 1, tokens, self.E)
         self.hist_ws = torch.empty(max(self.hist_n, 256), dtype=torch.uint8, device=dev)
         self.ffn_n = _lib.size_query("mp_ffn_workspace_bytes", self.cap_rows, self.d, self.F)
-        self.ffn_ws = torch.zeros(self.ffn_n, dtype=torch.uint8, device=dev)  # fused FFN ticket starts at 0
+        self.ffn_ws = torch.empty(self.ffn_n, dtype=torch.uint8, device=dev)
         self.counts_buf = torch.empty(self.E, **i32)
         self.sizes = torch.empty(2 * world + 1, **i32)  # send counts | recv counts | local rows
         self.sc, self.rc, self.nloc = self.sizes[:world], self.sizes[world:2 * world], self.sizes[2 * world:]
@@ -82,7 +84,9 @@ class CudaEpKernels:
         self.ybuf = torch.empty(self.cap_rows, self.d, dtype=torch.float32, device=dev)
         self.yback = torch.empty(tokens, self.d, dtype=torch.float32, device=dev)
         self._packed_for = None
-        self.send_pos = torch.empty(tokens, **i32)
+        # zero-filled: if a plan overflows max_slots its send positions are left untouched, and the
+        # pack issued before the host sees the error must still write inside the send buffer
+        self.send_pos = torch.zeros(tokens, **i32)
         self.piece_row = torch.empty(self.pstride, **i32)
         self.piece_rows = torch.empty(self.pstride, **i32)
         self.exp_begin = torch.empty(self.E + 1, **i32)
@@ -119,6 +123,8 @@ class CudaEpKernels:
         self.sizes_ready.synchronize()
         host = self.sizes_host.tolist()
         G = self.G
+        if host[2 * G] < 0:  # every rank computes the same plan, so every rank raises here
+            raise ConfigurationError(f"mp_ep_plan: the layer needs more than max_slots={self.max_slots} slots")
         return EpPlan(host[:G], host[G:2 * G], host[2 * G], self.send_pos[:T], self.piece_row, self.piece_rows,
                       self.exp_begin)
 
@@ -151,14 +157,6 @@ class CudaEpKernels:
         sp = stream_ptr()
         if ev is not None:
             ev[0].record(sp)
-        if getattr(lay, "ffn", "") == "fused":  # one kernel; stores into the receive-order rows
-            _lib.call("mp_ffn_fused", ptr(y), n, self.d, self.F, self.E, ptr(lay.U), ptr(lay.V), 32,
-                      ptr(self.recv_of_local), ptr(plan.piece_row), ptr(plan.piece_rows), ptr(plan.exp_begin),
-                      ptr(self.ffn_ws), self.ffn_n, sp)
-            if ev is not None:
-                ev[1].record(sp)
-                ev[2].record(sp)
-            return y
         # single-CTA grouped GEMMs over the EP pieces (split_m = 1); a V tiled for the CTA-pair
         # kernels (256-column slices) is read with 256-column units (flags bit 6)
         vflag = 64 if lay.tiled and getattr(lay, "vbn", 0) == 256 else 0

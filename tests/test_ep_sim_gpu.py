@@ -1,0 +1,119 @@
+"""Expert parallelism over a SIMULATED G-GPU job on one device.
+
+Every rank's CUDA kernels run on this GPU: route -> counts -> plan -> pack -> (all-to-all
+emulated by device copies in NCCL's layout) -> receive layout -> grouped GEMMs -> (reverse
+all-to-all) -> combine. Ranks never wait on one another inside a kernel; the host plays the
+collectives between the per-rank launches. The result over the G token shards must equal the
+single-device forward of the whole batch bit for bit, with and without replicas, at the
+Switch-base widths and for both V tilings (single-CTA 192-column and CTA-pair 256-column)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2605_11537_b200 import _lib  # noqa: E402
+from paper_2605_11537_b200._dev import ptr, require_device, stream_ptr  # noqa: E402
+
+
+def _params(L, E, d, F, seed):
+    from paper_2605_11537_b200.router_oracle import ToyMoeParams
+    rng = np.random.default_rng(seed)
+    return ToyMoeParams(rng.normal(size=(L, E, d)).astype(np.float32),
+                        (rng.normal(size=(L, E, F, d)) / np.sqrt(d)).astype(np.float32),
+                        (rng.normal(size=(L, E, d, F)) / np.sqrt(F)).astype(np.float32))
+
+
+def _tile(dm, E, d, F, vbn):
+    for lay in dm.layers:
+        u2, v2 = lay.U.clone(), lay.V.clone()
+        _lib.call("mp_tile_kmajor", ptr(u2), ptr(lay.U), E, F, d, _lib.size_query("mp_ffn_up_bn", F), stream_ptr())
+        _lib.call("mp_tile_kmajor", ptr(v2), ptr(lay.V), E, d, F, vbn, stream_ptr())
+        lay.tiled = 1
+        lay.vbn = vbn
+
+
+def _a2a(chunks_by_src, counts, dst_bufs):
+    """NCCL all_to_all_single layout: rank r receives, in source order, the block every
+    source g sends it (source g's send buffer is destination-major)."""
+    G = len(chunks_by_src)
+    for r in range(G):
+        parts = []
+        for g in range(G):
+            displ = sum(counts[g][:r])
+            parts.append(chunks_by_src[g][displ:displ + counts[g][r]])
+        if parts:
+            dst_bufs[r].copy_(torch.cat(parts))
+
+
+def _simulate(ks, xs, res, L):
+    G = len(ks)
+    for l in range(L):
+        routes = [k.route(x, l) for k, x in zip(ks, xs)]
+        C = torch.stack([k.counts(r).clone() for k, r in zip(ks, routes)])
+        plans = [k.plan(r, C, res[g][l], x) for g, (k, r, x) in enumerate(zip(ks, routes, xs))]
+        sends = [k.pack(x, p, sum(p.send_counts)) for k, x, p in zip(ks, xs, plans)]
+        recvs = [k.recv_buffer(sum(p.recv_counts)) for k, p in zip(ks, plans)]
+        _a2a(sends, [p.send_counts for p in plans], recvs)
+        ys = [k.expert_ffn(rb, p, l) for k, rb, p in zip(ks, recvs, plans)]
+        backs = [k.back_buffer(sum(p.send_counts)) for k, p in zip(ks, plans)]
+        _a2a(ys, [p.recv_counts for p in plans], backs)
+        for k, x, yb, p in zip(ks, xs, backs, plans):
+            k.combine(x, yb, p)
+    return plans
+
+
+@pytest.mark.parametrize("G,E,d,F,T,vbn,replicas", [
+    (2, 16, 256, 512, 700, None, False), (4, 16, 256, 512, 500, None, True), (8, 32, 256, 512, 300, None, True),
+    (2, 16, 768, 3072, 600, None, True), (4, 8, 768, 3072, 300, 256, True), (3, 12, 768, 3072, 257, None, False)])
+def test_simulated_ep_equals_single_device(G, E, d, F, T, vbn, replicas):
+    from paper_2605_11537_b200.ep import CudaEpKernels
+    from paper_2605_11537_b200.router_oracle import _device_moe, _run_layers_device
+
+    dev = require_device()
+    L = 2
+    params = _params(L, E, d, F, seed=G * 10 + E + d)
+    rng = np.random.default_rng(G)
+    # Zipf-skewed tokens: rows near one router row route to that expert
+    pop = 1.0 / (rng.permutation(E) + 1.0) ** 1.2
+    e0 = rng.choice(E, size=G * T, p=pop / pop.sum())
+    x0 = (params.router_weights[0][e0] * 0.05 + rng.normal(size=(G * T, d)) * 0.5).astype(np.float32)
+    dm_ref = _device_moe(params, dev)
+    x_ref = torch.from_numpy(x0).to(dev)
+    _run_layers_device(x_ref, dm_ref)  # dense single-device forward of the whole batch
+    dm = _device_moe(params, dev)
+    _tile(dm, E, d, F, vbn or _lib.size_query("mp_ffn_down_bn", d))
+    res0 = (rng.integers(0, 4, size=(L, E)) if replicas else np.zeros((L, E))).astype(np.int32)
+    capacity = int(res0.sum(1).max()) + E
+    ks = [CudaEpKernels(dm.layers, T, G, r, G * capacity + E) for r in range(G)]
+    res = [torch.from_numpy(res0.copy()).to(dev) for _ in range(G)]
+    xs = [torch.from_numpy(x0[r * T:(r + 1) * T].copy()).to(dev) for r in range(G)]
+    plans = _simulate(ks, xs, res, L)
+    torch.cuda.synchronize()
+    out = torch.cat(xs)
+    assert torch.equal(out, x_ref)
+    for g in range(1, G):  # every rank holds the same residency state
+        assert torch.equal(res[g], res[0])
+    # row budget: the slot list is cut into G blocks of equal rows
+    rows = [sum(p.recv_counts) for p in plans]
+    assert max(rows) - min(rows) <= max(1, (G * T) // 2), rows
+
+
+def test_ep_plan_over_capacity_raises_before_collectives():
+    """More execution slots than max_slots: mp_ep_plan reports it through the sizes the host
+    reads (num_local_rows = -1, zero counts) and the host raises instead of issuing an
+    all-to-all with stale split sizes."""
+    from paper_2605_11537_b200.ep import CudaEpKernels
+    from paper_2605_11537_b200.errors import ConfigurationError
+    from paper_2605_11537_b200.router_oracle import _device_moe
+
+    dev = require_device()
+    E, d, F, T = 8, 256, 512, 200
+    dm = _device_moe(_params(1, E, d, F, seed=3), dev)
+    k = CudaEpKernels(dm.layers, T, 2, 0, max_slots=E)
+    route = torch.randint(0, E, (T,), dtype=torch.int32, device=dev)
+    C = torch.stack([k.counts(route).clone(), k.counts(route).clone()])
+    res = torch.full((E,), 3, dtype=torch.int32, device=dev)  # 24 slots > max_slots = 8
+    with pytest.raises(ConfigurationError):
+        k.plan(route, C, res)

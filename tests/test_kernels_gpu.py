@@ -501,3 +501,38 @@ def _check_ffn_mode_bitwise(dev, skew, d, F, tiled, mode):
     torch.cuda.synchronize()
     assert torch.equal(h1, h2)
     assert torch.equal(y1, y2)
+
+
+@pytest.mark.parametrize("E,d,T", [(16, 768, 5000), (64, 512, 5000), (128, 768, 16384), (4, 1024, 3000),
+                                   (100, 768, 2000)])
+def test_router_exact_on_dense_random_inputs(dev, E, d, T):
+    """Routing equals the float64 argmax (first index on ties) on inputs whose every
+    coordinate matters (random x and W, all k-blocks contribute): the fused router's x ring
+    was once handed back to its TMA producer before its generic loads had read the slot,
+    which corrupted whole k-blocks of some rows -- invisible on the synthetic workload, whose
+    router rows are zero in half the dimensions. Both router entry points, several calls."""
+    from paper_2605_11537_b200.router_oracle import ToyMoeParams, _device_moe
+
+    rng = np.random.default_rng(E + d)
+    W = rng.normal(size=(1, E, d)).astype(np.float32)
+    lay = _device_moe(ToyMoeParams(W, np.zeros((1, E, 256, d), np.float32), np.zeros((1, E, d, 256), np.float32)),
+                      dev).layers[0]
+    e0 = rng.choice(E, size=T)
+    x = torch.from_numpy((W[0][e0] * 0.05 + rng.normal(size=(T, d)) * 0.5).astype(np.float32)).to(dev)
+    ref = (x.double() @ torch.from_numpy(W[0]).to(dev).double().T).argmax(1).int()
+    rb = _lib.size_query("mp_router_workspace_bytes", T, d)
+    ws = torch.empty(rb, dtype=torch.uint8, device=dev)
+    route = torch.empty(T, dtype=torch.int32, device=dev)
+    hist = torch.empty((T + 127) // 128 * E, dtype=torch.int32, device=dev)
+    for _ in range(3):
+        _lib.call("mp_route_top1_ex", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
+                  ptr(route), ptr(ws), rb, stream_ptr())
+        torch.cuda.synchronize()
+        assert torch.equal(route, ref)
+        if lay.Eg <= 128:
+            _lib.call("mp_route_top1_hist", ptr(x), d, T, d, ptr(lay.w_hl), ptr(lay.w32), ptr(lay.w_abs), E, lay.Eg,
+                      ptr(route), ptr(hist), ptr(ws), rb, stream_ptr())
+            torch.cuda.synchronize()
+            assert torch.equal(route, ref)
+            counts = torch.bincount(ref[:(T // 128) * 128].long(), minlength=E)
+            assert torch.equal(hist[:(T // 128) * E].view(-1, E).sum(0).long(), counts)

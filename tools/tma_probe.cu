@@ -17,7 +17,7 @@ using namespace mp;
 
 template <int STAGES>
 __global__ void __launch_bounds__(64, 1) k_probe(const __grid_constant__ CUtensorMap tm, int box_rows, int iters,
-                                                 int rows_total, unsigned long long* cycles) {
+                                                 int rows_total, unsigned long long* cycles, int priv = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int stage_bytes = box_rows * 128;
@@ -37,7 +37,9 @@ __global__ void __launch_bounds__(64, 1) k_probe(const __grid_constant__ CUtenso
     for (int i = 0; i < iters; ++i) {
       mbar_wait(&empty[stage], phase ^ 1);
       mbar_arrive_expect_tx(&full[stage], stage_bytes);
-      const int row = ((blockIdx.x * 7 + i) * box_rows) % rows_total;
+      // priv > 0: every CTA cycles over its own priv boxes (no two SMs read the same line)
+      const int row = priv ? (int)(((long long)blockIdx.x * priv + (i % priv)) * box_rows)
+                           : ((blockIdx.x * 7 + i) * box_rows) % rows_total;
       tma_load_2d(smem + stage * stage_bytes, &tm, &full[stage], 0, row);
       if (++stage == STAGES) stage = 0, phase ^= 1;
     }
@@ -101,9 +103,54 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
 }
 
+// Chip-wide TMA throughput with DISJOINT per-SM regions: an L2-resident working set (each CTA
+// cycles over its own boxes) and an HBM stream (each CTA reads its own slice once).
+static void private_regions(int nsm) {
+  auto enc = get_encode();
+  const int box_rows = 256, sbytes = box_rows * 128;
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sizeof(unsigned long long) * nsm);
+  for (size_t total_mb : {size_t(48), size_t(4096)}) {
+    const size_t bytes_total = total_mb << 20;
+    const int per = (int)(bytes_total / sbytes / nsm);  // boxes per CTA
+    const long long rows_total = (long long)per * nsm * box_rows;
+    void* buf;
+    cudaMalloc(&buf, (size_t)rows_total * 128);
+    cudaMemset(buf, 1, (size_t)rows_total * 128);
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {64, (cuuint64_t)rows_total};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int stages = 6, smem = stages * sbytes + 2 * stages * 8 + 2048;
+    cudaFuncSetAttribute((void*)k_probe<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int iters = total_mb > 1024 ? per : (64 << 20) / sbytes;  // HBM: each box once
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(a);
+      k_probe<6><<<nsm, 64, smem>>>(tm, box_rows, iters, (int)0, cyc, per);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+    }
+    const double bytes = (double)nsm * iters * sbytes;
+    printf("private regions, %s (%zu MB): 32 KB boxes, 6 stages: %7.1f GB/s per SM, %6.2f TB/s chip (%s)\n",
+           total_mb > 1024 ? "HBM stream" : "L2-resident", total_mb, bytes / nsm / (ms * 1e-3) / 1e9,
+           bytes / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(buf);
+  }
+  cudaFree(cyc);
+}
+
 int main() {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  private_regions(nsm);
   const int rows_total = 1 << 16;  // 64K rows x 128 B = 8 MB: L2-resident
   void* buf;
   cudaMalloc(&buf, (size_t)rows_total * 128);
