@@ -53,6 +53,8 @@ def parse_args():
     p.add_argument("--capacity", type=int, default=296)
     p.add_argument("--demand-unit", type=int, default=128)
     p.add_argument("--predictor", choices=["constructed", "random"], default="constructed")
+    p.add_argument("--physical-replicas", action="store_true",
+                   help="every replica slot owns a copy of its expert's weights (K9 weight pools)")
     p.add_argument("--batches", type=int, default=4, help="distinct synthetic batches cycled over the steps")
     p.add_argument("--cpu-sample-tokens", type=int, default=2048)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -451,6 +453,7 @@ def run_ours(args):
     cfg = PipelineConfig(num_layers=args.layers, num_experts=args.experts, tokens=args.tokens,
                          capacity=args.capacity, demand_unit=args.demand_unit, replication=args.replication,
                          predictor=args.predictor, ffn=args.ffn, seed=args.seed, skew=args.skew,
+                         physical_replicas=args.physical_replicas,
                          batch_seed=1_000_003 * (rank + 1) + args.seed)
     pipe = MoEPipeline(cfg)
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
@@ -706,6 +709,27 @@ def run_baselines(args, pipe, x, batches, ms_on, moe_only):
                                "headline_over_this": ms / ms_on}
     pipe.sru.heads.copy_(heads_keep)
     pipe.res.zero_()
+    if not base_cfg.physical_replicas and base_cfg.ffn == "two":
+        # K9: the same plan with every replica slot owning a physical copy of its expert's weights
+        # (per-layer pools, LOAD / REPLICATE / OFFLOAD copies on the device) -- on one GPU the
+        # copies cost HBM bandwidth the aliased replicas do not: each replica streams its own copy
+        pipe.cfg = dataclasses.replace(base_cfg, physical_replicas=True)
+        pipe._init_replica_pools()
+        time_graph_steps(pipe, x, batches, 2)  # cold pools filled (first loads) outside the timing
+        before = pipe.replica_stats()
+        ms = time_graph_steps(pipe, x, batches, steps)
+        after = pipe.replica_stats()
+        n = steps + 5  # time_graph_steps also runs 3 eager warm-up steps and 2 untimed replays
+        per = {k: (after[k] - before[k]) / n for k in ("loads", "replicates", "offloads", "bytes")}
+        out["physical_replicas"] = {"value": T / (ms * 1e-3), "ms_per_step": ms, "headline_over_this": ms / ms_on,
+                                    "copies_per_step": {k: per[k] for k in ("loads", "replicates", "offloads")},
+                                    "copy_bytes_per_step": per["bytes"], "pool_overflow": after["overflow"],
+                                    "pool_gb": sum(u.numel() + v.numel() for u, v in zip(pipe.pool_u, pipe.pool_v))
+                                    * 2 / 1e9}
+        pipe.cfg = base_cfg
+        del pipe.pool_u, pipe.pool_v, pipe.pool_state, pipe.piece_wbase
+        torch.cuda.empty_cache()
+        pipe.res.zero_()
     ms_hf = hf_loop_ms_per_step(pipe, batches, 3)
     out["hf_loop"] = {"value": T / (ms_hf * 1e-3), "ms_per_step": ms_hf, "steps": 3,
                       "what": "MoE layers only (router + per-expert mask/gather/2 matmuls/scatter, bf16 cuBLAS)"}

@@ -272,6 +272,34 @@ MP_API int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, in
 MP_API int mp_ffn_down_bn(int dp);
 /* column-tile width (and mp_tile_kmajor BN) of the pre-tiled expert U weights for GEMM1 */
 MP_API int mp_ffn_up_bn(int Fp);
+/* K9 physical replicas (north_star; src/placement.py:143-160 LOAD / REPLICATE / OFFLOAD, PAPER.md
+ * :172-178). A layer's pool of P expert-sized weight slots (pre-tiled U and V of one expert each)
+ * materialises the residency state res[e] (replicas per expert, after placement and the
+ * execution map): state = mp_pool_state_bytes(E, R, P) device bytes, R = max replicas of one
+ * expert, set up by mp_pool_init. mp_pool_update diffs res against the materialised counts:
+ * surplus ordinals are OFFLOADed (slots freed), missing ones get a slot and a copy job --
+ * REPLICATE from the expert's ordinal-0 copy, or LOAD from the master weights when the expert
+ * had no copy; mp_replica_copy runs the jobs (expert_bytes per tensor), mp_piece_pool maps every
+ * GEMM piece (mp_exec_map outputs) to the weight slot of its replica, and mp_ffn_up_pool /
+ * mp_ffn_down_pool run the grouped GEMMs on the pool (same flags as mp_ffn_up/down, single-CTA
+ * pre-tiled only). mp_pool_stats copies {loads, replicates, offloads since init, overflow flag}
+ * into 4 device ints. All device-side (no host sync). */
+MP_API size_t mp_pool_state_bytes(int E, int R, int P);
+MP_API int mp_pool_init(int E, int R, int P, void* state, void* stream);
+MP_API int mp_pool_update(const int32_t* res, int E, int R, int P, void* state, void* stream);
+MP_API int mp_replica_copy(const void* master_u, const void* master_v, void* pool_u, void* pool_v, size_t expert_bytes,
+                           int P, const void* state, int E, int R, void* stream);
+MP_API int mp_piece_pool(const int32_t* piece_row, const int32_t* exp_begin, int E, const int32_t* tok_of_row,
+                         const int32_t* token_to_slot, const void* state, int R, int P, int32_t* piece_wbase,
+                         int max_pieces, void* stream);
+MP_API int mp_pool_stats(const void* state, int E, int R, int P, int32_t* out4, void* stream);
+MP_API int mp_ffn_up_pool(int T, int dp, int Fp, int E, int W, const void* pool_u, int flags, const int32_t* piece_row,
+                          const int32_t* piece_rows, const int32_t* exp_begin, const int32_t* piece_wbase, void* ws,
+                          size_t ws_bytes, void* stream);
+MP_API int mp_ffn_down_pool(float* y, int T, int dp, int Fp, int E, int W, const void* pool_v, int flags,
+                            const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                            const int32_t* exp_begin, const int32_t* piece_wbase, void* ws, size_t ws_bytes,
+                            void* stream);
 /* Diagnostics: per-CTA %globaltimer start / end (ns) of the last grouped-GEMM launch
  * (host arrays of n <= 1024). */
 MP_API int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1, int n);
@@ -307,10 +335,6 @@ MP_API int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, const
 MP_API int mp_gather_rows_bf16(const void* buf, int n, int d, const int32_t* idx, void* out, void* stream);
 MP_API int mp_ep_combine(float* x, int T, int d, const float* yback, const int32_t* send_pos, void* stream);
 
-/* ------------------------------------------------------------------ K9
- * Physical replica copy (LOAD/REPLICATE events, src/placement.py:149-156):
- * dst <- src, `bytes` long, device-to-device (or peer) on `stream`. */
-MP_API int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream);
 
 /* Whole-step CUDA graphs (capture on `stream`, replay) and timing events that remain
  * valid inside a captured graph (recorded as external event nodes). Host plumbing. */

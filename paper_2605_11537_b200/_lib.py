@@ -79,9 +79,16 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_down": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down_bn": (_I, [_I]),
     "mp_ffn_up_bn": (_I, [_I]),
+    "mp_pool_state_bytes": (_Z, [_I, _I, _I]),
+    "mp_pool_init": (_I, [_I, _I, _I, _P, _P]),
+    "mp_pool_update": (_I, [_P, _I, _I, _I, _P, _P]),
+    "mp_replica_copy": (_I, [_P, _P, _P, _P, _Z, _I, _P, _I, _I, _P]),
+    "mp_piece_pool": (_I, [_P, _P, _I, _P, _P, _P, _I, _I, _P, _I, _P]),
+    "mp_pool_stats": (_I, [_P, _I, _I, _I, _P, _P]),
+    "mp_ffn_up_pool": (_I, [_I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
+    "mp_ffn_down_pool": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_debug_cta_times": (_I, [_P, _P, _I]),
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),
-    "mp_replica_copy": (_I, [_P, _P, _Z, _P]),
     "mp_ep_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "mp_ep_plan": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ep_pack": (_I, [_P, _I, _I, _P, _P, _P]),

@@ -1,5 +1,5 @@
 // C-ABI plumbing: error strings, device info, TMA map encoding, the generic
-// dense tcgen05 GEMM entry point and the replica copy.
+// dense tcgen05 GEMM entry point.
 #include <vector>
 #include <stdarg.h>
 #include <string.h>
@@ -193,11 +193,6 @@ extern "C" int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream) {
   const int grid = (int)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
   if (n4) MP_CUDA_TRY(launch_pdl(k_f32_to_bf16, dim3(grid), dim3(256), 0, (cudaStream_t)stream, (const float4*)x, (uint2*)y, n4));
   MP_CUDA_TRY(cudaGetLastError());
-  return MP_OK;
-}
-
-extern "C" int mp_replica_copy(void* dst, const void* src, size_t bytes, void* stream) {
-  MP_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
   return MP_OK;
 }
 

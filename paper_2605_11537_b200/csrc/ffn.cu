@@ -118,13 +118,13 @@ static int tmap_b(CUtensorMap* tb, const void* w, int E, int N, int K, int bn, i
 //        instead of the residual add, bit 6 = V tiled with 256-column slices (the pair layout)
 static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* piece_row, const int32_t* piece_rows,
                   const int32_t* exp_begin, const __nv_bfloat16* xperm, __nv_bfloat16* hid, int flags,
-                  cudaStream_t st) {
+                  cudaStream_t st, const int32_t* piece_wbase = nullptr, int W = 0) {
   // GEMM1: hid = relu(xperm . U_e^T)   [rows x Fp], BN = 256, H written by TMA bulk stores
   // with an L2 evict_last hint (GEMM2 re-reads it right away: GEMM1 151 -> 142 us)
   const int tiled = flags & 1, pair = (flags >> 1) & 1;
   CUtensorMap ta, tb, tc;
   int rc = make_tmap_bf16(&ta, xperm, T, dp, dp, kBlockM);
-  if (!rc) rc = tmap_b(&tb, u, E, Fp, dp, 256, tiled, pair ? 128 : 256);
+  if (!rc) rc = tmap_b(&tb, u, piece_wbase ? W : E, Fp, dp, 256, tiled, pair ? 128 : 256);
   if (!rc) rc = make_tmap_bf16_store(&tc, hid, T, Fp, Fp);
   if (rc) return rc;
   EpiStoreBf16Tma et{hid, Fp, nullptr, 1, 0, 1};
@@ -133,19 +133,21 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
     return launch_gemm2<256, 6>(ta, tb, s, et, num_sms() & ~1, st, &tc);
   }
   SegSched s{piece_row, piece_rows, exp_begin, E, Fp / 256, 256, Fp, dp / 64, tiled, 0};
+  s.piece_wbase = piece_wbase;
   return launch_gemm<256, 4>(ta, tb, s, et, ffn_grid(), st, &tc);
 }
 
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
-                    const __nv_bfloat16* hid, int flags, cudaStream_t st) {
+                    const __nv_bfloat16* hid, int flags, cudaStream_t st, const int32_t* piece_wbase = nullptr,
+                    int W = 0) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
   const int tiled = flags & 1, pair = (flags >> 1) & 1;
   const int bn = (pair || (flags & 64)) ? 256 : mp_ffn_down_bn(dp);
   MP_REQUIRE(dp % bn == 0, MP_ERR_CONFIG, "ffn_down: dp=%d not a multiple of the V tile %d", dp, bn);
   CUtensorMap ta, tb;
   int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
-  if (!rc) rc = tmap_b(&tb, v, E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
+  if (!rc) rc = tmap_b(&tb, v, piece_wbase ? W : E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
   if (rc) return rc;
   EpiScatterAdd e{y, dp, tok_of_row, (flags >> 5) & 1};
   if (pair) {
@@ -154,6 +156,7 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
   }
   // units walked backwards: the H rows GEMM1 wrote last are still in L2
   SegSched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled, 1};
+  s.piece_wbase = piece_wbase;
   if (bn == 256) return launch_gemm<256, 4>(ta, tb, s, e, ffn_grid(), st);
   if (bn == 192) return launch_gemm<192, 5>(ta, tb, s, e, ffn_grid(), st);
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, ffn_grid(), st);
@@ -192,6 +195,29 @@ extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v
   FFN_CHECKS();
   return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags,
                   (cudaStream_t)stream);
+}
+
+// Physical replicas: B operand rows of piece p come from weight slot piece_wbase[p] of a pool of W
+// expert-sized slots (same pre-tiled layout), single-CTA kernels only.
+extern "C" int mp_ffn_up_pool(int T, int dp, int Fp, int E, int W, const void* pool_u, int flags,
+                              const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
+                              const int32_t* piece_wbase, void* ws, size_t ws_bytes, void* stream) {
+  FFN_CHECKS();
+  MP_REQUIRE((flags & 1) && !(flags & 2) && piece_wbase != nullptr && W >= 1, MP_ERR_CONFIG,
+             "mp_ffn_up_pool: needs pre-tiled single-CTA weights and a piece -> slot table");
+  return ffn_up(T, dp, Fp, E, pool_u, piece_row, piece_rows, exp_begin, xperm, hid, flags, (cudaStream_t)stream,
+                piece_wbase, W);
+}
+
+extern "C" int mp_ffn_down_pool(float* y, int T, int dp, int Fp, int E, int W, const void* pool_v, int flags,
+                                const int32_t* tok_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                                const int32_t* exp_begin, const int32_t* piece_wbase, void* ws, size_t ws_bytes,
+                                void* stream) {
+  FFN_CHECKS();
+  MP_REQUIRE((flags & 1) && !(flags & 2) && piece_wbase != nullptr && W >= 1, MP_ERR_CONFIG,
+             "mp_ffn_down_pool: needs pre-tiled single-CTA weights and a piece -> slot table");
+  return ffn_down(y, T, dp, Fp, E, pool_v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags,
+                  (cudaStream_t)stream, piece_wbase, W);
 }
 
 extern "C" int mp_moe_ffn(const float* x, float* y, int T, int dp, int Fp, int E, const void* u, const void* v,

@@ -362,6 +362,7 @@ struct SegSched {
   int reverse;  // 1: walk the unit list backwards (GEMM2 consumes the hidden rows GEMM1 wrote LAST first,
                 //    while they are still in L2)
   int prep_cap = 768;  // <= GemmSmem<BN, STAGES>::kPrepInts of the launch
+  const int32_t* piece_wbase = nullptr;  // physical replicas: weight slot of each piece (else its expert)
   __device__ void prepare(int* tab) {
     if (E + 1 > prep_cap) return;  // table of GemmSmem::kPrepInts ints; else exp_begin stays global
     for (int e = threadIdx.x; e <= E; e += blockDim.x) tab[e] = exp_begin[e];
@@ -380,7 +381,8 @@ struct SegSched {
     const int local = u - b * n_tiles;
     const int nt = local / cnt;
     const int p = b + (local - nt * cnt);
-    const int brow = b_tiled ? (lo * n_tiles + nt) * kb * bn : lo * n_per_expert + nt * bn;
+    const int wb = piece_wbase ? __ldg(&piece_wbase[p]) : lo;
+    const int brow = b_tiled ? (wb * n_tiles + nt) * kb * bn : wb * n_per_expert + nt * bn;
     return Unit{__ldg(&piece_row[p]), __ldg(&piece_rows[p]), brow, nt * bn};
   }
   __device__ int num_kb() const { return kb; }

@@ -55,6 +55,9 @@ class PipelineConfig:
                                   # grouped GEMMs) | pair (CTA-pair cta_group::2 grouped GEMMs)
     skew: float = 1.2
     noise: float = 0.1
+    physical_replicas: bool = False  # every replica slot owns a copy of its expert's weights (K9):
+                                  # LOAD / REPLICATE / OFFLOAD copy weights in a per-layer pool; off:
+                                  # replicas on one GPU alias the expert's single copy
     seed: int = 0                 # model: routers, experts, predictor (identical on every rank)
     batch_seed: int | None = None  # synthetic batches (per rank under EP); None: derived from seed
 
@@ -219,6 +222,42 @@ class MoEPipeline:
         self.ws_ffn = ws(self.ws_ffn_n)
         self.pstride = pstride
         self.launches_per_step = None
+        if cfg.physical_replicas:
+            self._init_replica_pools()
+
+    def _init_replica_pools(self) -> None:
+        """Per-layer pools of P = max_slots expert-sized weight slots (K9, csrc/replica.cu)."""
+        from .errors import ConfigurationError
+
+        cfg = self.cfg
+        if cfg.ffn != "two":
+            raise ConfigurationError("physical replicas run on the single-CTA grouped GEMMs (ffn='two')")
+        E, d, F = cfg.num_experts, self.dp, self.Fp
+        self.pool_P = self.max_slots
+        self.pool_R = self.max_slots
+        nb = _lib.size_query("mp_pool_state_bytes", E, self.pool_R, self.pool_P)
+        self.pool_state, self.pool_u, self.pool_v = [], [], []
+        sp = stream_ptr()
+        for l in range(cfg.num_layers):
+            st = torch.empty(nb, dtype=torch.uint8, device=self.dev)
+            _lib.call("mp_pool_init", E, self.pool_R, self.pool_P, ptr(st), sp)
+            self.pool_state.append(st)
+            self.pool_u.append(torch.empty(self.pool_P * F, d, dtype=torch.bfloat16, device=self.dev))
+            self.pool_v.append(torch.empty(self.pool_P * d, F, dtype=torch.bfloat16, device=self.dev))
+        self.piece_wbase = torch.zeros(cfg.num_layers, self.pstride, dtype=torch.int32, device=self.dev)
+        self.pool_stats = torch.zeros(cfg.num_layers, 4, dtype=torch.int32, device=self.dev)
+
+    def replica_stats(self) -> dict:
+        """Copies since the pools were created: {loads, replicates, offloads, bytes, overflow}."""
+        if not self.cfg.physical_replicas:
+            return {}
+        sp = stream_ptr()
+        for l in range(self.cfg.num_layers):
+            _lib.call("mp_pool_stats", ptr(self.pool_state[l]), self.cfg.num_experts, self.pool_R, self.pool_P,
+                      ptr(self.pool_stats[l]), sp)
+        s = self.pool_stats.sum(0).tolist()
+        return {"loads": s[0], "replicates": s[1], "offloads": s[2],
+                "bytes": (s[0] + s[1]) * self.expert_weight_bytes(), "overflow": bool(s[3])}
 
     # ------------------------------------------------------------------ pieces of a step
     def predict(self, x: torch.Tensor, sp: int) -> int:
@@ -288,6 +327,29 @@ class MoEPipeline:
             _lib.call("mp_ffn_gather", ptr(x), T, d, F, E, ptr(self.tok_of_row[l]), ptr(self.ws_ffn), self.ws_ffn_n,
                       sp)
             n += 1
+        if cfg.physical_replicas:  # materialise the layer's residency in the weight pool, then run on it
+            E_, R, P = cfg.num_experts, self.pool_R, self.pool_P
+            st = self.pool_state[l]
+            _lib.call("mp_pool_update", ptr(self.res[l]), E_, R, P, ptr(st), sp)
+            _lib.call("mp_replica_copy", ptr(lay.U), ptr(lay.V), ptr(self.pool_u[l]), ptr(self.pool_v[l]),
+                      2 * d * F, P, ptr(st), E_, R, sp)
+            _lib.call("mp_piece_pool", ptr(self.piece_row[l]), ptr(self.exp_begin[l]), E_, ptr(self.tok_of_row[l]),
+                      ptr(self.exec_slot[l]), ptr(st), R, P, ptr(self.piece_wbase[l]), self.pstride, sp)
+            n += 4  # pool update | copies (two passes) | piece -> slot
+            if ev is not None:
+                ev[0].record(sp)
+            flags = lay.tiled
+            _lib.call("mp_ffn_up_pool", T, d, F, E, P, ptr(self.pool_u[l]), flags, ptr(self.piece_row[l]),
+                      ptr(self.piece_rows[l]), ptr(self.exp_begin[l]), ptr(self.piece_wbase[l]), ptr(self.ws_ffn),
+                      self.ws_ffn_n, sp)
+            if ev is not None:
+                ev[1].record(sp)
+            _lib.call("mp_ffn_down_pool", ptr(x), T, d, F, E, P, ptr(self.pool_v[l]), flags, ptr(self.tok_of_row[l]),
+                      ptr(self.piece_row[l]), ptr(self.piece_rows[l]), ptr(self.exp_begin[l]),
+                      ptr(self.piece_wbase[l]), ptr(self.ws_ffn), self.ws_ffn_n, sp)
+            if ev is not None:
+                ev[2].record(sp)
+            return n + 2
         if ev is not None:
             ev[0].record(sp)
         flags = lay.tiled | (2 if use_pair else 0)
