@@ -59,6 +59,7 @@ def parse_args():
     p.add_argument("--cpu-sample-tokens", type=int, default=2048)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-e2e-api", action="store_true", help="skip timing the numpy drop-in API chain")
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--skew", type=float, default=1.2, help="Zipf skew of the synthetic routing")
     p.add_argument("--no-graph", action="store_true", help="launch kernels one by one instead of a CUDA graph")
@@ -633,6 +634,8 @@ def run_ours(args):
     }
 
     result["config"]["ffn_kernels"] = pipe.cfg.ffn  # resolved from --ffn auto
+    if not ep:
+        result["cost_model"] = cost_model_rows(pipe, [up[l] + down[l] for l in range(L)])
     if not args.no_checks and not ep:
         result["checks"].update(float_checks(pipe, last, seed=args.seed))
     if not args.no_e2e:
@@ -642,6 +645,8 @@ def run_ours(args):
         del graph, graph_ev
         result["baselines"] = run_baselines(args, pipe, x, batches, ms_step, moe_only)
         result["grouped_gemm_config2"] = config2_gemm(args, peaks)
+    if not args.no_e2e_api and not ep:
+        result["e2e_api"] = run_e2e_api(args, pipe, batches)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(args)
         result["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
@@ -652,6 +657,32 @@ def run_ours(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def cost_model_rows(pipe, layer_ms):
+    """the reference's per-batch Metrics (src/simulator.py:210-235) of the last
+    step, from the device counts of its transfer events and replica-slot queues
+    (MoEPipeline.metrics, csrc/counts.cu): once in cost-model units (CostModel() defaults) and
+    once with the measured expert-GEMM time of each layer as its makespan (ms)."""
+    from dataclasses import asdict
+
+    from paper_2605_11537_b200.simulator import CostModel, metrics_row
+
+    m_model, counts = pipe.metrics(CostModel())
+    m_meas, _ = pipe.metrics(CostModel(), layer_latency=layer_ms)
+    E, C = pipe.cfg.num_experts, pipe.cfg.capacity
+    return {
+        "events_per_step": {"loads": int(counts[:, 0].sum()), "replicates": int(counts[:, 1].sum()),
+                            "offloads": int(counts[:, 2].sum())},
+        "longest_queue_per_layer": counts[:, 3].tolist(),
+        "slots_per_layer": counts[:, 4].tolist(),
+        "metrics_cost_model": asdict(m_model),
+        "metrics_measured_ms": asdict(m_meas),
+        "report_row": metrics_row(0, "replicated" if pipe.cfg.replication != "off" else "distinct-only", E, C,
+                                  m_meas),
+        "how": "mp_layer_counts over the step's device arrays (token events, offloads, corrective loads, "
+               "token->slot map); layer makespan = cost model, or the measured GEMM1 + GEMM2 ms",
+    }
 
 
 def weights_hash_equal(pipe, world):
@@ -743,6 +774,58 @@ def run_baselines(args, pipe, x, batches, ms_on, moe_only):
                                 "on_over_hf_loop_moe": ms_hf / ms_on,
                                 "target": ">= 3x the non-replicated GPU baseline (north star)"}
     return out
+
+
+def run_e2e_api(args, pipe, batches, steps=3):
+    """The drop-in API a moesim user calls, numpy in and numpy out, on the same model and batches:
+    predict_batch -> plan_layers_with_fallback -> apply_batch -> execution_map -> moe_forward
+    (reference call chain src/simulator.py:127-208 + src/router_oracle.py:145-178). Every call
+    runs its kernels eagerly (no graph) and round-trips its results through host memory, as the
+    reference API returns numpy objects. The output is compared bit for bit with the engine's
+    step on the same batch (replica layouts do not change the bits)."""
+    import time
+
+    import numpy as np
+    import torch
+
+    from paper_2605_11537_b200.placement import DeviceState, apply_batch, execution_map
+    from paper_2605_11537_b200.planner import plan_layers_with_fallback
+    from paper_2605_11537_b200.predictor import predict_batch
+    from paper_2605_11537_b200.router_oracle import moe_forward
+    from paper_2605_11537_b200.workload import Batch
+
+    t0 = time.perf_counter()
+    params, sru = pipe.toy_params(), pipe.sru_params()
+    host = [Batch(k, b[0].cpu().numpy(), b[2].cpu().numpy().astype(np.int64)) for k, b in enumerate(batches)]
+    setup_s = time.perf_counter() - t0
+    C = pipe.cfg.capacity
+    state = DeviceState(pipe.cfg.num_layers, C)
+
+    def one(batch):
+        table = predict_batch(batch, sru)
+        plan = plan_layers_with_fallback(table, C, distinct_only=pipe.cfg.replication == "off")
+        apply_batch(state, table, plan)
+        _, ex, _ = execution_map(state, batch.oracle_routing)
+        return moe_forward(batch.embeddings, params, ex)
+
+    one(host[0])  # device copies of the weights are built and cached on first use
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = None
+    for k in range(steps):
+        out = one(host[k % len(host)])
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / steps
+    last = (steps - 1) % len(host)
+    x = batches[last][0].clone()
+    pipe.step(x)
+    same = bool(np.array_equal(out, x.cpu().numpy()))
+    T, d = pipe.cfg.tokens, pipe.cfg.d_model
+    return {"value": T / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": T * d * 4 + pipe.cfg.num_layers * T * 8,
+            "d2h_bytes_per_step": T * d * 4, "output_equals_engine_bitwise": same, "setup_s": setup_s,
+            "api": "predict_batch -> plan_layers_with_fallback -> apply_batch -> execution_map -> moe_forward "
+                   "(numpy in / out, eager launches, wall clock)"}
 
 
 def run_e2e(args, pipe, batches, world):

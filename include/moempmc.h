@@ -114,6 +114,18 @@ MP_API int mp_exec_map_hist(const int32_t* route, int T, int E, int max_slots, i
                             int32_t* tok_of_row, int32_t* piece_row, int32_t* piece_rows, int32_t* exp_begin,
                             const float* x, int d, void* xperm, void* ws, size_t ws_bytes, void* stream);
 
+/* Per-layer cost-model inputs of one batch (src/simulator.py:210-235 over simulate_layer
+ * :62-81 and the TransferLog, src/placement.py:35-63), counted on the device. One block per
+ * layer; for layer l, counts[l*5 + {0..4}] = {LOAD events (token_event kind LOAD +
+ * sum_e corrective[l,e]), REPLICATE events, OFFLOAD events (sum_e offloads[l,e]), longest
+ * slot queue (max_s #{t : token_to_slot[l,t] == s}), num_slots[l]}. token_event (L x T,
+ * mp_place), offloads (L x E_off, mp_place) and corrective (L x E_corr, mp_exec_map) may be
+ * NULL (counted as 0). *err |= 1 when a token maps outside [0, num_slots[l]).
+ * max_slots <= 49152. */
+MP_API int mp_layer_counts(const int32_t* token_event, const int32_t* offloads, const int32_t* corrective,
+                           const int32_t* token_to_slot, const int32_t* num_slots, int L, int T, int E_off,
+                           int E_corr, int max_slots, int32_t* counts, int32_t* err, void* stream);
+
 /* Replica segments from an explicit token -> slot map (a reference Placement,
  * src/router_oracle.py:64-74, as consumed by moe_forward :160-175): rows are
  * grouped by slot (stable in token order); slot_expert[s] must be

@@ -88,6 +88,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_up_pool": (_I, [_I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_ffn_down_pool": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_debug_cta_times": (_I, [_P, _P, _I]),
+    "mp_layer_counts": (_I, [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "mp_tile_kmajor": (_I, [_P, _P, _I, _I, _I, _I, _P]),
     "mp_ep_workspace_bytes": (_Z, [_I, _I, _I, _I]),
     "mp_ep_plan": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _Z, _P]),

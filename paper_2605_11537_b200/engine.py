@@ -493,6 +493,31 @@ class MoEPipeline:
         v = lay.V.view(lay.E, d // lay.vbn, F // 64, lay.vbn, 64)[e].permute(0, 2, 1, 3).reshape(d, F)
         return u, v
 
+    def toy_params(self):
+        """The engine's MoE weights as the reference's ToyMoeParams (float32 numpy, reference
+        layouts; bf16 values, so the drop-in API re-quantises them losslessly)."""
+        import numpy as np
+
+        from .router_oracle import ToyMoeParams
+
+        cfg, L, E, d, F = self.cfg, self.cfg.num_layers, self.cfg.num_experts, self.dp, self.Fp
+        router = np.stack([self.wl.router(l).cpu().numpy() for l in range(L)])
+        u = np.empty((L, E, F, d), dtype=np.float32)
+        v = np.empty((L, E, d, F), dtype=np.float32)
+        for l in range(L):
+            lay = self.layers[l]
+            u[l] = lay.U.view(E, F // lay.ubn, d // 64, lay.ubn, 64).permute(0, 1, 3, 2, 4).reshape(E, F, d) \
+                .float().cpu().numpy()
+            v[l] = lay.V.view(E, d // lay.vbn, F // 64, lay.vbn, 64).permute(0, 1, 3, 2, 4).reshape(E, d, F) \
+                .float().cpu().numpy()
+        return ToyMoeParams(router, u, v)
+
+    def sru_params(self):
+        """The engine's predictor as the reference's SruParams (float64 host copies)."""
+        from .predictor import SruLayerParams, SruParams
+
+        return SruParams(layers=[SruLayerParams(*lay) for lay in self.sru_host], heads=self.heads_host)
+
     # ------------------------------------------------------------------ CUDA graph
     def capture(self, x: torch.Tensor, events=None) -> "StepGraph":
         """Capture one step over the fixed residual-stream buffer ``x`` (run ``step`` once
@@ -534,6 +559,24 @@ class MoEPipeline:
     def touched_experts(self) -> torch.Tensor:
         """(L,) experts that received tokens in the last step (device)."""
         return (self.exp_begin[:, 1:] > self.exp_begin[:, :-1]).sum(dim=1)
+
+    def layer_counts(self):
+        """(L, 5) device counts of the last step -- {LOAD (placement + corrective), REPLICATE,
+        OFFLOAD events, longest replica-slot queue, slots} (csrc/counts.cu)."""
+        from .simulator import layer_counts
+
+        return layer_counts(self.exec_slot, self.exec_slots, self.max_slots, token_event=self.pred_event,
+                            offloads=self.offloads, corrective=self.corrective)
+
+    def metrics(self, cost=None, layer_latency=None):
+        """The reference's per-batch ``Metrics`` (src/simulator.py:210-235) of the last step from
+        its device counts; ``layer_latency`` (per MoE layer, e.g. measured ms) replaces the
+        cost model's layer makespans. Returns (Metrics, counts)."""
+        from .simulator import CostModel, metrics_from_counts
+
+        counts = self.layer_counts()
+        acc = float((self.assign == self.route).float().mean().item())
+        return metrics_from_counts(counts, self.cfg.tokens, cost or CostModel(), acc, layer_latency), counts
 
 
 class OverlappedPipeline:

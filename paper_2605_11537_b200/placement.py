@@ -70,6 +70,8 @@ class DeviceState:
         self.num_layers = check_positive("num_layers", num_layers)
         self.capacity = check_positive("capacity", capacity)
         self._resident: list[dict[int, list[int]]] = [{} for _ in range(num_layers)]
+        self.last_place_device = None  # device arrays of the last apply_batch / execution_map
+        self.last_exec_device = None   # (cost-model counts, simulator.py)
 
     def resident(self, layer: int) -> dict[int, list[int]]:
         return self._resident[layer]
@@ -154,6 +156,8 @@ def _place_layers(state: DeviceState, rows: np.ndarray, layers: list[int], caps_
     ws = WORKSPACE.get("place", nbytes, dev)
     _lib.call("mp_place", ptr(a_d), L, T, E, ptr(caps_d), int(plan_capacity), int(state.capacity), ptr(res_d),
               ptr(tts), ptr(tev), ptr(offl), ptr(fb), ptr(ns), ptr(ws), nbytes, stream_ptr())
+    # device-side results of the last placement, for the cost-model counts (simulator.py)
+    state.last_place_device = {"layers": list(layers), "token_event": tev, "offloads": offl, "E": E, "T": T}
     tts, tev, offl, fb, res_new = (t.cpu().numpy() for t in (tts, tev, offl, fb, res_d))
     out = []
     for i, l in enumerate(layers):
@@ -241,6 +245,8 @@ def execution_map(state: DeviceState, true_routing):
     ws = WORKSPACE.get("exec", nbytes, dev)
     _lib.call("mp_exec_map", ptr(a_d), L, T, E, max_slots, 0, ptr(res_d), ptr(tts), ptr(corr), ptr(ns), None,
               ptr(tor), ptr(prow), ptr(prows), ptr(eb), ptr(ws), nbytes, stream_ptr())
+    state.last_exec_device = {"token_to_slot": tts, "corrective": corr, "num_slots": ns, "E": E, "T": T,
+                              "max_slots": max_slots}
     tts, corr, res_new = tts.cpu().numpy(), corr.cpu().numpy(), res_d.cpu().numpy()
     layers = []
     for l in range(L):

@@ -44,7 +44,7 @@ from moesim import (  # noqa: E402
 )
 from moesim.predictor import SruLayerParams, SruParams, init_params  # noqa: E402
 from moesim.router_oracle import random_params  # noqa: E402
-from moesim.simulator import BatchRunner  # noqa: E402
+from moesim.simulator import BatchRunner, CostModel, simulate_strategy  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 
@@ -168,6 +168,47 @@ def exec_cases():
                 "fallback_layers": list(outcome.log.fallback_layers),
             })
         out.append({"L": L, "E": E, "T": T, "capacity": C, "batches": batches})
+    return out
+
+
+def metrics_cases():
+    """simulate_strategy (src/simulator.py:268-273) per strategy, predictor and cost model:
+    per-batch Metrics of the reference, with the hash tables it predicted (the GPU predictor
+    is bf16, so the parity test feeds these tables and checks the cost model on its own)."""
+    from dataclasses import asdict
+
+    rng = np.random.default_rng(55)
+    costs = [(1.0, 10.0, 2.0, 5.0), (1.0, 1.0, 0.1, 0.1), (0.5, 3.0, 0.0, 7.25)]
+    out = []
+    for trial in range(60):
+        L = int(rng.integers(1, 4))
+        E = int(rng.integers(2, 10))
+        d = int(rng.integers(4, 12))
+        T = int(rng.integers(4, 48))
+        shape = ModelShape(L, E, d, T)
+        hot = trial % 3 == 2
+        if hot:
+            nh = int(rng.integers(1, E + 1))
+            trace = generate_hot_trace(shape, num_batches=4, num_hot=nh, seed=trial)
+            gen = {"kind": "hot", "num_hot": nh}
+        else:
+            sk = float(rng.uniform(0, 2))
+            trace = generate_trace(shape, num_batches=4, skew=sk, seed=trial)
+            gen = {"kind": "zipf", "skew": sk}
+        C = int(rng.integers(max(1, E - 2), E + 25))
+        strategy = ("resident-all", "distinct-only", "replicated")[trial % 3 if trial % 5 else 2]
+        cost = costs[trial % len(costs)]
+        use_sru = trial % 2 == 1
+        params = init_params(L, E, d, num_sru_layers=2, seed=trial) if use_sru else "oracle"
+        runner = BatchRunner(trace, strategy, C, params=params, cost=CostModel(*cost))
+        batches = []
+        for batch in trace.batches:
+            outcome = runner.run_batch(batch)
+            batches.append({"table": outcome.table.assignment.tolist(), "metrics": asdict(outcome.metrics)})
+        res = simulate_strategy(trace, strategy, C, params=params, cost=CostModel(*cost))
+        assert [asdict(m) for m in res.per_batch] == [b["metrics"] for b in batches]
+        out.append({"L": L, "E": E, "d": d, "T": T, "seed": trial, "gen": gen, "capacity": C, "strategy": strategy,
+                    "cost": cost, "sru": use_sru, "batches": batches, "aggregate": asdict(res.aggregate)})
     return out
 
 
@@ -317,11 +358,15 @@ def main():
     if "--only-train" in sys.argv:
         training_cases()
         return
+    if "--only-metrics" in sys.argv:
+        (OUT / "metrics.json").write_text(json.dumps(metrics_cases()))
+        return
     io_files()
     training_cases()
     (OUT / "planner.json").write_text(json.dumps(planner_cases()))
     (OUT / "placement.json").write_text(json.dumps(placement_cases()))
     (OUT / "exec.json").write_text(json.dumps(exec_cases()))
+    (OUT / "metrics.json").write_text(json.dumps(metrics_cases()))
     arrays, meta = sru_cases()
     np.savez_compressed(OUT / "sru.npz", **arrays)
     marrays, mmeta, cfg1 = moe_cases()

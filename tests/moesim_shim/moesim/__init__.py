@@ -10,9 +10,11 @@ import numpy as np
 
 from oracle import moesim_oracle as _O
 from paper_2605_11537_b200.errors import (  # noqa: F401
+    AggregationError,
     ConfigurationError,
     DeviceError,
     InfeasibleCapacityError,
+    MetricError,
     MoesimError,
     NumericError,
     PlacementError,
@@ -42,6 +44,15 @@ from paper_2605_11537_b200.router_oracle import (  # noqa: F401
     moe_forward,
     oracle_route_batch,
     route_top1,
+)
+from paper_2605_11537_b200.pipeline import PipelineConfig, mode_equivalence_check, run_pipeline  # noqa: F401
+from paper_2605_11537_b200.simulator import (  # noqa: F401
+    BatchRunner,
+    CostModel,
+    Metrics,
+    simulate_layer,
+    simulate_strategy,
+    utilization,
 )
 from paper_2605_11537_b200.training import TrainingResult, train_predictor  # noqa: F401
 from paper_2605_11537_b200.workload import Batch, ModelShape, RoutingTrace  # noqa: F401

@@ -133,3 +133,30 @@ def test_step_graph_counts_its_kernels_and_replays_the_step(replication, ffn, E,
     assert g.launches == g.issued, (g.launches, g.issued)
     assert g.launches > 0
     assert torch.equal(x, x_eager)
+
+
+def test_overlapped_pipeline_equals_sequential():
+    """The two-stream schedule (predictor of batch i+1 on its own stream while batch i is planned,
+    placed and forwarded; engine.OverlappedPipeline) gives the sequential schedule's bits: the
+    analogue of the reference's mode_equivalence_check (src/pipeline.py:227-245) on the device path."""
+    from paper_2605_11537_b200.engine import MoEPipeline, OverlappedPipeline, PipelineConfig
+
+    cfg = PipelineConfig(num_layers=3, num_experts=32, d_model=256, d_ff=512, tokens=4096, sru_layers=2,
+                         capacity=64, predictor="random", seed=11)
+    seq, ovl = MoEPipeline(cfg), MoEPipeline(cfg)
+    batches = [seq.wl.batch(cfg.tokens)[0] for _ in range(4)]
+    s = torch.cuda.Stream()
+    outs, res = [], []
+    with torch.cuda.stream(s):
+        for b in batches:
+            x = b.clone()
+            seq.step(x)
+            outs.append(x.clone())
+            res.append(seq.res.clone())
+    torch.cuda.synchronize()
+    ov = OverlappedPipeline(ovl)
+    ov.run(batches, 4)
+    torch.cuda.synchronize()
+    assert torch.equal(ov.xbuf[0], outs[2]) and torch.equal(ov.xbuf[1], outs[3])
+    assert torch.equal(ovl.res, res[3])
+    assert torch.equal(ov.assign[1], seq.assign)  # batch 3's predicted table

@@ -9,7 +9,7 @@ ROOT=$(cd "$(dirname "$0")/.." && pwd)
 DIR=$ROOT/reftests_scratch
 if [ "${1:-run}" = stage ]; then
   rm -rf "$DIR" && mkdir -p "$DIR"
-  for f in test_planner test_placement test_predictor test_router_oracle; do
+  for f in test_planner test_placement test_predictor test_router_oracle test_simulator test_pipeline; do
     cp /root/reference/pkg/tests/$f.py "$DIR/"
   done
   cp "$ROOT/tests/moesim_shim/conftest_ref.py" "$DIR/conftest.py"
