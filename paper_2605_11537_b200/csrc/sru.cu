@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
   griddep_wait();
   __shared__ float sA[kSpWarps][128], sB[kSpWarps][128];
   __shared__ float sCin[128];
+  __shared__ float sLA[128], sLB[128];  // look-back: the low half-window's composed map
   __shared__ int s_ticket, s_lo, s_found;
   const int nstr = d / 128 + (d % 128 != 0);
   if (threadIdx.x == 0) s_ticket = atomicAdd(&flags[nstr * nblk], 1);
@@ -348,10 +349,13 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
       agg[(size_t)me * 256 + c] = BA;
       agg[(size_t)me * 256 + 128 + c] = BB;
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // the release below is cumulative over the block's writes ordered by the barrier
     if (threadIdx.x == 0) sp_st_release(&flags[me], 1);
+    // Look back in windows of 32 predecessors: warp 0 waits for their flags; then two threads
+    // per channel load their 16 maps of the window at once (one L2 round trip per window)
+    // and compose them; the high half (closer to this block) is applied first.
     float MA = 1.f, MB = 0.f;  // composition of the maps of the blocks walked so far
+    const int ch = threadIdx.x & 127, hh = threadIdx.x >> 7;
     int base = blk - 1;
     for (;;) {
       if (w == 0) {
@@ -367,27 +371,38 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
       }
       __syncthreads();
       const int lo = s_lo, found = s_found;
-      if (c < 128) {
-        const int stop = found ? lo + 1 : lo;
-        for (int j = base; j >= stop; j -= 8) {  // 8 independent loads in flight
-          float ra[8], rb[8];
+      const int stop = found ? lo + 1 : lo;
+      const int jhi = base - 16 * hh;  // this thread's entries: jhi, jhi - 1, ..., jhi - 15 (>= stop)
+      float ra[16], rb[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (j - i >= stop) {
-              const size_t o = (size_t)(str * nblk + j - i) * 256 + c;
-              ra[i] = __ldcg(&agg[o]);
-              rb[i] = __ldcg(&agg[o + 128]);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (j - i >= stop) {  // M <- M o map(j - i)
-              MB = fmaf(MA, rb[i], MB);
-              MA *= ra[i];
-            }
-          }
+      for (int i = 0; i < 16; ++i) {
+        if (jhi - i >= stop) {
+          const size_t o = (size_t)(str * nblk + jhi - i) * 256 + ch;
+          ra[i] = __ldcg(&agg[o]);
+          rb[i] = __ldcg(&agg[o + 128]);
         }
-        if (found) cin = fmaf(MA, __ldcg(&incl[(size_t)(str * nblk + lo) * 128 + c]), MB);
+      }
+      const float ci = (found && hh == 0) ? __ldcg(&incl[(size_t)(str * nblk + lo) * 128 + ch]) : 0.f;
+      float HA = 1.f, HB = 0.f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (jhi - i >= stop) {  // H <- H o map(jhi - i)
+          HB = fmaf(HA, rb[i], HB);
+          HA *= ra[i];
+        }
+      }
+      if (hh == 1) {
+        sLA[ch] = HA;
+        sLB[ch] = HB;
+      }
+      __syncthreads();
+      if (hh == 0) {
+        MB = fmaf(MA, HB, MB);  // M <- M o high half
+        MA *= HA;
+        const float LA = sLA[ch], LB = sLB[ch];
+        MB = fmaf(MA, LB, MB);  // M <- M o low half
+        MA *= LA;
+        if (found) cin = fmaf(MA, ci, MB);
       }
       if (found) break;
       base = lo - 1;
@@ -399,7 +414,6 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
     incl[(size_t)me * 128 + c] = fmaf(BA, cin, BB);
     sCin[c] = cin;
   }
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) sp_st_release(&flags[me], 2);
   if (!act || t0 >= T) return;
@@ -634,3 +648,4 @@ extern "C" int mp_heads_argmax(const void* h_bf16, const void* heads, int T, int
   if (bn == 128) return launch_gemm<128, 6>(ta, tb, s, e, grid, st);
   return launch_gemm<64, 8>(ta, tb, s, e, grid, st);
 }
+
