@@ -246,6 +246,12 @@ MP_API int mp_train_ce(const double* logits, const int64_t* labels, int S, int T
                        double* dlogits, double* row_loss, void* stream);
 MP_API int mp_train_sum(const double* in, int n, double* out, void* stream);
 MP_API int mp_train_axpy(double* y, const double* x, size_t n, double alpha, void* stream);
+/* Float64 GEMM of the trainer's dense products (the reference's numpy float64 matmuls,
+ * src/predictor.py:238-334): C[MxN] = op(A) op(B) + beta C, row-major with leading dimensions
+ * lda / ldb / ldc; op(A) = A (ta = 0, M x K) or A^T (ta = 1, A stored K x M); op(B) = B
+ * (tb = 0, K x N) or B^T (tb = 1, B stored N x K). */
+MP_API int mp_dgemm(int ta, int tb, int M, int N, int K, const double* A, int lda, const double* B, int ldb,
+                    double beta, double* C, int ldc, void* stream);
 MP_API int mp_train_nonfinite(const double* x, size_t n, int32_t* flag, void* stream);
 
 /* ------------------------------------------------------------------ K6 gather + K7 + K8

@@ -59,6 +59,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_train_ce": (_I, [_P, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "mp_train_sum": (_I, [_P, _I, _P, _P]),
     "mp_train_axpy": (_I, [_P, _P, _Z, _D, _P]),
+    "mp_dgemm": (_I, [_I, _I, _I, _I, _I, _P, _I, _P, _I, _D, _P, _I, _P]),
     "mp_train_nonfinite": (_I, [_P, _Z, _P, _P]),
     "mp_sru_scan_total": (_I, [_I, _I, _P, _P, _Z, _P]),
     "mp_sru_fold_carry": (_I, [_P, _I, _I, _P, _P, _P]),

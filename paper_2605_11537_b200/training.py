@@ -8,7 +8,8 @@ the epoch on divergence, ``ConfigurationError`` on bad arguments. Float64 like t
 reference. The recurrences (forward with caches, back-propagation through time of the
 cell state), the softmax cross-entropy, the reductions and the SGD update run in
 libmoempmc (csrc/train.cu, no FMA contraction so the cell updates round like the
-reference's numpy expressions); the dense products are float64 library GEMMs.
+reference's numpy expressions); the dense products are the library's own float64 GEMM
+(``mp_dgemm``, csrc/dgemm.cu).
 Parameters stay on the device for the whole run; the loss of every step is read back
 (the reference checks it for finiteness per step, src/predictor.py:364-367).
 """
@@ -57,6 +58,20 @@ def _axpy(y: torch.Tensor, x: torch.Tensor, alpha: float, sp: int) -> None:
     _lib.call("mp_train_axpy", ptr(y), ptr(x), y.numel(), float(alpha), sp)
 
 
+def _mm(a: torch.Tensor, b: torch.Tensor, ta: bool = False, tb: bool = False, out: torch.Tensor | None = None,
+        accumulate: bool = False) -> torch.Tensor:
+    """op(a) @ op(b) in float64 through mp_dgemm (op = transpose when ta / tb); with
+    ``accumulate`` the product is added to ``out``."""
+    a, b = a.contiguous(), b.contiguous()
+    M, K = (a.shape[1], a.shape[0]) if ta else a.shape
+    N = b.shape[0] if tb else b.shape[1]
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.float64, device=a.device)
+    _lib.call("mp_dgemm", int(ta), int(tb), M, N, K, ptr(a), a.shape[1], ptr(b), b.shape[1],
+              1.0 if accumulate else 0.0, ptr(out), N, stream_ptr())
+    return out
+
+
 def _loss_and_grads_dev(p: _DevParams, x: torch.Tensor, labels: torch.Tensor):
     """x (S, T, d) float64, labels (S, L, T) int64 on the device -> (loss, grads as _DevParams-like)."""
     sp = stream_ptr()
@@ -68,9 +83,9 @@ def _loss_and_grads_dev(p: _DevParams, x: torch.Tensor, labels: torch.Tensor):
     h = x
     for lay in p.layers:  # forward with caches (src/predictor.py:238-254)
         xf = h.reshape(N, d)
-        u = xf @ lay["w"].T
-        fm = xf @ lay["w_f"].T
-        rm = xf @ lay["w_r"].T
+        u = _mm(xf, lay["w"], tb=True)
+        fm = _mm(xf, lay["w_f"], tb=True)
+        rm = _mm(xf, lay["w_r"], tb=True)
         f, r, c, g, hn = (torch.empty(S, T, d, **f64) for _ in range(5))
         _lib.call("mp_sru_train_fwd", ptr(u), ptr(fm), ptr(rm), ptr(lay["b_f"]), ptr(lay["b_r"]), ptr(h), S, T, d,
                   ptr(f), ptr(r), ptr(c), ptr(g), ptr(hn), sp)
@@ -83,11 +98,11 @@ def _loss_and_grads_dev(p: _DevParams, x: torch.Tensor, labels: torch.Tensor):
     row_loss = torch.empty(N, **f64)
     lsum = torch.empty(L, **f64)
     for l in range(L):  # heads: softmax cross-entropy (src/predictor.py:310-326)
-        z = hf @ p.heads[l].T
+        z = _mm(hf, p.heads[l], tb=True)
         _lib.call("mp_train_ce", ptr(z), ptr(labels), S, T, L, l, E, ptr(dz), ptr(row_loss), sp)
         _lib.call("mp_train_sum", ptr(row_loss), N, ptr(lsum[l:l + 1]), sp)
-        head_grads[l] = dz.T @ hf
-        _axpy(dh, dz @ p.heads[l], 1.0, sp)
+        _mm(dz, hf, ta=True, out=head_grads[l])
+        _mm(dz, p.heads[l], out=dh, accumulate=True)
     grads = []
     bsf, bsr = torch.empty(S, d, **f64), torch.empty(S, d, **f64)
     for lay, (xc, u, f, r, c, g) in zip(reversed(p.layers), reversed(caches)):  # BPTT (src/predictor.py:257-294)
@@ -95,14 +110,15 @@ def _loss_and_grads_dev(p: _DevParams, x: torch.Tensor, labels: torch.Tensor):
         _lib.call("mp_sru_train_bwd", ptr(dh), ptr(xc), ptr(u), ptr(f), ptr(r), ptr(c), ptr(g), S, T, d, ptr(du),
                   ptr(dfp), ptr(drp), ptr(dho), ptr(bsf), ptr(bsr), sp)
         xf = xc.reshape(N, d)
-        gl = {"w": du.reshape(N, d).T @ xf, "w_f": dfp.reshape(N, d).T @ xf, "w_r": drp.reshape(N, d).T @ xf,
+        gl = {"w": _mm(du.reshape(N, d), xf, ta=True), "w_f": _mm(dfp.reshape(N, d), xf, ta=True),
+              "w_r": _mm(drp.reshape(N, d), xf, ta=True),
               "b_f": torch.empty(d, **f64), "b_r": torch.empty(d, **f64)}
         _lib.call("mp_train_colsum", ptr(bsf), S, d, ptr(gl["b_f"]), sp)
         _lib.call("mp_train_colsum", ptr(bsr), S, d, ptr(gl["b_r"]), sp)
         dho = dho.reshape(N, d)
-        _axpy(dho, du.reshape(N, d) @ lay["w"], 1.0, sp)
-        _axpy(dho, dfp.reshape(N, d) @ lay["w_f"], 1.0, sp)
-        _axpy(dho, drp.reshape(N, d) @ lay["w_r"], 1.0, sp)
+        _mm(du.reshape(N, d), lay["w"], out=dho, accumulate=True)
+        _mm(dfp.reshape(N, d), lay["w_f"], out=dho, accumulate=True)
+        _mm(drp.reshape(N, d), lay["w_r"], out=dho, accumulate=True)
         dh = dho
         grads.append(gl)
     grads.reverse()

@@ -81,3 +81,23 @@ def test_degenerate_skew_reaches_high_accuracy():
     res = train_predictor(RoutingTrace(shape, bs[:32]), epochs=80, learning_rate=0.001, seed=0, num_sru_layers=2)
     scores = [evaluate_accuracy(predict_batch(b, res.params), b.oracle_routing) for b in bs[32:]]
     assert float(np.mean(scores)) >= 0.99
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_dgemm_matches_float64_reference(ta, tb):
+    """mp_dgemm (the trainer's float64 products) vs a float64 matmul, ragged sizes, accumulate."""
+    import torch
+
+    from paper_2605_11537_b200.training import _mm
+
+    g = torch.Generator().manual_seed(7 + 2 * ta + tb)
+    for M, N, K in ((1, 1, 1), (70, 33, 129), (128, 64, 512), (5, 200, 3), (300, 17, 0)):
+        a = torch.randn((K, M) if ta else (M, K), generator=g, dtype=torch.float64)
+        b = torch.randn((N, K) if tb else (K, N), generator=g, dtype=torch.float64)
+        ref = (a.T if ta else a) @ (b.T if tb else b)
+        got = _mm(a.cuda(), b.cuda(), ta=bool(ta), tb=bool(tb)).cpu()
+        assert torch.allclose(got, ref, rtol=1e-12, atol=1e-12 * max(1, K))
+        c0 = torch.randn(M, N, generator=g, dtype=torch.float64)
+        out = c0.cuda()
+        _mm(a.cuda(), b.cuda(), ta=bool(ta), tb=bool(tb), out=out, accumulate=True)
+        assert torch.allclose(out.cpu(), ref + c0, rtol=1e-12, atol=1e-12 * max(1, K))
