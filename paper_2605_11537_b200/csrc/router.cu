@@ -80,7 +80,10 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
   return v;
 }
 
-constexpr int kRfConvThreads = 256;  // convert + epilogue threads (warps 4..11)
+constexpr int kRfConvThreads = 512;  // convert + epilogue threads (warps 4..19): the split-bf16
+                                      // conversion is latency bound, 16 warps keep it under the MMA
+constexpr int kRfRows = 128 / (kRfConvThreads / 8);  // tile rows per converting thread
+constexpr int kRouterThreads = 128 + kRfConvThreads;
 
 // Fused router (Eg <= 128): the split of x into bf16 hi/lo and the bound scale
 // sum_k |x_k| * wabs_k are computed INSIDE the GEMM. A producer warp (warp 3) streams x
@@ -92,24 +95,24 @@ constexpr int kRfConvThreads = 256;  // convert + epilogue threads (warps 4..11)
 // with B = [w_hi ; w_lo] stacked as 2Eg rows of one tile; logit = acc[e] + acc[Eg + e].
 // Roles: warp 0 TMA (B), warp 3 TMA (x), warp 1 MMA, warp 2 TMEM, warps 4..11 convert +
 // epilogue. The operand ring is 2 deep.
-constexpr int kRxStages = 2;
-constexpr int kRxXStages = 3;
+constexpr int kRxStages = 3;   // B (router weight) ring
+constexpr int kRxXStages = 3;  // x ring; each stage is converted IN PLACE into the A operand tiles
 template <int EG>
 struct RxSmem {
   static constexpr int kB = 2 * EG * 128;
   static constexpr int kA = 128 * 128;
-  static constexpr int kStage = kB + 2 * kA;
-  static constexpr int kXs = 128 * 64 * 4;  // one x k-block: 128 rows x 64 fp32 as two 16 KB boxes
-  static constexpr int kXOffset = kRxStages * kStage;
+  static constexpr int kXs = 128 * 64 * 4;  // one x k-block: 128 rows x 64 fp32 as two 16 KB boxes = [hi | lo]
+  static constexpr int kXOffset = kRxStages * kB;
   static constexpr int kBarOffset = kXOffset + kRxXStages * kXs;
-  // full[S], conv[S], empty[S], xfull[X], xempty[X], tfull, tempty
-  static constexpr int kXbOffset = kBarOffset + (3 * kRxStages + 2 * kRxXStages + 2) * 8 + 8;
+  // bfull[S], bempty[S], xfull[X], conv[X], xempty[X], tfull, tempty
+  static constexpr int kXbOffset = kBarOffset + (2 * kRxStages + 3 * kRxXStages + 2) * 8 + 8;
   static constexpr int kHistOffset = kXbOffset + 128 * 4;  // EG ints: the tile's expert histogram
-  static constexpr int kBytes = kHistOffset + EG * 4 + 1024;
+  static constexpr int kTopOffset = kHistOffset + EG * 4;  // per column group: best, second (float), best index
+  static constexpr int kBytes = kTopOffset + 3 * (EG / 32) * 128 * 4 + 1024;
 };
 
 template <int EG>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kRouterThreads, 1)
     k_router_fused_tx(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX, int T, int d,
                       const float* __restrict__ wabs, int E, int32_t* __restrict__ route, float eps,
                       int32_t* __restrict__ count, int32_t* __restrict__ list,
@@ -119,11 +122,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   using L = RxSmem<EG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
-  uint64_t* conv = full + kRxStages;
-  uint64_t* empty = conv + kRxStages;
-  uint64_t* xfull = empty + kRxStages;
-  uint64_t* xempty = xfull + kRxXStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);  // B stage landed
+  uint64_t* empty = full + kRxStages;                                     // B stage consumed by the MMA
+  uint64_t* xfull = empty + kRxStages;                                    // x stage landed
+  uint64_t* conv = xfull + kRxXStages;                                    // x stage converted to hi | lo
+  uint64_t* xempty = conv + kRxXStages;                                   // hi | lo consumed by the MMA
   uint64_t* tfull = xempty + kRxXStages;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
@@ -137,15 +140,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch(&tmX);
     for (int s = 0; s < kRxStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], kRfConvThreads / 32);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < kRxXStages; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], kRfConvThreads / 32);
+      mbar_init(&conv[s], kRfConvThreads / 32);
+      mbar_init(&xempty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, 4 * (EG / 32));  // every TMEM-reading epilogue warp
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 2 * EG < 32 ? 32 : 2 * EG);
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sb = smem + stage * L::kStage;
+          uint8_t* sb = smem + stage * L::kB;
           mbar_arrive_expect_tx(&full[stage], L::kB);
           tma_load_2d(sb, &tmB, &full[stage], kb * 64, 0);
           tma_load_2d(sb + EG * 128, &tmB, &full[stage], d + kb * 64, 0);
@@ -193,27 +196,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       constexpr uint32_t id_all = idesc_bf16_f32(kBlockM, 2 * EG);
       constexpr uint32_t id_hi = idesc_bf16_f32(kBlockM, EG);
-      uint32_t stage = 0, phase = 0, tile = 0;
+      uint32_t stage = 0, phase = 0, xstage = 0, xphase = 0, tile = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
         mbar_wait(tempty, (tile & 1) ^ 1);
         tc_fence_after();
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
-          mbar_wait(&conv[stage], phase);
+          mbar_wait(&conv[xstage], xphase);
           tc_fence_after();
-          uint8_t* sb = smem + stage * L::kStage;
-          const uint64_t bdesc = sw128_kmajor_desc(smem_u32(sb));
-          const uint64_t dhi = sw128_kmajor_desc(smem_u32(sb + L::kB));
-          const uint64_t dlo = sw128_kmajor_desc(smem_u32(sb + L::kB + L::kA));
+          const uint64_t bdesc = sw128_kmajor_desc(smem_u32(smem + stage * L::kB));
+          uint8_t* sa = smem + L::kXOffset + xstage * L::kXs;
+          const uint64_t dhi = sw128_kmajor_desc(smem_u32(sa));
+          const uint64_t dlo = sw128_kmajor_desc(smem_u32(sa + L::kA));
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             umma_bf16(tmem_base, dhi + 2 * k, bdesc + 2 * k, id_all, (kb | k) != 0);
             umma_bf16(tmem_base, dlo + 2 * k, bdesc + 2 * k, id_hi, 1);
           }
           umma_commit(&empty[stage]);
+          umma_commit(&xempty[xstage]);
           if (++stage == kRxStages) {
             stage = 0;
             phase ^= 1;
+          }
+          if (++xstage == kRxXStages) {
+            xstage = 0;
+            xphase ^= 1;
           }
         }
         umma_commit(tfull);
@@ -221,42 +229,49 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ convert + epilogue
-    const int ct = threadIdx.x - 128;  // 0..255
+    const int ct = threadIdx.x - 128;  // 0..kRfConvThreads-1
     const int jc = ct & 7;             // 32-byte (8 fp32) column chunk of the k-block
-    const int r0 = ct >> 3;            // rows r0 + 32 i, i = 0..3
+    const int r0 = ct >> 3;            // rows r0 + (kRfConvThreads / 8) i, i < kRfRows
     const int box = jc >> 2, c16 = (jc & 3) * 2;  // x box (32 columns) and 16-byte chunk inside a 128 B row
     int* s_hist = reinterpret_cast<int*>(smem + L::kHistOffset);
+    float* s_top = reinterpret_cast<float*>(smem + L::kTopOffset);
+    int* s_topi = reinterpret_cast<int*>(s_top + 2 * (EG / 32) * 128);
     if (hist_cc != nullptr) {
       for (int e = ct; e < EG; e += kRfConvThreads) s_hist[e] = 0;
       named_bar_sync(1, kRfConvThreads);
     }
-    uint32_t stage = 0, phase = 0, xstage = 0, xphase = 0, tile = 0;
+    uint32_t xstage = 0, xphase = 0, tile = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
       const int row_base = u * kBlockM;
-      float part[4] = {0.f, 0.f, 0.f, 0.f};
+      float part[kRfRows] = {};
+      // bound-scale weights of the next k-block are loaded one iteration ahead (L2 latency off
+      // the conversion's critical path)
+      float4 w0n = __ldg(reinterpret_cast<const float4*>(wabs + 8 * jc));
+      float4 w1n = __ldg(reinterpret_cast<const float4*>(wabs + 8 * jc + 4));
       for (int kb = 0; kb < nkb; ++kb) {
+        const float4 w0 = w0n, w1 = w1n;
+        if (kb + 1 < nkb) {
+          w0n = __ldg(reinterpret_cast<const float4*>(wabs + (kb + 1) * 64 + 8 * jc));
+          w1n = __ldg(reinterpret_cast<const float4*>(wabs + (kb + 1) * 64 + 8 * jc + 4));
+        }
         mbar_wait(&xfull[xstage], xphase);
-        const uint32_t sx = smem_u32(smem + L::kXOffset + xstage * L::kXs + box * (L::kXs / 2));
-        float4 cur[4][2];
+        uint8_t* sxs = smem + L::kXOffset + xstage * L::kXs;
+        const uint32_t sx = smem_u32(sxs + box * (L::kXs / 2));
+        float4 cur[kRfRows][2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = r0 + 32 * i;
+        for (int i = 0; i < kRfRows; ++i) {
+          const int r = r0 + (kRfConvThreads / 8) * i;
           cur[i][0] = lds_f4(sx + r * 128 + (((c16) ^ (r & 7)) << 4));
           cur[i][1] = lds_f4(sx + r * 128 + (((c16 + 1) ^ (r & 7)) << 4));
         }
-        uint64_t* x_release = &xempty[xstage];  // released only after the values are consumed (below)
-        if (++xstage == kRxXStages) {
-          xstage = 0;
-          xphase ^= 1;
-        }
-        const float4 w0 = __ldg(reinterpret_cast<const float4*>(wabs + kb * 64 + 8 * jc));
-        const float4 w1 = __ldg(reinterpret_cast<const float4*>(wabs + kb * 64 + 8 * jc + 4));
-        mbar_wait(&empty[stage], phase ^ 1);  // MMA done with this stage's operand tiles
-        uint8_t* shi = smem + stage * L::kStage + L::kB;
+        // every converting thread has its x values in registers before the stage is overwritten
+        // by the operand tiles (hi in the first 16 KB, lo in the second)
+        named_bar_sync(2, kRfConvThreads);
+        uint8_t* shi = sxs;
         uint8_t* slo = shi + L::kA;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = r0 + 32 * i;
+        for (int i = 0; i < kRfRows; ++i) {
+          const int r = r0 + (kRfConvThreads / 8) * i;
           const float f[8] = {cur[i][0].x, cur[i][0].y, cur[i][0].z, cur[i][0].w,
                               cur[i][1].x, cur[i][1].y, cur[i][1].z, cur[i][1].w};
           uint32_t hw[4], lw[4];
@@ -274,59 +289,74 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           part[i] += fabsf(f[0]) * w0.x + fabsf(f[1]) * w0.y + fabsf(f[2]) * w0.z + fabsf(f[3]) * w0.w +
                      fabsf(f[4]) * w1.x + fabsf(f[5]) * w1.y + fabsf(f[6]) * w1.z + fabsf(f[7]) * w1.w;
         }
-        fence_proxy_async();
+        fence_proxy_async();  // generic-proxy operand writes -> the tensor core's async-proxy reads
         __syncwarp();
-        // The x ring slot is handed back only now: its values have been consumed into the
-        // operand tiles above. (Releasing it right after issuing the loads let the next TMA
-        // land before the loads had read -- the loads were generic and still in flight.)
-        if (lane == 0) {
-          mbar_arrive(x_release);
-          mbar_arrive(&conv[stage]);
-        }
-        if (++stage == kRxStages) {
-          stage = 0;
-          phase ^= 1;
+        if (lane == 0) mbar_arrive(&conv[xstage]);
+        if (++xstage == kRxXStages) {
+          xstage = 0;
+          xphase ^= 1;
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < kRfRows; ++i) {
         float v = part[i];
         v += __shfl_xor_sync(0xffffffffu, v, 1);
         v += __shfl_xor_sync(0xffffffffu, v, 2);
         v += __shfl_xor_sync(0xffffffffu, v, 4);
-        if (jc == 0) s_xb[r0 + 32 * i] = v * 1.0001f + 1e-30f;
+        if (jc == 0) s_xb[r0 + (kRfConvThreads / 8) * i] = v * 1.0001f + 1e-30f;
       }
       named_bar_sync(1, kRfConvThreads);
-      if (warp < 8) {
+      // top-2 logits per row: the (EG / 32) column groups of the accumulator are read by
+      // (EG / 32) x 4 warps (warp & 3 = TMEM lane quadrant), then merged in expert order
+      constexpr int kParts = EG / 32;
+      const int part_id = (warp - 4) >> 2;
+      if (part_id < kParts) {
         mbar_wait(tfull, tile & 1);
         tc_fence_after();
         const int r = (warp & 3) * 32 + lane;
-        const uint32_t taddr = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-        float b1 = -INFINITY, b2 = -INFINITY;
-        int bi = 0;
-#pragma unroll 1
-        for (int c = 0; c < EG; c += 32) {
-          float a[32], b[32];
-          tmem_ld32(taddr + c, a);
-          tmem_ld32(taddr + EG + c, b);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int e = c + i;
-            const float v = a[i] + b[i];
-            if (e < E) {
-              if (v > b1) {
-                b2 = b1;
-                b1 = v;
-                bi = e;
-              } else if (v > b2) {
-                b2 = v;
-              }
-            }
-          }
-        }
+        const uint32_t taddr = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 32 * part_id;
+        float a[32], b[32];
+        tmem_ld32(taddr, a);
+        tmem_ld32(taddr + EG, b);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty);
+        float b1 = -INFINITY, b2 = -INFINITY;
+        int bi = 32 * part_id;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int e = 32 * part_id + i;
+          const float v = a[i] + b[i];
+          if (e < E) {
+            if (v > b1) {
+              b2 = b1;
+              b1 = v;
+              bi = e;
+            } else if (v > b2) {
+              b2 = v;
+            }
+          }
+        }
+        s_top[(0 * kParts + part_id) * 128 + r] = b1;
+        s_top[(1 * kParts + part_id) * 128 + r] = b2;
+        s_topi[part_id * 128 + r] = bi;
+      }
+      named_bar_sync(1, kRfConvThreads);
+      if (warp < 8) {
+        const int r = (warp & 3) * 32 + lane;
+        float b1 = s_top[r], b2 = s_top[kParts * 128 + r];
+        int bi = s_topi[r];
+#pragma unroll
+        for (int q = 1; q < kParts; ++q) {  // ascending experts: a later group wins only on '>'
+          const float c1 = s_top[q * 128 + r], c2 = s_top[(kParts + q) * 128 + r];
+          if (c1 > b1) {
+            b2 = fmaxf(b1, c2);
+            b1 = c1;
+            bi = s_topi[q * 128 + r];
+          } else {
+            b2 = fmaxf(b2, c1);
+          }
+        }
         const int t = row_base + r;
         if (hist_cc != nullptr) {
           // near ties re-decided here in float64 by the warp (the arithmetic of
@@ -401,7 +431,7 @@ static int launch_router_fused_tx(const float* x, int ldx, int T, int d, const v
   }
   if (hist_cc == nullptr) MP_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
   const int units = cdiv(T, kBlockM);
-  MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kGemmThreads), smem, st, tb, tx, T,
+  MP_CUDA_TRY(launch_pdl(kern, dim3(units < num_sms() ? units : num_sms()), dim3(kRouterThreads), smem, st, tb, tx, T,
                          d, w_abs, E, route, eps, count, list, x, ldx, w32, hist_cc));
   return MP_OK;
 }
