@@ -360,108 +360,6 @@ __device__ void exec_layer_body(int l, int* sm, int* red, const int32_t* demand,
                   piece_row, piece_rows, exp_begin, pieces_stride, err);
 }
 
-// In-place exclusive scan of n ints in shared memory by ONE warp (lane = contiguous run);
-// returns the total. Integer sums: identical to block_exclusive_scan.
-__device__ inline int warp_exclusive_scan(int* a, int n) {
-  const int lane = threadIdx.x & 31;
-  const int per = (n + 31) / 32;
-  const int b = min(n, lane * per), e = min(n, b + per);
-  int s = 0;
-  for (int i = b; i < e; ++i) s += a[i];
-  int incl = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  int run = incl - s;
-  for (int i = b; i < e; ++i) {
-    const int v = a[i];
-    a[i] = run;
-    run += v;
-  }
-  __syncwarp();
-  return total;
-}
-
-// exec_layer_core for ONE warp (threads 0..31 of the block): the same slot / row / piece
-// layout without block-wide barriers (the 1024-thread form spends most of its time in
-// them). demand and res_in are shared-memory arrays; global outputs only when `write`.
-__device__ void exec_layer_warp(int* sm, const int32_t* demand, const int32_t* res_in, bool write, int E,
-                                int max_slots, int split_m, int32_t* res, int32_t* __restrict__ corrective,
-                                int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
-                                int32_t* __restrict__ slot_row_g, int32_t* __restrict__ piece_row,
-                                int32_t* __restrict__ piece_rows, int32_t* __restrict__ exp_begin,
-                                int32_t* __restrict__ err) {
-  const int lane = threadIdx.x & 31;
-  int* s_off = sm;              // E + 1
-  int* s_n = s_off + E + 1;     // E
-  int* s_row = s_n + E;         // max_slots + 1
-  int* s_pc = s_row + max_slots + 1;
-  for (int e = lane; e < E; e += 32) {
-    const int n = demand[e], rp = res_in[e];
-    const int cnt = rp > 0 ? rp : (n > 0 ? 1 : 0);
-    if (write) {
-      corrective[e] = (rp == 0 && n > 0) ? 1 : 0;
-      res[e] = cnt;
-    }
-    s_off[e] = cnt;
-    s_n[e] = n;
-  }
-  __syncwarp();
-  const int ns = warp_exclusive_scan(s_off, E);
-  if (lane == 0) {
-    s_off[E] = ns;
-    if (write) num_slots[0] = ns;
-  }
-  __syncwarp();
-  if (ns > max_slots) {
-    if (write && lane == 0) atomicExch(err, 1);
-    return;
-  }
-  for (int s = lane; s < ns; s += 32) {
-    int lo = 0, hi = E;  // invariant s_off[lo] <= s < s_off[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (s_off[mid] <= s) lo = mid; else hi = mid;
-    }
-    const int j = s - s_off[lo], c = s_off[lo + 1] - s_off[lo], n = s_n[lo];
-    const int size = n > j ? (n - j + c - 1) / c : 0;
-    s_row[s] = size;
-    s_pc[s] = (split_m & 1) ? cdiv(size, kBlockMRows) : (size > 0 ? 1 : 0);
-  }
-  __syncwarp();
-  if (split_m & 2) {  // CTA-pair GEMM: even piece count per expert
-    for (int e = lane; e < E; e += 32) {
-      int tot = 0;
-      for (int s = s_off[e]; s < s_off[e + 1]; ++s) tot += s_pc[s];
-      if (tot & 1) s_pc[s_off[e + 1] - 1] += 1;
-    }
-    __syncwarp();
-  }
-  warp_exclusive_scan(s_row, ns);
-  const int P = warp_exclusive_scan(s_pc, ns);
-  if (lane == 0) s_pc[ns] = P;
-  __syncwarp();
-  if (!write) return;
-  for (int s = lane; s < ns; s += 32) slot_row_g[s] = s_row[s];
-  int total_rows = 0;
-  for (int e = lane; e < E; e += 32) total_rows += s_n[e];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) total_rows += __shfl_xor_sync(0xffffffffu, total_rows, o);
-  for (int s = lane; s < ns; s += 32) {
-    const int row0 = s_row[s];
-    const int size = (s + 1 < ns ? s_row[s + 1] : total_rows) - row0;
-    const int p0 = s_pc[s], np = s_pc[s + 1] - p0;
-    emit_pieces(piece_row, piece_rows, p0, np, row0, size, split_m & 1);
-  }
-  for (int e = lane; e <= E; e += 32) {
-    off_g[e] = s_off[e];
-    exp_begin[e] = s_pc[s_off[e]];
-  }
-}
-
 __global__ void k_exec_layer(const int32_t* __restrict__ demand, int E, int max_slots, int split_m,
                              int32_t* __restrict__ res, int32_t* __restrict__ corrective,
                              int32_t* __restrict__ num_slots, int32_t* __restrict__ off_g,
