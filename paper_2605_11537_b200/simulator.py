@@ -276,12 +276,15 @@ class BatchRunner:
 
     def _run_predicted(self, batch, table: HashTable) -> BatchOutcome:
         plan = self._plan(table)
+        self.state.last_place_device = self.state.last_exec_device = None
         _, placement, log = apply_batch(self.state, table, plan)
         place = self.state.last_place_device
         # tokens execute on their true experts; a miss loads the expert first (corrective LOAD)
         _, execution, xlog = execution_map(self.state, batch.oracle_routing)
         log.extend(xlog)
         ex = self.state.last_exec_device
+        if ex is None:  # no tokens: simulate_layer rejects an empty token map (src/simulator.py:70-71)
+            raise ConfigurationError("token map must be nonempty")
         full = place is not None and place["layers"] == list(range(table.num_layers))
         counts = layer_counts(ex["token_to_slot"], ex["num_slots"], ex["max_slots"],
                               token_event=place["token_event"][:, :ex["T"]] if full else None,
