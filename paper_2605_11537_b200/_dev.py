@@ -66,6 +66,37 @@ class Workspace:
 WORKSPACE = Workspace()
 
 
+def upload_rows(arr, d: int, dp: int, dev, name: str = "embeddings") -> torch.Tensor:
+    """(T, d) float rows -> (T, dp) float32 device tensor, zero padded. Non-finite values raise
+    NumericError like src/validation.py:22-27, checked on the device (one flag read) instead of
+    a host pass over the array; float64 input is narrowed on the device."""
+    from .errors import NumericError
+
+    a = np.asarray(arr)
+    if a.dtype not in (np.float32, np.float64):
+        a = a.astype(np.float32)
+    a = np.ascontiguousarray(a)
+    t = torch.from_numpy(a).to(dev)
+    if not bool(torch.isfinite(t).all().item()):
+        raise NumericError(f"{name} contains non-finite values")
+    if t.ndim != 2 or t.shape[1] != d:
+        return t  # the caller reports the shape error
+    if dp == d and t.dtype == torch.float32:
+        return t
+    out = torch.zeros(t.shape[0], dp, dtype=torch.float32, device=dev)
+    out[:, :d] = t
+    return out
+
+
+def download(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy through page-locked memory (torch's caching host allocator reuses
+    the pinned block once the array is released): a pageable D2H of a 50 MB stream runs at
+    ~2 GB/s, a pinned one at PCIe speed."""
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
+
+
 def round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import WORKSPACE, pow2_at_least, ptr, require_device, round_up, stream_ptr
+from ._dev import WORKSPACE, download, pow2_at_least, ptr, require_device, round_up, stream_ptr, upload_rows
 from .errors import ConfigurationError, NumericError
 
 DEFAULT_SRU_LAYERS = 10  # src/predictor.py:19
@@ -266,17 +266,14 @@ def sru_stack_device(x32: torch.Tensor, dw: DeviceSru, c0: torch.Tensor | None =
 
 
 def _embeddings_device(embeddings, d_model: int, dev) -> torch.Tensor:
-    x = check_finite("embeddings", embeddings).astype(np.float64)
+    x = upload_rows(embeddings, d_model, round_up(max(d_model, 64), 64), dev)
     if x.ndim != 2:
         raise ConfigurationError("embeddings must be (tokens, d_model)")
     if x.shape[0] == 0:
         raise ConfigurationError("batch must contain at least one token")
-    if x.shape[1] != d_model:
+    if x.shape[1] != round_up(max(d_model, 64), 64):
         raise ConfigurationError(f"embedding width {x.shape[1]} != d_model {d_model}")
-    dp = round_up(max(d_model, 64), 64)
-    out = torch.zeros(x.shape[0], dp, dtype=torch.float32)
-    out[:, :d_model] = torch.from_numpy(x)
-    return out.to(dev)
+    return x
 
 
 def _raise_if_nonfinite(flag: torch.Tensor) -> None:
@@ -309,7 +306,7 @@ def sru_forward(embeddings, params: SruParams) -> np.ndarray:
     dw = _device_sru(params, dev)
     h, _, nf = sru_stack_device(x, dw)
     _raise_if_nonfinite(nf)
-    return h[:, : params.d_model].double().cpu().numpy()
+    return download(h[:, : params.d_model].double())
 
 
 def sparsemax(z) -> np.ndarray:

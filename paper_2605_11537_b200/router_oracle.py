@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import WORKSPACE, ptr, require_device, round_up, stream_ptr
+from ._dev import WORKSPACE, download, ptr, require_device, round_up, stream_ptr, upload_rows
 from .errors import ConfigurationError, PlacementError
 from .predictor import check_finite
 
@@ -204,13 +204,11 @@ def ffn_device(x: torch.Tensor, y: torch.Tensor, layer: DeviceMoeLayer, tor, pro
 
 
 def _stream_device(embeddings, d: int, dp: int, dev) -> torch.Tensor:
-    emb = check_finite("embeddings", getattr(embeddings, "embeddings", embeddings))
-    emb = np.asarray(emb, dtype=np.float32)
-    if emb.ndim != 2 or emb.shape[1] != d:
-        raise ConfigurationError(f"embeddings shape {emb.shape} != (tokens, {d})")
-    x = torch.zeros(emb.shape[0], dp, dtype=torch.float32)
-    x[:, :d] = torch.from_numpy(emb)
-    return x.to(dev)
+    emb = getattr(embeddings, "embeddings", embeddings)
+    x = upload_rows(emb, d, dp, dev)
+    if x.ndim != 2 or x.shape[1] != dp:
+        raise ConfigurationError(f"embeddings shape {tuple(np.shape(emb))} != (tokens, {d})")
+    return x
 
 
 # ----------------------------------------------------------------------------- public API
@@ -333,7 +331,7 @@ def moe_forward(batch, params: ToyMoeParams, placement=DENSE_BASELINE) -> np.nda
         _run_layers_device(x, dm)
     else:
         _run_layers_device(x, dm, placement=_validated_placement(placement, params, T, dev))
-    return x[:, : params.d_model].cpu().numpy()
+    return download(x[:, : params.d_model] if params.d_model != dm.dp else x)
 
 
 # ---------------------------------------------------------------- parameter files
