@@ -372,8 +372,14 @@ class MoEPipeline:
         all-gathered predicted assignments so every rank holds the same state."""
         import torch.distributed as dist
 
+        from .errors import ConfigurationError
         from .ep import CudaEpKernels, ExpertParallelMoE
 
+        if self.cfg.physical_replicas:
+            # every GPU keeps all master weights under EP (DESIGN.md §6): a replica hosted on a GPU
+            # reads them there, so per-slot weight pools would only add copies
+            raise ConfigurationError("physical replicas are a single-GPU mode; expert parallelism reads the "
+                                     "resident master weights on every GPU")
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
