@@ -68,6 +68,8 @@ def parse_args():
     p.add_argument("--no-baselines", action="store_true", help="skip the same-run baseline measurements")
     p.add_argument("--no-checks", action="store_true", help="skip the float correctness checks")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
+    p.add_argument("--ep-compact", action="store_true",
+                   help="expert parallelism with split sizes read back every layer (no step graph)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
     p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")
     p.add_argument("--overlap", choices=["on", "off"], default="off",
@@ -460,7 +462,10 @@ def run_ours(args):
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
     ep = world > 1 or args.ep
     if ep:
-        pipe.enable_expert_parallel()
+        # fixed-split dispatch (2 T / G rows per peer block): graph-capturable; --ep-compact reads
+        # the split sizes back every layer instead
+        pipe.enable_expert_parallel(peer_cap=0 if args.ep_compact else None)
+    ep_graph = ep and not args.ep_compact
     weights_same = weights_hash_equal(pipe, world)
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]
     x = torch.empty(T, d, device="cuda")
@@ -490,7 +495,7 @@ def run_ours(args):
         overlap = OverlappedPipeline(pipe, ev, args.ffn_sms, args.pred_sms)
         overlap.run([b[0] for b in batches], 2)
         torch.cuda.synchronize()
-    elif not args.no_graph and not ep:
+    elif not args.no_graph and (not ep or ep_graph):
         # one CUDA graph per step for the timed loop; a second capture with events around every
         # GEMM (event nodes cost ~8 us each inside a graph) is replayed once afterwards for the
         # roofline's per-launch durations
@@ -569,7 +574,7 @@ def run_ours(args):
     # "MoE layers only" next to end-to-end -- the predictor + plan part of the
     # step captured alone and timed the same way; the MoE layers are the rest of the step
     moe_only = None
-    if graph is not None:
+    if graph is not None and not ep:
         g_pred = pipe.capture_call(lambda sp: pipe.predict(x, sp) + pipe.plan_and_place(sp))
         for _ in range(3):
             g_pred.replay()
@@ -631,6 +636,8 @@ def run_ours(args):
         "moe_layers_only": moe_only,
         "cuda_graph": graph is not None or overlap is not None,
         "overlap": overlap is not None,
+        "ep_dispatch": ({"mode": "fixed-split" if ep_graph else "compact", "peer_cap_rows": pipe.ep.k.peer_cap,
+                         "overflowed": pipe.ep_overflowed() if ep_graph else False} if ep else None),
     }
 
     result["config"]["ffn_kernels"] = pipe.cfg.ffn  # resolved from --ffn auto
@@ -655,6 +662,9 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
+        for g in (graph, locals().get("graph_ev")):  # graphs with captured NCCL collectives go first
+            if g is not None:
+                g.destroy()
         dist.destroy_process_group()
     return 0
 
@@ -848,7 +858,7 @@ def run_e2e(args, pipe, batches, world):
     in_free = [torch.cuda.Event() for _ in range(2)]
     comp_done = [torch.cuda.Event() for _ in range(2)]
     d2h_done = [torch.cuda.Event() for _ in range(2)]
-    graph = pipe._bench_graph if not args.no_graph and getattr(pipe, "ep", None) is None else None
+    graph = pipe._bench_graph if not args.no_graph else None
 
     def run(n, timed):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -352,6 +352,19 @@ MP_API int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, const
                              int32_t* recv_of_local, void* ws, size_t ws_bytes, void* stream);
 MP_API int mp_gather_rows_bf16(const void* buf, int n, int d, const int32_t* idx, void* out, void* stream);
 MP_API int mp_ep_combine(float* x, int T, int d, const float* yback, const int32_t* send_pos, void* stream);
+/* Fixed-split form (graph-capturable dispatch, no split sizes on the host): every (source,
+ * destination) block of the send / receive buffers holds peer_cap rows, so the caller's
+ * all-to-alls use equal static splits of peer_cap * d elements. If the layer needs more
+ * than peer_cap rows for some peer, *overflow |= 1 and the layer does nothing on the device
+ * (no pieces, no sends): check the flag once per step and re-run the step with
+ * mp_ep_plan. peer_cap = 0 is mp_ep_plan. mp_gather_rows_bf16_dn gathers min(n_max,
+ * *n_dev) rows (n_dev = the plan's num_local_rows, on the device). */
+MP_API int mp_ep_plan_cap(const int32_t* route, int T, const int32_t* C, int G, int E, int rank, int max_slots,
+                          int split_m, int peer_cap, int32_t* overflow, int32_t* res, int32_t* send_counts,
+                          int32_t* recv_counts, int32_t* num_local_rows, int32_t* send_pos, int32_t* piece_row,
+                          int32_t* piece_rows, int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
+MP_API int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
+                                  void* out, void* stream);
 
 
 /* Whole-step CUDA graphs (capture on `stream`, replay) and timing events that remain

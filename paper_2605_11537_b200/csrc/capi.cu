@@ -1,5 +1,6 @@
 // C-ABI plumbing: error strings, device info, TMA map encoding, the generic
 // dense tcgen05 GEMM entry point.
+#include <cstring>
 #include <vector>
 #include <stdarg.h>
 #include <string.h>
@@ -224,11 +225,22 @@ extern "C" int mp_graph_end_counted(void* stream, void** graph_exec, int32_t* ke
   cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
   std::vector<cudaGraphNode_t> nodes(n);
   if (e == cudaSuccess && n) e = cudaGraphGetNodes(g, nodes.data(), &n);
+  // kernel nodes of THIS library (namespace mp): collectives (NCCL) and torch copies captured
+  // into the same graph are not counted
   int32_t k = 0;
   for (size_t i = 0; e == cudaSuccess && i < n; ++i) {
     cudaGraphNodeType t;
     e = cudaGraphNodeGetType(nodes[i], &t);
-    k += (e == cudaSuccess && t == cudaGraphNodeTypeKernel);
+    if (e != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp = {};
+    const char* name = nullptr;
+    if (cudaGraphKernelNodeGetParams(nodes[i], &kp) == cudaSuccess && kp.func != nullptr &&
+        cudaFuncGetName(&name, kp.func) == cudaSuccess && name != nullptr)
+      k += std::strncmp(name, "_ZN2mp", 6) == 0 || std::strncmp(name, "mp::", 4) == 0 ||
+           std::strncmp(name, "void mp::", 9) == 0;  // mangled or demangled
+    else
+      k += 1;  // name unavailable: count it
+    (void)cudaGetLastError();
   }
   cudaGraphExec_t ex = nullptr;
   if (e == cudaSuccess) e = cudaGraphInstantiateWithFlags(&ex, g, 0);

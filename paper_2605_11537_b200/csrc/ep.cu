@@ -18,6 +18,13 @@
 // Sender packs rows by (destination, slot, position); receiver lays rows out by
 // (slot, global position) -- the single-device order -- so the grouped GEMM and
 // its results are bit-identical to the 1-GPU path.
+//
+// Fixed-split ("capacity") mode, peer_cap > 0: every (source, destination) block of the
+// send / receive buffers has peer_cap rows, so the all-to-alls have equal, static splits
+// and the whole step can be captured in a CUDA graph (no split sizes reach the host). A
+// layer whose plan needs more than peer_cap rows for some peer sets *overflow and turns
+// into a no-op on the device (no pieces, no sends); the caller checks the flag once per
+// step and re-runs the step in the compact mode.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -45,11 +52,14 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
                           int32_t* __restrict__ res, EpPlanWs w, int32_t* __restrict__ send_counts,
                           int32_t* __restrict__ recv_counts, int32_t* __restrict__ num_local_rows,
                           int32_t* __restrict__ piece_row, int32_t* __restrict__ piece_rows,
-                          int32_t* __restrict__ exp_begin, int32_t* __restrict__ err) {
+                          int32_t* __restrict__ exp_begin, int32_t* __restrict__ err, int peer_cap,
+                          int32_t* __restrict__ overflow) {
   griddep_launch_dependents();
   griddep_wait();
   extern __shared__ int sm[];
   __shared__ int red[40];
+  __shared__ int s_over;
+  if (threadIdx.x == 0) s_over = 0;
   int* s_off = sm;                   // E + 1
   int* s_lb = s_off + E + 1;         // max_slots + 1 : local base (hosted slots)
   int* s_pc = s_lb + max_slots + 1;  // max_slots + 1 : pieces per slot
@@ -77,7 +87,9 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
     if (threadIdx.x == 0) {
       atomicExch(err, 1);
       *num_local_rows = -1;
+      if (overflow) atomicOr(overflow, 1);  // fixed-split mode: the host re-runs the step compactly
     }
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) exp_begin[e] = 0;
     for (int g = threadIdx.x; g < G; g += blockDim.x) send_counts[g] = recv_counts[g] = 0;
     return;
   }
@@ -126,6 +138,27 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
     *num_local_rows = nloc;
   }
   __syncthreads();
+  if (peer_cap > 0) {  // every (source, destination) block against the fixed split: all ranks hold
+                       // the same counts and plan, so all reach the same decision
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int pair = warp; pair < G * G; pair += blockDim.x >> 5) {
+      const int src = pair / G, dst = pair - src * G;
+      int sum = 0;
+      for (int s = lane; s < S; s += 32) sum += s_gpu[s] == dst ? s_rows[(size_t)src * max_slots + s] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0 && sum > peer_cap) s_over = 1;
+    }
+  }
+  __syncthreads();
+  if (s_over) {  // fixed splits too small: the layer becomes a no-op on every rank, the step is flagged
+    if (threadIdx.x == 0) {
+      atomicExch(err, 1);
+      if (overflow) atomicOr(overflow, 1);
+    }
+    for (int e = threadIdx.x; e <= E; e += blockDim.x) exp_begin[e] = 0;
+    return;
+  }
   // sender tables (this rank) and receiver tables, one thread per peer
   {  // per peer d (one warp each, G <= 32): exclusive scans over the slots, 32 slots per step
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,6 +187,7 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
       if (lane == 0) {
         send_counts[d] = acc_s;
         recv_counts[d] = acc_r;
+
       }
     }
   }
@@ -161,7 +195,10 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
     const int gpu = s_gpu[s];
     int displ = 0;
-    for (int g = 0; g < gpu; ++g) displ += send_counts[g];
+    if (peer_cap > 0)
+      displ = gpu * peer_cap;
+    else
+      for (int g = 0; g < gpu; ++g) displ += send_counts[g];
     w.send_base[s] += displ;
     if (gpu == rank) {
       int acc = s_lb[s], rdispl = 0;
@@ -169,7 +206,7 @@ __global__ void k_ep_plan(const int32_t* __restrict__ C, int G, int E, int rank,
         w.local_start[(size_t)g * max_slots + s] = acc;
         acc += s_rows[(size_t)g * max_slots + s];
         w.recv_start[(size_t)g * max_slots + s] += rdispl;
-        rdispl += recv_counts[g];
+        rdispl += peer_cap > 0 ? peer_cap : recv_counts[g];
       }
       const int row0 = s_lb[s], size = w.slot_size[s];
       const int p0 = s_pc[s], np = s_pc[s + 1] - p0;
@@ -187,10 +224,13 @@ __global__ void k_ep_send_pos(const int32_t* __restrict__ route, int T, int E, i
                               EpPlanWs w, int32_t* __restrict__ send_pos, const int32_t* __restrict__ err) {
   griddep_launch_dependents();
   griddep_wait();
-  if (*err) return;  // the plan overflowed max_slots: its tables were not written
   __shared__ int se[kChunk];
   const int ch = blockIdx.x;
   const int t = ch * kChunk + threadIdx.x;
+  if (*err) {  // the plan overflowed (max_slots or the fixed split): nothing is sent or combined
+    if (t < T) send_pos[t] = -1;
+    return;
+  }
   const int e = (t < T) ? __ldg(&route[t]) : -1;
   se[threadIdx.x] = e;
   __syncthreads();
@@ -210,7 +250,7 @@ __global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32
   griddep_launch_dependents();
   griddep_wait();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (t >= T) return;
+  if (t >= T || send_pos[t] < 0) return;
   const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * d);
   uint2* dst = reinterpret_cast<uint2*>(sendbuf + (size_t)send_pos[t] * d);
   for (int k = lane; k < d / 4; k += 32) {
@@ -234,13 +274,14 @@ __global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ 
   for (int k = threadIdx.x; k < n; k += blockDim.x) recv_of_local[l0 + k] = r0 + k;
 }
 
-// xperm[row] = buf[idx[row]] for bf16 rows; one warp per row.
+// xperm[row] = buf[idx[row]] for bf16 rows; one warp per row. n_dev (optional): the row
+// count lives on the device (fixed-split EP: n is the buffer's capacity).
 __global__ void k_gather_bf16(const __nv_bfloat16* __restrict__ buf, int n, int d, const int32_t* __restrict__ idx,
-                              __nv_bfloat16* __restrict__ out) {
+                              __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ n_dev) {
   griddep_launch_dependents();
   griddep_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (row >= n) return;
+  if (row >= n || (n_dev != nullptr && row >= *n_dev)) return;
   const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)__ldg(&idx[row]) * d);
   uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * d);
   for (int k = lane; k < d / 8; k += 32) dst[k] = __ldg(&src[k]);
@@ -252,7 +293,7 @@ __global__ void k_ep_combine(float* __restrict__ x, int T, int d, const float* _
   griddep_launch_dependents();
   griddep_wait();
   const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (t >= T) return;
+  if (t >= T || send_pos[t] < 0) return;
   float4* dst = reinterpret_cast<float4*>(x + (size_t)t * d);
   const float4* src = reinterpret_cast<const float4*>(yback + (size_t)send_pos[t] * d);
   for (int k = lane; k < d / 4; k += 32) {
@@ -295,6 +336,13 @@ static EpPlanWs carve(void* ws, int G, int E, int max_slots, int32_t** cc, int n
 
 using namespace mp;
 
+extern "C" int mp_ep_plan_cap(const int32_t* route, int T, const int32_t* C, int G, int E, int rank, int max_slots,
+                              int split_m, int peer_cap, int32_t* overflow, int32_t* res, int32_t* send_counts,
+                              int32_t* recv_counts, int32_t* num_local_rows, int32_t* send_pos, int32_t* piece_row,
+                              int32_t* piece_rows, int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
+extern "C" int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
+                                      void* out, void* stream);
+
 extern "C" size_t mp_ep_workspace_bytes(int G, int T, int E, int max_slots) {
   const int nch = cdiv(T > 0 ? T : 1, kChunk);
   return al(4 * (size_t)(E + 1)) + 2 * al(4 * (size_t)E) + 3 * al(4 * (size_t)max_slots) +
@@ -305,8 +353,16 @@ extern "C" int mp_ep_plan(const int32_t* route, int T, const int32_t* C, int G, 
                           int split_m, int32_t* res, int32_t* send_counts, int32_t* recv_counts,
                           int32_t* num_local_rows, int32_t* send_pos, int32_t* piece_row, int32_t* piece_rows,
                           int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
-  MP_REQUIRE(G >= 1 && G <= 32 && rank >= 0 && rank < G && E >= 1 && max_slots >= E && T >= 0, MP_ERR_CONFIG,
-             "mp_ep_plan: bad sizes G=%d rank=%d E=%d", G, rank, E);
+  return mp_ep_plan_cap(route, T, C, G, E, rank, max_slots, split_m, 0, nullptr, res, send_counts, recv_counts,
+                        num_local_rows, send_pos, piece_row, piece_rows, exp_begin, ws, ws_bytes, stream);
+}
+
+extern "C" int mp_ep_plan_cap(const int32_t* route, int T, const int32_t* C, int G, int E, int rank, int max_slots,
+                              int split_m, int peer_cap, int32_t* overflow, int32_t* res, int32_t* send_counts,
+                              int32_t* recv_counts, int32_t* num_local_rows, int32_t* send_pos, int32_t* piece_row,
+                              int32_t* piece_rows, int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream) {
+  MP_REQUIRE(G >= 1 && G <= 32 && rank >= 0 && rank < G && E >= 1 && max_slots >= E && T >= 0 && peer_cap >= 0,
+             MP_ERR_CONFIG, "mp_ep_plan: bad sizes G=%d rank=%d E=%d peer_cap=%d", G, rank, E, peer_cap);
   MP_REQUIRE(ws_bytes >= mp_ep_workspace_bytes(G, T, E, max_slots), MP_ERR_CONFIG, "mp_ep_plan: workspace");
   cudaStream_t st = (cudaStream_t)stream;
   const int nch = cdiv(T > 0 ? T : 1, kChunk);
@@ -321,7 +377,7 @@ extern "C" int mp_ep_plan(const int32_t* route, int T, const int32_t* C, int G, 
   }
   MP_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
   k_ep_plan<<<1, 1024, sm, st>>>(C, G, E, rank, max_slots, split_m & 1, res, w, send_counts, recv_counts,
-                                 num_local_rows, piece_row, piece_rows, exp_begin, err);
+                                 num_local_rows, piece_row, piece_rows, exp_begin, err, peer_cap, overflow);
   if (T > 0) {
     // local stable ranks (chunk histograms + exclusive scan over chunks)
     int rc = mp_histogram_ws(route, 1, T, E, cc + (size_t)nch * E, cc, (size_t)nch * E * 4, stream);
@@ -354,10 +410,15 @@ extern "C" int mp_ep_recv_layout(int G, int T, int E, int rank, int max_slots, c
 }
 
 extern "C" int mp_gather_rows_bf16(const void* buf, int n, int d, const int32_t* idx, void* out, void* stream) {
+  return mp_gather_rows_bf16_dn(buf, n, d, idx, nullptr, out, stream);
+}
+
+extern "C" int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
+                                      void* out, void* stream) {
   MP_REQUIRE(d % 8 == 0, MP_ERR_CONFIG, "mp_gather_rows_bf16: d %% 8 != 0");
-  if (n > 0)
-    k_gather_bf16<<<cdiv(n * 32, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)buf, n, d, idx,
-                                                                         (__nv_bfloat16*)out);
+  if (n_max > 0)
+    k_gather_bf16<<<cdiv(n_max * 32, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)buf, n_max, d, idx,
+                                                                             (__nv_bfloat16*)out, n_dev);
   MP_CUDA_TRY(cudaGetLastError());
   return MP_OK;
 }

@@ -365,11 +365,16 @@ class MoEPipeline:
         return n + 2
 
     # ------------------------------------------------------------------ expert parallelism
-    def enable_expert_parallel(self, group=None) -> None:
+    def enable_expert_parallel(self, group=None, peer_cap: int | None = 0) -> None:
         """Shard experts' work over the ranks of ``group`` (one process per GPU, NCCL):
         every rank keeps all weights, routes its own tokens and dispatches them to the GPU
         hosting their replica (paper_2605_11537_b200/ep.py). Residency is planned from the
-        all-gathered predicted assignments so every rank holds the same state."""
+        all-gathered predicted assignments so every rank holds the same state.
+
+        ``peer_cap`` > 0: fixed-split dispatch with that many rows per (source, destination)
+        block -- no host read-back, the step can be captured in a CUDA graph; ``None``: the
+        default capacity 2 T / G rows (T at G = 1); 0: compact dispatch (split sizes read
+        back once per layer)."""
         import torch.distributed as dist
 
         from .errors import ConfigurationError
@@ -385,7 +390,10 @@ class MoEPipeline:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         cfg = self.cfg
         # slots of the global plan: G * C capacity slots + at most one corrective replica per expert
-        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.world * cfg.capacity + cfg.num_experts)
+        if peer_cap is None:
+            peer_cap = cfg.tokens if self.world == 1 else min(cfg.tokens, -(-2 * cfg.tokens // self.world))
+        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.world * cfg.capacity + cfg.num_experts,
+                          peer_cap=peer_cap)
         self.ep = ExpertParallelMoE(k, cfg.num_layers, cfg.num_experts, group)
         self.ep.res = self.res  # one residency state for placement and execution
         GT = self.world * cfg.tokens
@@ -432,6 +440,36 @@ class MoEPipeline:
         return n + 1
 
     def step_ep(self, x: torch.Tensor, events=None) -> int:
+        """One expert-parallel step. Fixed-split dispatch (``peer_cap``): outside a CUDA-graph
+        capture the overflow flag is checked once at the end; on overflow the step is rolled
+        back (input stream and residency state) and re-run with compact dispatch. A captured
+        step leaves the check to the caller (``ep_overflowed``)."""
+        k = self.ep.k
+        if not k.peer_cap or torch.cuda.is_current_stream_capturing():
+            return self._step_ep(x, events)
+        x0, res0 = x.clone(), self.res.clone()
+        k.overflow.zero_()
+        n = self._step_ep(x, events)
+        if int(k.overflow.item()):
+            x.copy_(x0)
+            self.res.copy_(res0)
+            cap, k.peer_cap = k.peer_cap, 0
+            try:
+                n = self._step_ep(x, events)
+            finally:
+                k.peer_cap = cap
+                k.overflow.zero_()
+        return n
+
+    def ep_overflowed(self) -> bool:
+        """Fixed-split dispatch: did any layer since the last reset need more than peer_cap rows
+        for some peer (that layer did nothing; the step must be re-run)? Resets the flag."""
+        k = self.ep.k
+        hit = bool(int(k.overflow.item()))
+        k.overflow.zero_()
+        return hit
+
+    def _step_ep(self, x: torch.Tensor, events=None) -> int:
         import torch.distributed as dist
 
         cfg, L, T, E = self.cfg, self.cfg.num_layers, self.cfg.tokens, self.cfg.num_experts
@@ -685,12 +723,18 @@ class StepGraph:
     def replay(self):
         _lib.call("mp_graph_launch", self.h, stream_ptr())
 
-    def __del__(self):
+    def destroy(self):
+        """Release the executable graph now (a graph holding captured NCCL collectives must be
+        destroyed before its process group)."""
         try:
             if self.h:
                 _lib.load_library().mp_graph_destroy(self.h)
         except Exception:
             pass
+        self.h = None
+
+    def __del__(self):
+        self.destroy()
 
 
 def _layer_from_device(router: torch.Tensor, u: torch.Tensor, v: torch.Tensor, ffn: str = "two") -> DeviceMoeLayer:

@@ -19,9 +19,13 @@ tokens. Per MoE layer, on every rank:
 
 Because the global ranks, slots, rows and per-row arithmetic are those of the
 single-device path, the output is bit-identical to one GPU running the whole
-batch. The all-to-all byte counts are data dependent, so each layer does one
-small device->host read of the split sizes (the reference's own executor is
-host driven, src/simulator.py:181-208).
+batch. In the compact mode the all-to-all byte counts are data dependent, so each layer
+does one small device->host read of the split sizes. In the fixed-split mode
+(``peer_cap`` > 0) every (source, destination) block of the send / receive buffers has
+peer_cap rows: the all-to-alls have static equal splits, nothing reaches the host and the
+whole step can be captured in one CUDA graph; a layer that would need more than peer_cap
+rows for some peer sets an overflow flag and does nothing, and the caller re-runs the step
+in the compact mode (MoEPipeline.step does so, checking the flag once per step).
 
 The kernel layer is pluggable: ``CudaEpKernels`` (the product) or, in the
 CPU multi-process tests only, a numpy restatement from ``oracle/``.
@@ -56,9 +60,11 @@ class CudaEpKernels:
 
     dispatch_dtype = torch.bfloat16
 
-    def __init__(self, layers: list[DeviceMoeLayer], tokens: int, world: int, rank: int, max_slots: int):
+    def __init__(self, layers: list[DeviceMoeLayer], tokens: int, world: int, rank: int, max_slots: int,
+                 peer_cap: int = 0):
         self.layers = layers
         self.T, self.G, self.rank, self.max_slots = tokens, world, rank, max_slots
+        self.peer_cap = int(peer_cap)  # rows per (source, destination) block; 0: compact, sizes read back
         lay = layers[0]
         self.E, self.d, self.F = lay.E, lay.dp, lay.Fp
         dev = lay.U.device
@@ -79,10 +85,12 @@ class CudaEpKernels:
         self.sizes_ready = torch.cuda.Event()
         # capacity buffers (no per-layer allocation): a rank sends at most T rows and receives
         # at most G * T
-        self.sendbuf = torch.empty(tokens, self.d, dtype=torch.bfloat16, device=dev)
+        self.overflow = torch.zeros(1, **i32)  # fixed-split mode: some layer needed more than peer_cap rows
+        send_rows = max(tokens, world * self.peer_cap)
+        self.sendbuf = torch.empty(send_rows, self.d, dtype=torch.bfloat16, device=dev)
         self.recvbuf = torch.empty(self.cap_rows, self.d, dtype=torch.bfloat16, device=dev)
         self.ybuf = torch.empty(self.cap_rows, self.d, dtype=torch.float32, device=dev)
-        self.yback = torch.empty(tokens, self.d, dtype=torch.float32, device=dev)
+        self.yback = torch.empty(send_rows, self.d, dtype=torch.float32, device=dev)
         self._packed_for = None
         # zero-filled: if a plan overflows max_slots its send positions are left untouched, and the
         # pack issued before the host sees the error must still write inside the send buffer
@@ -90,7 +98,7 @@ class CudaEpKernels:
         self.piece_row = torch.empty(self.pstride, **i32)
         self.piece_rows = torch.empty(self.pstride, **i32)
         self.exp_begin = torch.empty(self.E + 1, **i32)
-        self.recv_of_local = torch.empty(self.cap_rows, **i32)
+        self.recv_of_local = torch.zeros(self.cap_rows, **i32)
 
     def route(self, x: torch.Tensor, l: int) -> torch.Tensor:
         return route_device(x, self.layers[l])
@@ -106,6 +114,20 @@ class CudaEpKernels:
         capacity send buffer BEFORE the host waits, so the pack overlaps the read-back."""
         T = route.shape[0]
         sp = stream_ptr()
+        if self.peer_cap:  # fixed splits: no host read-back, graph-capturable
+            _lib.call("mp_ep_plan_cap", ptr(route), T, ptr(C), self.G, self.E, self.rank, self.max_slots, 1,
+                      self.peer_cap, ptr(self.overflow), ptr(res), ptr(self.sc), ptr(self.rc), ptr(self.nloc),
+                      ptr(self.send_pos), ptr(self.piece_row), ptr(self.piece_rows), ptr(self.exp_begin),
+                      ptr(self.ws), self.ws_n, sp)
+            n = self.G * self.peer_cap
+            if x is not None:
+                _lib.call("mp_ep_pack", ptr(x), T, self.d, ptr(self.send_pos), ptr(self.sendbuf), sp)
+            _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
+                      ptr(self.recv_of_local), ptr(self.ws), self.ws_n, sp)
+            self._packed_for = x
+            self._layout_ready = True
+            return EpPlan([self.peer_cap] * self.G, [self.peer_cap] * self.G, n, self.send_pos[:T], self.piece_row,
+                          self.piece_rows, self.exp_begin)
         _lib.call("mp_ep_plan", ptr(route), T, ptr(C), self.G, self.E, self.rank, self.max_slots, 1, ptr(res),
                   ptr(self.sc), ptr(self.rc), ptr(self.nloc), ptr(self.send_pos), ptr(self.piece_row),
                   ptr(self.piece_rows), ptr(self.exp_begin), ptr(self.ws), self.ws_n, sp)
@@ -151,9 +173,10 @@ class CudaEpKernels:
             _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
                       ptr(self.recv_of_local), ptr(self.ws), self.ws_n, stream_ptr())
         self._layout_ready = False
-        # xperm region of the FFN workspace <- received rows in local (slot-major) order
-        _lib.call("mp_gather_rows_bf16", ptr(recvbuf), n, self.d, ptr(self.recv_of_local), ptr(self.ffn_ws),
-                  stream_ptr())
+        # xperm region of the FFN workspace <- received rows in local (slot-major) order (fixed
+        # splits: the number of local rows stays on the device)
+        _lib.call("mp_gather_rows_bf16_dn", ptr(recvbuf), n, self.d, ptr(self.recv_of_local),
+                  ptr(self.nloc) if self.peer_cap else None, ptr(self.ffn_ws), stream_ptr())
         sp = stream_ptr()
         if ev is not None:
             ev[0].record(sp)

@@ -160,3 +160,58 @@ def test_overlapped_pipeline_equals_sequential():
     assert torch.equal(ov.xbuf[0], outs[2]) and torch.equal(ov.xbuf[1], outs[3])
     assert torch.equal(ovl.res, res[3])
     assert torch.equal(ov.assign[1], seq.assign)  # batch 3's predicted table
+
+
+def test_fixed_split_expert_parallel_step_graph_and_rollback():
+    """Fixed-split EP dispatch through a real NCCL group (world size 1, collectives forced):
+    the eager step and a CUDA graph of the whole step (all-gathers and static all-to-alls
+    captured) give the single-device step's bits; a split too small for the layers is
+    detected once per step, rolled back (stream and residency) and re-run compactly."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        cfg = PipelineConfig(num_layers=3, num_experts=32, d_model=256, d_ff=512, tokens=4096, sru_layers=3,
+                             capacity=64, seed=5)
+        a = MoEPipeline(cfg)
+        emb, _, _ = a.wl.batch(cfg.tokens)
+        xa = emb.clone()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            a.step(xa)
+            b = MoEPipeline(cfg)
+            b.enable_expert_parallel(peer_cap=None)
+            b.force_collectives = True
+            assert b.ep.k.peer_cap == cfg.tokens
+            xb = emb.clone()
+            b.step(xb)  # eager fixed-split step (plans residency for the replays below)
+            torch.cuda.synchronize()
+            assert torch.equal(xa, xb)
+            g = b.capture(xb)
+            for _ in range(2):
+                xb.copy_(emb)
+                g.replay()
+            torch.cuda.synchronize()
+            assert not b.ep_overflowed()
+            assert torch.equal(xa, xb)
+            g.destroy()  # a graph holding captured NCCL collectives goes before its process group
+            # a fixed split of 64 rows cannot hold the layer: flagged, rolled back, re-run compactly
+            c = MoEPipeline(cfg)
+            c.enable_expert_parallel(peer_cap=64)
+            c.force_collectives = True
+            xc = emb.clone()
+            c.step(xc)
+            torch.cuda.synchronize()
+            assert c.ep.k.peer_cap == 64 and not c.ep_overflowed()
+            assert torch.equal(xa, xc)
+            assert torch.equal(c.res, b.res)
+    finally:
+        dist.destroy_process_group()

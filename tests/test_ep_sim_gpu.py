@@ -117,3 +117,57 @@ def test_ep_plan_over_capacity_raises_before_collectives():
     res = torch.full((E,), 3, dtype=torch.int32, device=dev)  # 24 slots > max_slots = 8
     with pytest.raises(ConfigurationError):
         k.plan(route, C, res)
+
+
+@pytest.mark.parametrize("G,E,d,F,T,replicas", [(2, 16, 256, 512, 700, True), (4, 16, 768, 3072, 300, True),
+                                                 (8, 32, 256, 512, 300, False)])
+def test_simulated_fixed_split_ep_equals_single_device(G, E, d, F, T, replicas):
+    """Fixed-split dispatch (static all-to-all splits of peer_cap rows per (source, destination)
+    block, graph-capturable): same bits as the single-device forward, no overflow."""
+    from paper_2605_11537_b200.ep import CudaEpKernels
+    from paper_2605_11537_b200.router_oracle import _device_moe, _run_layers_device
+
+    dev = require_device()
+    L = 2
+    params = _params(L, E, d, F, seed=7 * G + E)
+    rng = np.random.default_rng(100 + G)
+    pop = 1.0 / (rng.permutation(E) + 1.0) ** 1.2
+    e0 = rng.choice(E, size=G * T, p=pop / pop.sum())
+    x0 = (params.router_weights[0][e0] * 0.05 + rng.normal(size=(G * T, d)) * 0.5).astype(np.float32)
+    x_ref = torch.from_numpy(x0).to(dev)
+    _run_layers_device(x_ref, _device_moe(params, dev))
+    dm = _device_moe(params, dev)
+    _tile(dm, E, d, F, _lib.size_query("mp_ffn_down_bn", d))
+    res0 = (rng.integers(0, 4, size=(L, E)) if replicas else np.zeros((L, E))).astype(np.int32)
+    capacity = int(res0.sum(1).max()) + E
+    cap = T if G == 1 else -(-2 * T // G)
+    ks = [CudaEpKernels(dm.layers, T, G, r, G * capacity + E, peer_cap=cap) for r in range(G)]
+    res = [torch.from_numpy(res0.copy()).to(dev) for _ in range(G)]
+    xs = [torch.from_numpy(x0[r * T:(r + 1) * T].copy()).to(dev) for r in range(G)]
+    _simulate(ks, xs, res, L)
+    torch.cuda.synchronize()
+    assert all(int(k.overflow.item()) == 0 for k in ks)
+    assert torch.equal(torch.cat(xs), x_ref)
+
+
+def test_simulated_fixed_split_overflow_is_a_flagged_no_op():
+    """A fixed split too small for the layer: EVERY rank flags the overflow (the decision comes
+    from the all-gathered counts, so the ranks agree and re-run together) and the layer leaves
+    every rank's residual stream untouched."""
+    from paper_2605_11537_b200.ep import CudaEpKernels
+    from paper_2605_11537_b200.router_oracle import _device_moe
+
+    dev = require_device()
+    G, E, d, F, T = 4, 16, 256, 512, 400
+    params = _params(1, E, d, F, seed=11)
+    dm = _device_moe(params, dev)
+    _tile(dm, E, d, F, _lib.size_query("mp_ffn_down_bn", d))
+    rng = np.random.default_rng(5)
+    x0 = rng.normal(size=(G * T, d)).astype(np.float32)
+    ks = [CudaEpKernels(dm.layers, T, G, r, G * (E + 8) + E, peer_cap=16) for r in range(G)]
+    res = [torch.zeros(1, E, dtype=torch.int32, device=dev) for _ in range(G)]
+    xs = [torch.from_numpy(x0[r * T:(r + 1) * T].copy()).to(dev) for r in range(G)]
+    _simulate(ks, xs, res, 1)
+    torch.cuda.synchronize()
+    assert all(int(k.overflow.item()) == 1 for k in ks)
+    assert torch.equal(torch.cat(xs).cpu(), torch.from_numpy(x0))
