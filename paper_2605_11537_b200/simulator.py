@@ -30,9 +30,9 @@ import torch
 
 from . import _lib
 from ._dev import ptr, require_device, stream_ptr
-from .errors import ConfigurationError, InfeasibleCapacityError, MetricError
+from .errors import ConfigurationError, MetricError
 from .placement import LOAD, OFFLOAD, REPLICATE, DeviceState, TransferLog, apply_batch, execution_map
-from .planner import ReplicaPlan, cap_replicas, check_positive, demand_counts
+from .planner import ReplicaPlan, check_positive, plan_layers_with_fallback
 from .predictor import HashTable, SruParams, evaluate_accuracy, predict_batch
 from .router_oracle import LayerPlacement, Placement
 
@@ -229,17 +229,9 @@ class BatchRunner:
         raise ConfigurationError("params must be SruParams or 'oracle'")
 
     def _plan(self, table: HashTable) -> ReplicaPlan:
-        layers = []
-        for layer in range(table.num_layers):
-            demand = demand_counts(table, layer)
-            if self.strategy == DISTINCT_ONLY:
-                layers.append({e: 1 for e in demand})
-                continue
-            try:
-                layers.append(cap_replicas(demand, self.capacity))
-            except InfeasibleCapacityError:
-                layers.append({})  # apply_layer degrades to distinct-only and flags it
-        return ReplicaPlan(capacity=self.capacity, layers=layers)
+        """BatchRunner._plan (src/simulator.py:135-146) on the GPU planner: distinct-only caps, or
+        capped replicas with an empty (fallback) plan for an infeasible layer."""
+        return plan_layers_with_fallback(table, self.capacity, distinct_only=self.strategy == DISTINCT_ONLY)
 
     def run_batch(self, batch, table: HashTable | None = None) -> BatchOutcome:
         if table is None:
@@ -302,26 +294,20 @@ class StrategyResult:
 
 
 def aggregate_metrics(per_batch: list[Metrics]) -> Metrics:
-    """Totals over batches; utilization time-weighted by slot time (src/simulator.py:245-265)."""
+    """Totals over batches; utilization time-weighted by slot time, stalls added to the latency
+    (src/simulator.py:245-265)."""
     if not per_batch:
         raise MetricError("cannot aggregate zero batches")
-    latency = sum(m.batch_latency + m.stall_time for m in per_batch)
-    busy = sum(m.busy_time for m in per_batch)
-    slot_time = sum(m.slot_time for m in per_batch)
-    tokens = sum(m.num_tokens for m in per_batch)
-    if latency <= 0 or slot_time <= 0:
+    tot = {f: sum(getattr(m, f) for m in per_batch)
+           for f in ("batch_latency", "stall_time", "transfer_time", "busy_time", "slot_time", "num_tokens")}
+    latency = sum(m.batch_latency + m.stall_time for m in per_batch)  # per-batch sums, in batch order
+    if latency <= 0 or tot["slot_time"] <= 0:
         raise MetricError("aggregate latency must be positive")
-    return Metrics(
-        batch_latency=latency,
-        throughput=tokens / latency,
-        utilization=min(1.0, busy / slot_time),
-        stall_time=sum(m.stall_time for m in per_batch),
-        transfer_time=sum(m.transfer_time for m in per_batch),
-        busy_time=busy,
-        slot_time=slot_time,
-        num_tokens=tokens,
-        prediction_accuracy=float(np.mean([m.prediction_accuracy for m in per_batch])),
-    )
+    return Metrics(batch_latency=latency, throughput=tot["num_tokens"] / latency,
+                   utilization=min(1.0, tot["busy_time"] / tot["slot_time"]), stall_time=tot["stall_time"],
+                   transfer_time=tot["transfer_time"], busy_time=tot["busy_time"], slot_time=tot["slot_time"],
+                   num_tokens=tot["num_tokens"],
+                   prediction_accuracy=float(np.mean([m.prediction_accuracy for m in per_batch])))
 
 
 def simulate_strategy(trace, strategy: str, capacity: int, params=ORACLE_PREDICTOR,
