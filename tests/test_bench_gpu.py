@@ -42,3 +42,9 @@ def test_bench_prints_one_contract_line():
     alg = d["roofline"]["algorithmic_bytes_per_layer"]
     t = (d["roofline"]["ms_gemm1"] + d["roofline"]["ms_gemm2"]) * 1e-3
     assert abs(alg / t / 1e9 - d["roofline"]["achieved"]) <= 1e-6 * d["roofline"]["achieved"]
+    # the numpy drop-in API chain reproduces the engine's bits; cost-model rows from device counts
+    assert d["e2e_api"]["output_equals_engine_bitwise"] is True and d["e2e_api"]["value"] > 0
+    cm = d["cost_model"]
+    assert len(cm["slots_per_layer"]) == 2 and cm["metrics_cost_model"]["num_tokens"] == 2048
+    # measured makespans = each layer's GEMM1 + GEMM2 ms (the roofline's per-layer means x 2 layers)
+    assert cm["metrics_measured_ms"]["batch_latency"] == pytest.approx(2 * t * 1e3, rel=1e-9)
