@@ -486,7 +486,7 @@ def run_ours(args):
 
     from paper_2605_11537_b200.engine import DeviceEvent
 
-    ev = [[DeviceEvent() for _ in range(3)] for _ in range(L)]
+    ev = [[DeviceEvent() for _ in range(7 if ep else 3)] for _ in range(L)]  # EP: + dispatch / combine a2a
     graph = None
     overlap = None
     if args.overlap == "on" and not ep and not args.no_graph:
@@ -541,6 +541,23 @@ def run_ours(args):
     # GEMM launch durations of the last timed step (events recorded inside the step / graph)
     up = [ev[l][0].elapsed_ms(ev[l][1]) for l in range(L)]
     down = [ev[l][1].elapsed_ms(ev[l][2]) for l in range(L)]
+    a2a = None
+    if ep:  # the dispatch (bf16 rows) and combine (fp32 rows) all-to-alls vs NVLink (north star)
+        k = pipe.ep.k
+        disp = sum(ev[l][3].elapsed_ms(ev[l][4]) for l in range(L)) / L
+        comb = sum(ev[l][5].elapsed_ms(ev[l][6]) for l in range(L)) / L
+        rows = world * k.peer_cap if k.peer_cap else T  # rows each rank sends per layer (compact: ~T)
+        remote = rows * (world - 1) / world if world > 1 else 0
+        nvlink = 900.0  # GB/s per direction per GPU, NVLink 5 (nominal)
+        bd, bc = remote * d * 2, remote * d * 4
+        a2a = {"dispatch_ms": disp, "combine_ms": comb, "dispatch_bytes_off_gpu": bd, "combine_bytes_off_gpu": bc,
+               "dispatch_GBs": bd / (disp * 1e-3) / 1e9 if disp > 0 else None,
+               "combine_GBs": bc / (comb * 1e-3) / 1e9 if comb > 0 else None, "nvlink_peak_GBs": nvlink,
+               "dispatch_frac": bd / (disp * 1e-3) / 1e9 / nvlink if disp > 0 else None,
+               "combine_frac": bc / (comb * 1e-3) / 1e9 / nvlink if comb > 0 else None,
+               "peak_source": "nominal NVLink 5, 900 GB/s per direction per GPU",
+               "how": "CUDA events around each layer's all-to-alls in an instrumented replay; bytes = rows this "
+                      "rank sends to other GPUs (fixed-split: G x peer_cap rows incl. padding)"}
 
     # exact routing / predictor accuracy of the last step (not timed)
     last = batches[(args.steps - 1) % len(batches)]
@@ -637,7 +654,8 @@ def run_ours(args):
         "cuda_graph": graph is not None or overlap is not None,
         "overlap": overlap is not None,
         "ep_dispatch": ({"mode": "fixed-split" if ep_graph else "compact", "peer_cap_rows": pipe.ep.k.peer_cap,
-                         "overflowed": pipe.ep_overflowed() if ep_graph else False} if ep else None),
+                         "overflowed": pipe.ep_overflowed() if ep_graph else False, "all_to_all": a2a}
+                        if ep else None),
     }
 
     result["config"]["ffn_kernels"] = pipe.cfg.ffn  # resolved from --ffn auto

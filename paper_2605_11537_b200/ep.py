@@ -233,11 +233,20 @@ class ExpertParallelMoE:
         n_recv = sum(plan.recv_counts)
         recvbuf = k.recv_buffer(n_recv) if early else \
             torch.empty(n_recv, x.shape[1], dtype=sendbuf.dtype, device=sendbuf.device)
+        timed = ev is not None and len(ev) >= 7  # events 3..6 bracket the dispatch and combine all-to-alls
+        if timed:
+            ev[3].record(stream_ptr())
         self._a2a(recvbuf, sendbuf, plan.recv_counts, plan.send_counts)
+        if timed:
+            ev[4].record(stream_ptr())
         y = k.expert_ffn(recvbuf, plan, l, ev) if ev is not None else k.expert_ffn(recvbuf, plan, l)
         n_send = sum(plan.send_counts)
         yback = k.back_buffer(n_send) if early else torch.empty(n_send, x.shape[1], dtype=y.dtype, device=y.device)
+        if timed:
+            ev[5].record(stream_ptr())
         self._a2a(yback, y, plan.send_counts, plan.recv_counts)
+        if timed:
+            ev[6].record(stream_ptr())
         k.combine(x, yback, plan)
         self.last_route = route
         return x
