@@ -68,6 +68,8 @@ def parse_args():
     p.add_argument("--no-baselines", action="store_true", help="skip the same-run baseline measurements")
     p.add_argument("--no-checks", action="store_true", help="skip the float correctness checks")
     p.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
+    p.add_argument("--ep-cap-factor", type=float, default=1.25,
+                   help="fixed-split EP: rows per peer block = factor x tokens / GPUs")
     p.add_argument("--ep-compact", action="store_true",
                    help="expert parallelism with split sizes read back every layer (no step graph)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
@@ -462,9 +464,9 @@ def run_ours(args):
     T, d, L = cfg.tokens, cfg.d_model, cfg.num_layers
     ep = world > 1 or args.ep
     if ep:
-        # fixed-split dispatch (2 T / G rows per peer block): graph-capturable; --ep-compact reads
+        # fixed-split dispatch (1.25 T / G rows per peer block): graph-capturable; --ep-compact reads
         # the split sizes back every layer instead
-        pipe.enable_expert_parallel(peer_cap=0 if args.ep_compact else None)
+        pipe.enable_expert_parallel(peer_cap=0 if args.ep_compact else None, cap_factor=args.ep_cap_factor)
     ep_graph = ep and not args.ep_compact
     weights_same = weights_hash_equal(pipe, world)
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]

@@ -365,16 +365,19 @@ class MoEPipeline:
         return n + 2
 
     # ------------------------------------------------------------------ expert parallelism
-    def enable_expert_parallel(self, group=None, peer_cap: int | None = 0) -> None:
+    def enable_expert_parallel(self, group=None, peer_cap: int | None = 0, cap_factor: float = 1.25) -> None:
         """Shard experts' work over the ranks of ``group`` (one process per GPU, NCCL):
         every rank keeps all weights, routes its own tokens and dispatches them to the GPU
         hosting their replica (paper_2605_11537_b200/ep.py). Residency is planned from the
         all-gathered predicted assignments so every rank holds the same state.
 
         ``peer_cap`` > 0: fixed-split dispatch with that many rows per (source, destination)
-        block -- no host read-back, the step can be captured in a CUDA graph; ``None``: the
-        default capacity 2 T / G rows (T at G = 1); 0: compact dispatch (split sizes read
-        back once per layer)."""
+        block -- no host read-back, the step can be captured in a CUDA graph; ``None``:
+        cap_factor x T / G rows rounded up to 128 (T at G = 1): the row-budgeted replica
+        placement gives every GPU ~T rows, ~T / G from each source, so 25 % headroom covers
+        statistically similar shards (a layer that needs more is re-run compactly); 0: compact
+        dispatch (split sizes read back once per layer). The padding travels: the all-to-alls
+        move G x peer_cap rows."""
         import torch.distributed as dist
 
         from .errors import ConfigurationError
@@ -391,7 +394,8 @@ class MoEPipeline:
         cfg = self.cfg
         # slots of the global plan: G * C capacity slots + at most one corrective replica per expert
         if peer_cap is None:
-            peer_cap = cfg.tokens if self.world == 1 else min(cfg.tokens, -(-2 * cfg.tokens // self.world))
+            want = math.ceil(cap_factor * cfg.tokens / self.world / 128) * 128
+            peer_cap = cfg.tokens if self.world == 1 else min(cfg.tokens, want)
         k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.world * cfg.capacity + cfg.num_experts,
                           peer_cap=peer_cap)
         self.ep = ExpertParallelMoE(k, cfg.num_layers, cfg.num_experts, group)
