@@ -43,20 +43,26 @@ def _fingerprint() -> str:
     return h.hexdigest()[:16]
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile csrc/*.cu into libmoempmc.so (skipped when sources are unchanged)."""
-    stamp = PKG / ".libmoempmc.stamp"
-    fp = _fingerprint()
-    if LIB.exists() and stamp.exists() and stamp.read_text().strip() == fp and not force:
-        return LIB
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          out: Path | None = None) -> Path:
+    """Compile csrc/*.cu into libmoempmc.so (skipped when sources are unchanged).
+
+    ``extra``/``out``: diagnostic builds (e.g. ``-DMP_UNIT_TRACE`` into another file, used by
+    tools/); the product library is always the plain build."""
+    lib = Path(out) if out is not None else LIB
+    extra = list(extra or [])
+    stamp = lib.with_name("." + lib.stem + ".stamp")
+    fp = _fingerprint() + " ".join(extra)
+    if lib.exists() and stamp.exists() and stamp.read_text().strip() == fp and not force:
+        return lib
     nvcc = os.environ.get("NVCC", "nvcc")
-    objdir = ROOT / "build" / "obj"
+    objdir = ROOT / "build" / ("obj" if not extra else "obj_" + hashlib.sha256(" ".join(extra).encode()).hexdigest()[:8])
     objdir.mkdir(parents=True, exist_ok=True)
     objs = []
     procs = []
     for src in _sources():
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *extra, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -71,12 +77,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if failed:
         msg = "\n".join(f"--- {s.name}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc, *NVCC_FLAGS, "-shared", "-o", str(tmp), *map(str, objs), "-ldl", "-lpthread", "-lrt"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     stamp.write_text(fp + "\n")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

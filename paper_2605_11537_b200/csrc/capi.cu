@@ -11,6 +11,9 @@
 
 #include "epilogues.cuh"
 #include "launch.cuh"
+#ifdef MP_DIAG
+#include "gemm2_sm100.cuh"
+#endif
 
 static thread_local char g_err[1024] = "";
 
@@ -143,11 +146,27 @@ int gemm_bf16(const void* A, const void* B, void* C, int M, int N, int K, int c_
   const int units = cdiv(M, kBlockM) * (N / bn);
   const int cap = grid_cap > 0 ? std::min(grid_cap, num_sms()) : num_sms();
   const int grid = units < cap ? units : cap;
-  if (c_dtype == 0 && bn == 256 && ldc > 0) {  // bf16 tile through TMA bulk stores
+#ifdef MP_DIAG
+  const bool diag_lsu = getenv("MP_DIAG_LSU") != nullptr;  // diagnostic: st.global epilogue
+  if (getenv("MP_DIAG_HINT")) store_hint = atoi(getenv("MP_DIAG_HINT"));
+#else
+  constexpr bool diag_lsu = false;
+#endif
+  if (c_dtype == 0 && bn == 256 && ldc > 0 && !diag_lsu) {  // bf16 tile through TMA bulk stores
     CUtensorMap tc;
     rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
     if (rc) return rc;
     EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, bias, act, sig_from, store_hint};
+#ifdef MP_DIAG
+    if (getenv("MP_DIAG_PAIR")) {
+      CUtensorMap tb2;
+      rc = make_tmap_bf16(&tb2, B, N, K, K, 128);
+      if (rc) return rc;
+      Dense2Sched s2{M, N / 256, K / 64, 256};
+      const int units2 = cdiv(M, 2 * kBlockM) * (N / 256);
+      return launch_gemm2<256, 6>(ta, tb2, s2, et, std::min(2 * units2, grid & ~1), st, &tc);
+    }
+#endif
     return launch_gemm<256, 4>(ta, tb, s, et, grid, st, &tc);
   }
   if (c_dtype == 0) {
@@ -309,3 +328,33 @@ extern "C" int mp_l2_persist(void* ptr, size_t bytes, float hit_ratio, void* str
   return MP_OK;
 }
 
+
+#ifdef MP_DIAG
+extern "C" __attribute__((visibility("default"))) int mp_debug_set_epi(int flags) {
+  MP_CUDA_TRY(cudaMemcpyToSymbol(mp::g_diag_epi, &flags, sizeof(int)));
+  return MP_OK;
+}
+
+// Diagnostic build only: the dense CTA-pair (cta_group::2) GEMM on the same operands as
+// mp_gemm_bf16 (bf16 out through TMA stores; ldc == 0: no stores), for single-vs-pair probes.
+extern "C" __attribute__((visibility("default"))) int mp_debug_gemm_pair(const void* A, const void* B, void* C, int M,
+                                                                         int N, int K, int ldc, void* stream) {
+  MP_REQUIRE(M >= 1 && K % 64 == 0 && N % 256 == 0, MP_ERR_CONFIG, "mp_debug_gemm_pair: K%%64, N%%256");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUtensorMap ta, tb, tc;
+  int rc = make_tmap_bf16(&ta, A, M, K, K, kBlockM);
+  if (!rc) rc = make_tmap_bf16(&tb, B, N, K, K, 128);
+  if (rc) return rc;
+  Dense2Sched s{M, N / 256, K / 64, 256};
+  const int units = cdiv(M, 2 * kBlockM) * (N / 256);
+  const int grid = std::min(2 * units, num_sms() & ~1);
+  if (ldc > 0) {
+    rc = make_tmap_bf16_store(&tc, C, M, N, ldc);
+    if (rc) return rc;
+    EpiStoreBf16Tma et{(__nv_bfloat16*)C, ldc, nullptr, 0, 0, 0};
+    return launch_gemm2<256, 6>(ta, tb, s, et, grid, st, &tc);
+  }
+  EpiStoreBf16 e{(__nv_bfloat16*)C, 0, nullptr, 0, 0};
+  return launch_gemm2<256, 6>(ta, tb, s, e, grid, st);
+}
+#endif

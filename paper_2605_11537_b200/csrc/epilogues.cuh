@@ -5,6 +5,11 @@
 
 namespace mp {
 
+#ifdef MP_DIAG
+// Diagnostic build only: bit 0 = the TMA-store epilogue packs its boxes but issues no store.
+static __device__ int g_diag_epi;
+#endif
+
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -165,6 +170,12 @@ struct EpiStoreBf16Tma {
         }
         fence_proxy_async();
         __syncwarp();
+#ifdef MP_DIAG
+        if (g_diag_epi & 1) {
+          __syncwarp();
+          return;
+        }
+#endif
         if (lane == 0) {
           if (keep_l2 == 1)
             tma_store_2d_hint(tm, box, U.n0 + c0 + c, U.a_row + row0, policy_evict_last());

@@ -239,3 +239,13 @@ extern "C" int mp_debug_cta_times(unsigned long long* t0, unsigned long long* t1
   MP_CUDA_TRY(cudaMemcpyFromSymbol(t1, mp::g_cta_t1, sizeof(unsigned long long) * n));
   return MP_OK;
 }
+
+#ifdef MP_DIAG
+extern "C" __attribute__((visibility("default"))) int mp_debug_unit_trace(unsigned long long* out, int n) {
+  MP_REQUIRE(n >= 1 && n <= mp::kTraceUnits, MP_ERR_CONFIG, "mp_debug_unit_trace: n in [1, %d]", mp::kTraceUnits);
+  for (int k = 0; k < 4; ++k)
+    MP_CUDA_TRY(cudaMemcpyFromSymbol(out + (size_t)k * n, mp::g_unit_t, sizeof(unsigned long long) * n,
+                                     sizeof(unsigned long long) * mp::kTraceUnits * k));
+  return MP_OK;
+}
+#endif

@@ -51,6 +51,21 @@ struct TmaStoreOf<E, decltype(void(E::kTmaStore))> {
 // copy of ffn.cu, i.e. the grouped expert GEMMs).
 static __device__ unsigned long long g_cta_t0[1024];
 static __device__ unsigned long long g_cta_t1[1024];
+#ifdef MP_DIAG
+// Diagnostic build only (MP_NVCC_EXTRA=-DMP_DIAG): per-unit %globaltimer stamps of the
+// last launch -- [0] producer issues the unit's first load, [1] MMA sees its first k-block,
+// [2] MMA has issued its last k-block, [3] CTA.
+constexpr int kTraceUnits = 8192;
+static __device__ unsigned long long g_unit_t[4][kTraceUnits];
+#define MP_TRACE(k, u, v) \
+  do {                    \
+    if ((u) < kTraceUnits) g_unit_t[k][u] = (v); \
+  } while (0)
+#else
+#define MP_TRACE(k, u, v) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -165,6 +180,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int kb = 0; kb < nkb; ++kb) {
             if constexpr (ASTAGES == 0) {
               mbar_wait(&empty[stage], phase ^ 1);
+              if (mt == 0 && kb == 0) {
+                MP_TRACE(0, u, global_ns());
+                MP_TRACE(3, u, (unsigned long long)blockIdx.x);
+              }
               uint8_t* sa = smem + stage * L::kStageBytes;
               uint8_t* sb = sa + L::kABytes;
               mbar_arrive_expect_tx(&full[stage], L::kStageBytes);
@@ -221,6 +240,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t d_tmem = tmem_base + as * BN;
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&full[stage], phase);
+            if (mt == 0 && kb == 0) MP_TRACE(1, u, global_ns());
             uint64_t adesc, bdesc;
             if constexpr (ASTAGES == 0) {
               const uint8_t* sa = smem + stage * L::kStageBytes;
@@ -251,6 +271,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
           umma_commit(&tfull[as]);
+          if (mt == mtiles - 1) MP_TRACE(2, u, global_ns());
         }
       }
     }

@@ -41,7 +41,7 @@ def main():
         print(f"M={M} N={N} K={K}: " + "  ".join(f"{k}={v:.1f}us ({fl / v / 1e6:.0f} TF)" for k, v in res.items()))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not ({"--stream", "--pair", "--epi"} & set(sys.argv)):
     main()
 
 
@@ -64,3 +64,80 @@ def stream_probe():
 
 if __name__ == "__main__" and "--stream" in sys.argv:
     stream_probe()
+
+
+def pair_probe():
+    """Single-CTA (M = 128) vs CTA-pair (cta_group::2, M = 256) dense GEMM, with and without
+    the bf16 store, on the diagnostic build (-DMP_DIAG exports mp_debug_gemm_pair)."""
+    import ctypes
+
+    from paper_2605_11537_b200.build import PKG, build
+
+    lib = _lib.load_library(build(extra=["-DMP_DIAG"], out=PKG / "libmoempmc_trace.so"))
+    lib.mp_debug_gemm_pair.restype = ctypes.c_int
+    lib.mp_debug_gemm_pair.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4 + [ctypes.c_void_p]
+    dev = require_device()
+    for (M, N, K) in [(16384, 3072, 768), (16384, 2304, 768), (16384, 768, 3072), (32768, 4096, 4096)]:
+        A = torch.randn(M, K, device=dev).bfloat16()
+        B = torch.randn(N, K, device=dev).bfloat16()
+        C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        C2 = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        fl = 2 * M * N * K
+        res = {}
+        res["single"] = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, N, None, 0, 0,
+                                                 stream_ptr()))
+        res["single_nostore"] = timeit(lambda: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, 0, None,
+                                                         0, 0, stream_ptr()))
+        res["pair"] = timeit(lambda: _lib.check(lib.mp_debug_gemm_pair(ptr(A), ptr(B), ptr(C2), M, N, K, N,
+                                                                       stream_ptr())))
+        res["pair_nostore"] = timeit(lambda: _lib.check(lib.mp_debug_gemm_pair(ptr(A), ptr(B), ptr(C2), M, N, K, 0,
+                                                                               stream_ptr())))
+        res["cublas"] = timeit(lambda: torch.matmul(A, B.T))
+        _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, N, None, 0, 0, stream_ptr())
+        _lib.check(lib.mp_debug_gemm_pair(ptr(A), ptr(B), ptr(C2), M, N, K, N, stream_ptr()))
+        torch.cuda.synchronize()
+        same = bool(torch.equal(C, C2))
+        print(f"M={M} N={N} K={K}: " + "  ".join(f"{k}={v:.1f}us ({fl / v / 1e6:.0f} TF)" for k, v in res.items())
+              + f"  pair==single {same}")
+
+
+if __name__ == "__main__" and "--pair" in sys.argv:
+    pair_probe()
+
+
+def epi_probe():
+    """Where the bf16-store epilogue's cost goes (diagnostic build): TMA bulk stores (product),
+    the same epilogue with the store instructions skipped, st.global stores through the smem
+    transpose (MP_DIAG_LSU), and no epilogue output at all."""
+    import ctypes
+    import os
+
+    from paper_2605_11537_b200.build import PKG, build
+
+    lib = _lib.load_library(build(extra=["-DMP_DIAG"], out=PKG / "libmoempmc_trace.so"))
+    lib.mp_debug_set_epi.restype = ctypes.c_int
+    lib.mp_debug_set_epi.argtypes = [ctypes.c_int]
+    dev = require_device()
+    for (M, N, K) in [(16384, 3072, 768), (16384, 2304, 768)]:
+        A = torch.randn(M, K, device=dev).bfloat16()
+        B = torch.randn(N, K, device=dev).bfloat16()
+        C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        fl = 2 * M * N * K
+        g = lambda ldc: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(C), M, N, K, 0, ldc, None, 0, 0, stream_ptr())
+        res = {"tma": timeit(lambda: g(N))}
+        lib.mp_debug_set_epi(1)
+        res["tma_pack_only"] = timeit(lambda: g(N))
+        lib.mp_debug_set_epi(0)
+        os.environ["MP_DIAG_LSU"] = "1"
+        res["lsu"] = timeit(lambda: g(N))
+        del os.environ["MP_DIAG_LSU"]
+        for h in (1, 2):
+            os.environ["MP_DIAG_HINT"] = str(h)
+            res[f"tma_hint{h}"] = timeit(lambda: g(N))
+        del os.environ["MP_DIAG_HINT"]
+        res["no_output"] = timeit(lambda: g(0))
+        print(f"M={M} N={N} K={K}: " + "  ".join(f"{k}={v:.1f}us ({fl / v / 1e6:.0f} TF)" for k, v in res.items()))
+
+
+if __name__ == "__main__" and "--epi" in sys.argv:
+    epi_probe()
