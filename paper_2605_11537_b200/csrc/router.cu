@@ -82,31 +82,56 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
 
 constexpr int kRfConvThreads = 512;  // convert + epilogue threads (warps 4..19): the split-bf16
                                       // conversion is latency bound, 16 warps keep it under the MMA
-constexpr int kRfRows = 128 / (kRfConvThreads / 8);  // tile rows per converting thread
 constexpr int kRouterThreads = 128 + kRfConvThreads;
 
 // Fused router (Eg <= 128): the split of x into bf16 hi/lo and the bound scale
 // sum_k |x_k| * wabs_k are computed INSIDE the GEMM. A producer warp (warp 3) streams x
-// fp32 k-blocks (two 128 x 32 SWIZZLE_128B boxes) into a 3-deep shared-memory ring; the 8
-// epilogue warps convert them into the two SWIZZLE_128B K-major operand tiles (no T x 2d
-// split buffer goes through HBM, no pre-pass launch). Per k-block (64 columns):
-//   acc[:, 0:Eg)   += x_hi . w_hi^T + x_lo . w_hi^T     (N = Eg MMA on the hi rows)
+// fp32 k-blocks (two 128 x 32 SWIZZLE_128B boxes) into a 3-deep shared-memory ring; the 16
+// convert warps read them into registers and write the bf16 hi / lo operand rows straight
+// into TENSOR memory (tcgen05.st), where the MMA reads its A operand: the split operand
+// never passes through shared memory, whose bandwidth (TMA writes, converter reads, MMA
+// operand reads) bounded the previous form at ~0.85 us per k-block. No T x 2d split buffer
+// goes through HBM, no pre-pass launch. Per k-block (64 columns):
+//   acc[:, 0:Eg)   += x_hi . w_hi^T + x_lo . w_hi^T     (N = Eg MMA on the lo rows)
 //   acc[:, Eg:2Eg) += x_hi . w_lo^T                     (part of one N = 2Eg MMA)
 // with B = [w_hi ; w_lo] stacked as 2Eg rows of one tile; logit = acc[e] + acc[Eg + e].
-// Roles: warp 0 TMA (B), warp 3 TMA (x), warp 1 MMA, warp 2 TMEM, warps 4..11 convert +
-// epilogue. The operand ring is 2 deep.
+// Roles: warp 0 TMA (B), warp 3 TMA (x), warp 1 MMA, warp 2 TMEM, warps 4..19 convert +
+// epilogue (warp w writes TMEM lanes 32 (w % 4) .. +31, k-columns 16 ((w - 4) / 4) .. +15).
+// TMEM: the accumulator (2 Eg columns) then kRxAStages operand stages of 64 columns
+// ([hi: 32 | lo: 32], two bf16 per column).
 constexpr int kRxStages = 3;   // B (router weight) ring
-constexpr int kRxXStages = 3;  // x ring; each stage is converted IN PLACE into the A operand tiles
+constexpr int kRxXStages = 3;  // x ring (fp32 k-blocks, freed once the converters hold them in registers)
+constexpr int kRxAStages = 4;  // TMEM operand stages
+constexpr uint32_t kRxTmemCols = 512;
+#ifdef MP_DIAG
+// Diagnostic build only: per-CTA %globaltimer stamps of the last fused-router launch.
+// [0] start, [1] setup done; per k-block kb < 12: [2 + kb] x issued (producer), [14 + kb]
+// landed, [26 + kb] read into registers, [38 + kb] TMEM stage free, [50 + kb] TMEM stores
+// done (converter warp 4), [62 + kb] operand ready (MMA); [74] accumulator full, [75] end.
+static __device__ unsigned long long g_rt[160][80];
+#define RT_STAMP(i)                                                                   \
+  do {                                                                                \
+    unsigned long long t_;                                                            \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                           \
+    if (blockIdx.x < 160) g_rt[blockIdx.x][i] = t_;                                   \
+  } while (0)
+#else
+#define RT_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
 template <int EG>
 struct RxSmem {
+  static_assert(2 * EG + kRxAStages * 64 <= (int)kRxTmemCols, "router TMEM columns");
   static constexpr int kB = 2 * EG * 128;
-  static constexpr int kA = 128 * 128;
-  static constexpr int kXs = 128 * 64 * 4;  // one x k-block: 128 rows x 64 fp32 as two 16 KB boxes = [hi | lo]
+  static constexpr int kXs = 128 * 64 * 4;  // one x k-block: 128 rows x 64 fp32 as two 16 KB boxes
   static constexpr int kXOffset = kRxStages * kB;
   static constexpr int kBarOffset = kXOffset + kRxXStages * kXs;
-  // bfull[S], bempty[S], xfull[X], conv[X], xempty[X], tfull, tempty
-  static constexpr int kXbOffset = kBarOffset + (2 * kRxStages + 3 * kRxXStages + 2) * 8 + 8;
-  static constexpr int kHistOffset = kXbOffset + 128 * 4;  // EG ints: the tile's expert histogram
+  // bfull[S], bempty[S], xfull[X], xfree[X], conv[A], aempty[A], tfull, tempty
+  static constexpr int kXbOffset = kBarOffset + (2 * kRxStages + 2 * kRxXStages + 2 * kRxAStages + 2) * 8 + 8;
+  static constexpr int kPartOffset = kXbOffset + 128 * 4;   // 4 x 128 partial bound sums
+  static constexpr int kHistOffset = kPartOffset + 4 * 128 * 4;  // EG ints: the tile's expert histogram
   static constexpr int kTopOffset = kHistOffset + EG * 4;  // per column group: best, second (float), best index
   static constexpr int kBytes = kTopOffset + 3 * (EG / 32) * 128 * 4 + 1024;
 };
@@ -125,9 +150,10 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);  // B stage landed
   uint64_t* empty = full + kRxStages;                                     // B stage consumed by the MMA
   uint64_t* xfull = empty + kRxStages;                                    // x stage landed
-  uint64_t* conv = xfull + kRxXStages;                                    // x stage converted to hi | lo
-  uint64_t* xempty = conv + kRxXStages;                                   // hi | lo consumed by the MMA
-  uint64_t* tfull = xempty + kRxXStages;
+  uint64_t* xfree = xfull + kRxXStages;                                   // x stage read by every converter
+  uint64_t* conv = xfree + kRxXStages;                                    // TMEM operand stage written
+  uint64_t* aempty = conv + kRxAStages;                                   // TMEM operand stage consumed
+  uint64_t* tfull = aempty + kRxAStages;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
   float* s_xb = reinterpret_cast<float*>(smem + L::kXbOffset);
@@ -144,19 +170,24 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     }
     for (int s = 0; s < kRxXStages; ++s) {
       mbar_init(&xfull[s], 1);
+      mbar_init(&xfree[s], kRfConvThreads / 32);
+    }
+    for (int s = 0; s < kRxAStages; ++s) {
       mbar_init(&conv[s], kRfConvThreads / 32);
-      mbar_init(&xempty[s], 1);
+      mbar_init(&aempty[s], 1);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 4 * (EG / 32));  // every TMEM-reading epilogue warp
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * EG < 32 ? 32 : 2 * EG);
+  if (threadIdx.x == 0) RT_STAMP(0);
+  if (warp == 2) tmem_alloc(tmem_slot, kRxTmemCols);
   griddep_wait();  // x is the previous layer's output
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) RT_STAMP(1);
 
   if (warp == 0) {
     if (lane == 0) {  // ------------------------------------------------ B producer
@@ -180,11 +211,12 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       uint32_t stage = 0, phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&xempty[stage], phase ^ 1);
+          mbar_wait(&xfree[stage], phase ^ 1);
           uint8_t* sx = smem + L::kXOffset + stage * L::kXs;
           mbar_arrive_expect_tx(&xfull[stage], L::kXs);
           tma_load_2d(sx, &tmX, &xfull[stage], kb * 64, u * kBlockM);  // rows >= T: zero fill
           tma_load_2d(sx + L::kXs / 2, &tmX, &xfull[stage], kb * 64 + 32, u * kBlockM);
+          if (kb < 12) RT_STAMP(2 + kb);
           if (++stage == kRxXStages) {
             stage = 0;
             phase ^= 1;
@@ -196,32 +228,31 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       constexpr uint32_t id_all = idesc_bf16_f32(kBlockM, 2 * EG);
       constexpr uint32_t id_hi = idesc_bf16_f32(kBlockM, EG);
-      uint32_t stage = 0, phase = 0, xstage = 0, xphase = 0, tile = 0;
+      uint32_t stage = 0, phase = 0, astage = 0, aphase = 0, tile = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
         mbar_wait(tempty, (tile & 1) ^ 1);
         tc_fence_after();
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
-          mbar_wait(&conv[xstage], xphase);
+          mbar_wait(&conv[astage], aphase);
           tc_fence_after();
+          if (kb < 12) RT_STAMP(62 + kb);
           const uint64_t bdesc = sw128_kmajor_desc(smem_u32(smem + stage * L::kB));
-          uint8_t* sa = smem + L::kXOffset + xstage * L::kXs;
-          const uint64_t dhi = sw128_kmajor_desc(smem_u32(sa));
-          const uint64_t dlo = sw128_kmajor_desc(smem_u32(sa + L::kA));
+          const uint32_t ahi = tmem_base + 2 * EG + astage * 64, alo = ahi + 32;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            umma_bf16(tmem_base, dhi + 2 * k, bdesc + 2 * k, id_all, (kb | k) != 0);
-            umma_bf16(tmem_base, dlo + 2 * k, bdesc + 2 * k, id_hi, 1);
+          for (int k = 0; k < 4; ++k) {  // K = 16 per MMA = 8 TMEM columns of packed bf16
+            umma_bf16_tmem_a(tmem_base, ahi + 8 * k, bdesc + 2 * k, id_all, (kb | k) != 0);
+            umma_bf16_tmem_a(tmem_base, alo + 8 * k, bdesc + 2 * k, id_hi, 1);
           }
           umma_commit(&empty[stage]);
-          umma_commit(&xempty[xstage]);
+          umma_commit(&aempty[astage]);
           if (++stage == kRxStages) {
             stage = 0;
             phase ^= 1;
           }
-          if (++xstage == kRxXStages) {
-            xstage = 0;
-            xphase ^= 1;
+          if (++astage == kRxAStages) {
+            astage = 0;
+            aphase ^= 1;
           }
         }
         umma_commit(tfull);
@@ -230,9 +261,11 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ convert + epilogue
     const int ct = threadIdx.x - 128;  // 0..kRfConvThreads-1
-    const int jc = ct & 7;             // 32-byte (8 fp32) column chunk of the k-block
-    const int r0 = ct >> 3;            // rows r0 + (kRfConvThreads / 8) i, i < kRfRows
-    const int box = jc >> 2, c16 = (jc & 3) * 2;  // x box (32 columns) and 16-byte chunk inside a 128 B row
+    const int rq = (warp & 3) * 32 + lane;  // tile row = TMEM lane this thread writes
+    const int jq = (warp - 4) >> 2;         // 16-column quarter of the k-block
+    const int box = jq >> 1, c0 = (jq & 1) * 4;  // x box (32 columns) and first 16-byte chunk inside a 128 B row
+    const uint32_t tq = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 2 * EG + 8 * jq;
+    float* s_part = reinterpret_cast<float*>(smem + L::kPartOffset);
     int* s_hist = reinterpret_cast<int*>(smem + L::kHistOffset);
     float* s_top = reinterpret_cast<float*>(smem + L::kTopOffset);
     int* s_topi = reinterpret_cast<int*>(s_top + 2 * (EG / 32) * 128);
@@ -240,71 +273,68 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       for (int e = ct; e < EG; e += kRfConvThreads) s_hist[e] = 0;
       named_bar_sync(1, kRfConvThreads);
     }
-    uint32_t xstage = 0, xphase = 0, tile = 0;
+    uint32_t xstage = 0, xphase = 0, astage = 0, aphase = 0, tile = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++tile) {
       const int row_base = u * kBlockM;
-      float part[kRfRows] = {};
+      float part = 0.f;
       // bound-scale weights of the next k-block are loaded one iteration ahead (L2 latency off
       // the conversion's critical path)
-      float4 w0n = __ldg(reinterpret_cast<const float4*>(wabs + 8 * jc));
-      float4 w1n = __ldg(reinterpret_cast<const float4*>(wabs + 8 * jc + 4));
+      const float4* wq = reinterpret_cast<const float4*>(wabs + 16 * jq);
+      float4 wn[4] = {__ldg(wq), __ldg(wq + 1), __ldg(wq + 2), __ldg(wq + 3)};
       for (int kb = 0; kb < nkb; ++kb) {
-        const float4 w0 = w0n, w1 = w1n;
+        const float4 w[4] = {wn[0], wn[1], wn[2], wn[3]};
         if (kb + 1 < nkb) {
-          w0n = __ldg(reinterpret_cast<const float4*>(wabs + (kb + 1) * 64 + 8 * jc));
-          w1n = __ldg(reinterpret_cast<const float4*>(wabs + (kb + 1) * 64 + 8 * jc + 4));
+          const float4* wk = wq + (kb + 1) * 16;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) wn[i] = __ldg(wk + i);
         }
         mbar_wait(&xfull[xstage], xphase);
-        uint8_t* sxs = smem + L::kXOffset + xstage * L::kXs;
-        const uint32_t sx = smem_u32(sxs + box * (L::kXs / 2));
-        float4 cur[kRfRows][2];
+        if (warp == 4 && lane == 0 && kb < 12) RT_STAMP(14 + kb);
+        const uint32_t sx = smem_u32(smem + L::kXOffset + xstage * L::kXs + box * (L::kXs / 2)) + rq * 128;
+        float4 v[4];
 #pragma unroll
-        for (int i = 0; i < kRfRows; ++i) {
-          const int r = r0 + (kRfConvThreads / 8) * i;
-          cur[i][0] = lds_f4(sx + r * 128 + (((c16) ^ (r & 7)) << 4));
-          cur[i][1] = lds_f4(sx + r * 128 + (((c16 + 1) ^ (r & 7)) << 4));
-        }
-        // every converting thread has its x values in registers before the stage is overwritten
-        // by the operand tiles (hi in the first 16 KB, lo in the second)
-        named_bar_sync(2, kRfConvThreads);
-        uint8_t* shi = sxs;
-        uint8_t* slo = shi + L::kA;
-#pragma unroll
-        for (int i = 0; i < kRfRows; ++i) {
-          const int r = r0 + (kRfConvThreads / 8) * i;
-          const float f[8] = {cur[i][0].x, cur[i][0].y, cur[i][0].z, cur[i][0].w,
-                              cur[i][1].x, cur[i][1].y, cur[i][1].z, cur[i][1].w};
-          uint32_t hw[4], lw[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
-            const float2 hf = __bfloat1622float2(h);
-            const __nv_bfloat162 lo = __floats2bfloat162_rn(f[2 * q] - hf.x, f[2 * q + 1] - hf.y);
-            hw[q] = *reinterpret_cast<const uint32_t*>(&h);
-            lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
-          }
-          const int off = r * 128 + ((jc ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(shi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-          *reinterpret_cast<uint4*>(slo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-          part[i] += fabsf(f[0]) * w0.x + fabsf(f[1]) * w0.y + fabsf(f[2]) * w0.z + fabsf(f[3]) * w0.w +
-                     fabsf(f[4]) * w1.x + fabsf(f[5]) * w1.y + fabsf(f[6]) * w1.z + fabsf(f[7]) * w1.w;
-        }
-        fence_proxy_async();  // generic-proxy operand writes -> the tensor core's async-proxy reads
+        for (int i = 0; i < 4; ++i) v[i] = lds_f4(sx + (((c0 + i) ^ (rq & 7)) << 4));
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[xstage]);
+        if (lane == 0) mbar_arrive(&xfree[xstage]);  // this warp is done with the x stage
+        if (warp == 4 && lane == 0 && kb < 12) RT_STAMP(26 + kb);
         if (++xstage == kRxXStages) {
           xstage = 0;
           xphase ^= 1;
         }
-      }
+        const float f[16] = {v[0].x, v[0].y, v[0].z, v[0].w, v[1].x, v[1].y, v[1].z, v[1].w,
+                             v[2].x, v[2].y, v[2].z, v[2].w, v[3].x, v[3].y, v[3].z, v[3].w};
+        uint32_t hw[8], lw[8];
 #pragma unroll
-      for (int i = 0; i < kRfRows; ++i) {
-        float v = part[i];
-        v += __shfl_xor_sync(0xffffffffu, v, 1);
-        v += __shfl_xor_sync(0xffffffffu, v, 2);
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        if (jc == 0) s_xb[r0 + (kRfConvThreads / 8) * i] = v * 1.0001f + 1e-30f;
+        for (int q = 0; q < 8; ++q) {
+          const __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * q], f[2 * q + 1]);
+          const float2 hf = __bfloat1622float2(h);
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(f[2 * q] - hf.x, f[2 * q + 1] - hf.y);
+          hw[q] = *reinterpret_cast<const uint32_t*>(&h);
+          lw[q] = *reinterpret_cast<const uint32_t*>(&lo);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          part += fabsf(f[4 * i]) * w[i].x + fabsf(f[4 * i + 1]) * w[i].y + fabsf(f[4 * i + 2]) * w[i].z +
+                  fabsf(f[4 * i + 3]) * w[i].w;
+        mbar_wait(&aempty[astage], aphase ^ 1);  // the MMA has read this operand stage
+        tc_fence_after();
+        if (warp == 4 && lane == 0 && kb < 12) RT_STAMP(38 + kb);
+        tmem_st8(tq + astage * 64, hw);
+        tmem_st8(tq + astage * 64 + 32, lw);
+        tmem_st_wait();
+        if (warp == 4 && lane == 0 && kb < 12) RT_STAMP(50 + kb);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[astage]);
+        if (++astage == kRxAStages) {
+          astage = 0;
+          aphase ^= 1;
+        }
       }
+      s_part[jq * 128 + rq] = part;
+      named_bar_sync(1, kRfConvThreads);
+      if (jq == 0)
+        s_xb[rq] = (s_part[rq] + s_part[128 + rq] + s_part[256 + rq] + s_part[384 + rq]) * 1.0001f + 1e-30f;
       named_bar_sync(1, kRfConvThreads);
       // top-2 logits per row: the (EG / 32) column groups of the accumulator are read by
       // (EG / 32) x 4 warps (warp & 3 = TMEM lane quadrant), then merged in expert order
@@ -313,6 +343,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
       if (part_id < kParts) {
         mbar_wait(tfull, tile & 1);
         tc_fence_after();
+        if (warp == 4 && lane == 0) RT_STAMP(74);
         const int r = (warp & 3) * 32 + lane;
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 32 * part_id;
         float a[32], b[32];
@@ -405,9 +436,10 @@ __global__ void __launch_bounds__(kRouterThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) RT_STAMP(75);
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 2 * EG < 32 ? 32 : 2 * EG);
+    tmem_dealloc(tmem_base, kRxTmemCols);
   }
 #endif
 }
@@ -545,3 +577,9 @@ extern "C" int mp_route_top1(const float* x, int ldx, int T, int d, const void* 
   return mp_route_top1_ex(x, ldx, T, d, w_hl, w_f32, wabs, E, Eg, route, ws, ws_bytes, stream);
 }
 
+#ifdef MP_DIAG
+extern "C" __attribute__((visibility("default"))) int mp_debug_router_trace(unsigned long long* out) {
+  MP_CUDA_TRY(cudaMemcpyFromSymbol(out, mp::g_rt, sizeof(mp::g_rt)));
+  return MP_OK;
+}
+#endif
