@@ -72,6 +72,9 @@ def parse_args():
                    help="fixed-split EP: rows per peer block = factor x tokens / GPUs")
     p.add_argument("--ep-compact", action="store_true",
                    help="expert parallelism with split sizes read back every layer (no step graph)")
+    p.add_argument("--ep-p2p", action="store_true",
+                   help="expert parallelism over peer memory: rows written into the destination's receive block, "
+                        "combine fused into GEMM2's epilogue over NVLink, device barriers (no all-to-all)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
     p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")
     p.add_argument("--overlap", choices=["on", "off"], default="off",
@@ -466,7 +469,8 @@ def run_ours(args):
     if ep:
         # fixed-split dispatch (1.25 T / G rows per peer block): graph-capturable; --ep-compact reads
         # the split sizes back every layer instead
-        pipe.enable_expert_parallel(peer_cap=0 if args.ep_compact else None, cap_factor=args.ep_cap_factor)
+        pipe.enable_expert_parallel(peer_cap=0 if args.ep_compact else None, cap_factor=args.ep_cap_factor,
+                                    p2p=args.ep_p2p and not args.ep_compact)
     ep_graph = ep and not args.ep_compact
     weights_same = weights_hash_equal(pipe, world)
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]
@@ -558,8 +562,12 @@ def run_ours(args):
                "dispatch_frac": bd / (disp * 1e-3) / 1e9 / nvlink if disp > 0 else None,
                "combine_frac": bc / (comb * 1e-3) / 1e9 / nvlink if comb > 0 else None,
                "peak_source": "nominal NVLink 5, 900 GB/s per direction per GPU",
-               "how": "CUDA events around each layer's all-to-alls in an instrumented replay; bytes = rows this "
-                      "rank sends to other GPUs (fixed-split: G x peer_cap rows incl. padding)"}
+               "how": ("CUDA events around each layer's peer-memory dispatch (rows stored into the destinations' "
+                       "receive blocks + device barrier) and its closing barrier (the combine itself runs inside "
+                       "GEMM2's epilogue as peer reductions); bytes = rows this rank sends to other GPUs"
+                       if k.p2p else
+                       "CUDA events around each layer's all-to-alls in an instrumented replay; bytes = rows this "
+                       "rank sends to other GPUs (fixed-split: G x peer_cap rows incl. padding)")}
 
     # exact routing / predictor accuracy of the last step (not timed)
     last = batches[(args.steps - 1) % len(batches)]
@@ -655,7 +663,8 @@ def run_ours(args):
         "moe_layers_only": moe_only,
         "cuda_graph": graph is not None or overlap is not None,
         "overlap": overlap is not None,
-        "ep_dispatch": ({"mode": "fixed-split" if ep_graph else "compact", "peer_cap_rows": pipe.ep.k.peer_cap,
+        "ep_dispatch": ({"mode": ("peer-memory" if pipe.ep.k.p2p else "fixed-split") if ep_graph else "compact",
+                         "peer_cap_rows": pipe.ep.k.peer_cap,
                          "overflowed": pipe.ep_overflowed() if ep_graph else False, "all_to_all": a2a}
                         if ep else None),
     }

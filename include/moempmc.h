@@ -365,6 +365,28 @@ MP_API int mp_ep_plan_cap(const int32_t* route, int T, const int32_t* C, int G, 
                           int32_t* piece_rows, int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 MP_API int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
                                   void* out, void* stream);
+/* Peer-memory form of the fixed-split dispatch / combine (NVLink P2P; no all-to-all):
+ * recv_rows / recv_tok / flags / peer_x are DEVICE arrays of G pointers, entry g = rank g's
+ * receive rows (G * peer_cap x d bf16), receive token indices (G * peer_cap int32), barrier
+ * flags (G int32, zero-initialised) and residual stream (T_home x d fp32), mapped into this
+ * process (CUDA IPC; entry `rank` is the local buffer).
+ *   mp_ep_pack_peer    token t -> rank g = send_pos[t] / peer_cap, row rank * peer_cap + j
+ *                      of g's receive rows, and t into g's recv_tok at the same row
+ *   mp_peer_barrier    device barrier of the G ranks (epoch counter in *epoch, one per rank);
+ *                      orders the peer-memory writes before it for every rank after it
+ *   mp_ep_gather_peer  mp_gather_rows_bf16_dn + dst_of_row[r] = home * T_home + t of the row
+ *   mp_ffn_down_peer   GEMM2 whose epilogue ADDS row r into peer_x[home][t] (the combine)
+ * Per layer: plan_cap -> pack_peer -> barrier -> recv_layout -> gather_peer -> ffn_up ->
+ * ffn_down_peer -> barrier. Bit-identical to the all-to-all form (one addend per element). */
+MP_API int mp_ep_pack_peer(const float* x, int T, int d, const int32_t* send_pos, int peer_cap, int rank,
+                           void* const* recv_rows, int32_t* const* recv_tok, void* stream);
+MP_API int mp_peer_barrier(int32_t* const* flags, int rank, int G, int32_t* epoch, void* stream);
+MP_API int mp_ep_gather_peer(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
+                             const int32_t* recv_tok, int peer_cap, int T_home, int32_t* dst_of_row, void* out,
+                             void* stream);
+MP_API int mp_ffn_down_peer(float* const* peer_x, int T_home, int T, int dp, int Fp, int E, const void* v, int flags,
+                            const int32_t* dst_of_row, const int32_t* piece_row, const int32_t* piece_rows,
+                            const int32_t* exp_begin, void* ws, size_t ws_bytes, void* stream);
 
 
 /* Whole-step CUDA graphs (capture on `stream`, replay) and timing events that remain

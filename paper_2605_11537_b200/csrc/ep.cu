@@ -260,6 +260,81 @@ __global__ void k_ep_pack(const float* __restrict__ x, int T, int d, const int32
   }
 }
 
+// Expert parallelism over peer memory (NVLink P2P, fixed-split layout): source rank `rank`
+// writes token t straight into destination g's receive block for it, row rank * peer_cap + j
+// (send_pos[t] = g * peer_cap + j), and the token index beside it, so g's GEMM2 can add the
+// result back into this rank's stream (EpiScatterAdd peer mode). One warp per token.
+__global__ void k_ep_pack_peer(const float* __restrict__ x, int T, int d, const int32_t* __restrict__ send_pos,
+                               int peer_cap, int rank, __nv_bfloat16* const* __restrict__ recv_rows,
+                               int32_t* const* __restrict__ recv_tok) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int sp = t < T ? send_pos[t] : -1;
+  if (sp >= 0) {
+    const int g = sp / peer_cap, row = rank * peer_cap + (sp - g * peer_cap);
+    const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * d);
+    uint2* dst = reinterpret_cast<uint2*>(recv_rows[g] + (size_t)row * d);
+    for (int k = lane; k < d / 4; k += 32) {
+      const float4 v = __ldg(&src[k]);
+      __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+      dst[k] = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+    }
+    if (lane == 0) recv_tok[g][row] = t;
+  }
+  // no fence here: the barrier kernel that follows waits for this grid's completion (memory
+  // flushed) and fences at system scope before it signals -- an on-stream barrier
+}
+
+// Receiver side of the peer-memory path: xperm[row] = recvbuf[idx[row]] and the destination
+// code of the row's result, home * T_home + t (home = idx / peer_cap, t from recv_tok).
+__global__ void k_ep_gather_peer(const __nv_bfloat16* __restrict__ buf, int n, int d, const int32_t* __restrict__ idx,
+                                 const int32_t* __restrict__ n_dev, const int32_t* __restrict__ recv_tok, int peer_cap,
+                                 int T_home, int32_t* __restrict__ dst_of_row, __nv_bfloat16* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n || (n_dev != nullptr && row >= *n_dev)) return;
+  const int ri = __ldg(&idx[row]);
+  const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)ri * d);
+  uint4* dst = reinterpret_cast<uint4*>(out + (size_t)row * d);
+  for (int k = lane; k < d / 8; k += 32) dst[k] = __ldg(&src[k]);
+  if (lane == 0) dst_of_row[row] = (ri / peer_cap) * T_home + recv_tok[ri];
+}
+
+// Device-side barrier over G ranks' flag arrays in peer memory (G <= 32, one warp): epoch e
+// = ++*epoch; lane g publishes e into rank g's slot for this rank (release, system scope),
+// lane s waits until rank s's e has arrived here (acquire). The kernels before it on the
+// stream -- the peer stores and reductions it hands over -- have completed with their memory
+// flushed when griddepcontrol.wait returns, and the system-scope fence orders them before the
+// flags (the pattern of an on-stream barrier: no fence in the producing kernels).
+__global__ void k_peer_barrier(int32_t* const* __restrict__ flags, int rank, int G, int32_t* __restrict__ epoch) {
+  griddep_wait();
+  const int lane = threadIdx.x;
+  int e = 0;
+  if (lane == 0) {
+    e = *epoch + 1;
+    *epoch = e;
+  }
+  e = __shfl_sync(0xffffffffu, e, 0);
+  __threadfence_system();
+  if (lane < G) {
+    int32_t* f = flags[lane] + rank;
+    asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(f), "r"(e) : "memory");
+  }
+  if (lane < G) {
+    const int32_t* f = flags[rank] + lane;
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if (v >= e) break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  griddep_launch_dependents();
+}
+
 // Receiver: local row of every received row, per (source, hosted slot) run.
 // grid (max_slots, G): one block per (slot, source); slots beyond the plan's count exit.
 __global__ void k_ep_recv_map(int G, int max_slots, const int32_t* __restrict__ num_slots_p, int rank, EpPlanWs w,
@@ -420,6 +495,32 @@ extern "C" int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const i
     k_gather_bf16<<<cdiv(n_max * 32, 256), 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)buf, n_max, d, idx,
                                                                              (__nv_bfloat16*)out, n_dev);
   MP_CUDA_TRY(cudaGetLastError());
+  return MP_OK;
+}
+
+extern "C" int mp_ep_pack_peer(const float* x, int T, int d, const int32_t* send_pos, int peer_cap, int rank,
+                               void* const* recv_rows, int32_t* const* recv_tok, void* stream) {
+  MP_REQUIRE(T >= 0 && d % 4 == 0 && peer_cap >= 1 && rank >= 0, MP_ERR_CONFIG, "mp_ep_pack_peer: bad sizes");
+  if (T == 0) return MP_OK;
+  MP_CUDA_TRY(launch_pdl(k_ep_pack_peer, dim3(cdiv(T * 32, 256)), dim3(256), 0, (cudaStream_t)stream, x, T, d,
+                         send_pos, peer_cap, rank, (__nv_bfloat16* const*)recv_rows, recv_tok));
+  return MP_OK;
+}
+
+extern "C" int mp_ep_gather_peer(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
+                                 const int32_t* recv_tok, int peer_cap, int T_home, int32_t* dst_of_row, void* out,
+                                 void* stream) {
+  MP_REQUIRE(n_max >= 0 && d % 8 == 0 && peer_cap >= 1 && T_home >= 1, MP_ERR_CONFIG, "mp_ep_gather_peer: bad sizes");
+  if (n_max == 0) return MP_OK;
+  MP_CUDA_TRY(launch_pdl(k_ep_gather_peer, dim3(cdiv(n_max * 32, 256)), dim3(256), 0, (cudaStream_t)stream,
+                         (const __nv_bfloat16*)buf, n_max, d, idx, n_dev, recv_tok, peer_cap, T_home, dst_of_row,
+                         (__nv_bfloat16*)out));
+  return MP_OK;
+}
+
+extern "C" int mp_peer_barrier(int32_t* const* flags, int rank, int G, int32_t* epoch, void* stream) {
+  MP_REQUIRE(G >= 1 && G <= 32 && rank >= 0 && rank < G, MP_ERR_CONFIG, "mp_peer_barrier: G in [1, 32]");
+  MP_CUDA_TRY(launch_pdl(k_peer_barrier, dim3(1), dim3(32), 0, (cudaStream_t)stream, flags, rank, G, epoch));
   return MP_OK;
 }
 

@@ -234,6 +234,8 @@ struct EpiScatterAdd {
   const int32_t* tok_of_row;
   int store = 0;              // 1: plain stores (x[tok] = y) -- every target row has exactly one
                               //    writer (the expert-parallel receive buffer needs no zeroing)
+  float* const* peer_x = nullptr;  // expert parallelism over peer memory: tok_of_row holds home * peer_T + t
+  int peer_T = 1;                  //    and the row is added into rank home's stream (an NVLink peer address)
   __device__ __forceinline__ const float* colvec() const { return nullptr; }
   template <int NC>
   __device__ __forceinline__ void run(const Unit& U, int mt, int r, uint32_t taddr, int c0, const float*,
@@ -242,12 +244,20 @@ struct EpiScatterAdd {
     const int rr = mt * kBlockM + r;
     const bool ok = rr < U.rows;
     const int tok = ok ? __ldg(&tok_of_row[U.a_row + rr]) : -1;
-    float* base = x + U.n0 + c0;
+    float* rowp = nullptr;  // this thread's destination row (+ the tile's first column)
+    if (tok >= 0)
+      rowp = (peer_x ? reinterpret_cast<float*>(__ldg(reinterpret_cast<const unsigned long long*>(peer_x) +
+                                                      tok / peer_T)) +
+                           (size_t)(tok % peer_T) * ldx
+                     : x + (size_t)tok * ldx) +
+             U.n0 + c0;
     float4* srow = reinterpret_cast<float4*>(scratch + lane * 20);
     const int pq = lane & 3;
-    int tt[4];  // token of the row this lane updates in store step `it`
+    float* tp[4];  // destination row of the row this lane updates in store step `it`
 #pragma unroll
-    for (int it = 0; it < 4; ++it) tt[it] = __shfl_sync(0xffffffffu, tok, it * 8 + (lane >> 2));
+    for (int it = 0; it < 4; ++it)
+      tp[it] = reinterpret_cast<float*>(
+          __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rowp), it * 8 + (lane >> 2)));
     tmem_chunks<NC>(taddr, [&](int c, float* v) {
       // two 16-column halves: lane = row -> smem, then 8 rows x 64 B per instruction.
       // The residual update is a vector reduction performed in L2 (red.global.add.v4.f32):
@@ -263,8 +273,8 @@ struct EpiScatterAdd {
         for (int it = 0; it < 4; ++it) {
           const int row = it * 8 + (lane >> 2);
           const float4 a = *reinterpret_cast<const float4*>(scratch + row * 20 + pq * 4);
-          if (tt[it] >= 0) {
-            float4* dst = reinterpret_cast<float4*>(base + (size_t)tt[it] * ldx + c + 16 * h) + pq;
+          if (tp[it] != nullptr) {
+            float4* dst = reinterpret_cast<float4*>(tp[it] + c + 16 * h) + pq;
             if (store)
               *dst = a;
             else

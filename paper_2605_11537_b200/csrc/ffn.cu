@@ -140,7 +140,7 @@ static int ffn_up(int T, int dp, int Fp, int E, const void* u, const int32_t* pi
 static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const int32_t* tok_of_row,
                     const int32_t* piece_row, const int32_t* piece_rows, const int32_t* exp_begin,
                     const __nv_bfloat16* hid, int flags, cudaStream_t st, const int32_t* piece_wbase = nullptr,
-                    int W = 0) {
+                    int W = 0, float* const* peer_x = nullptr, int peer_T = 1) {
   // GEMM2: y[tok] += hid . V_e^T   [rows x dp], scatter + residual epilogue
   const int tiled = flags & 1, pair = (flags >> 1) & 1;
   const int bn = (pair || (flags & 64)) ? 256 : mp_ffn_down_bn(dp);
@@ -149,7 +149,7 @@ static int ffn_down(float* y, int T, int dp, int Fp, int E, const void* v, const
   int rc = make_tmap_bf16(&ta, hid, T, Fp, Fp, kBlockM);
   if (!rc) rc = tmap_b(&tb, v, piece_wbase ? W : E, dp, Fp, bn, tiled, pair ? bn / 2 : bn);
   if (rc) return rc;
-  EpiScatterAdd e{y, dp, tok_of_row, (flags >> 5) & 1};
+  EpiScatterAdd e{y, dp, tok_of_row, (flags >> 5) & 1, peer_x, peer_T};
   if (pair) {
     Seg2Sched s{piece_row, piece_rows, exp_begin, E, dp / bn, bn, dp, Fp / 64, tiled};
     return launch_gemm2<256, 6>(ta, tb, s, e, num_sms() & ~1, st);
@@ -195,6 +195,20 @@ extern "C" int mp_ffn_down(float* y, int T, int dp, int Fp, int E, const void* v
   FFN_CHECKS();
   return ffn_down(y, T, dp, Fp, E, v, tok_of_row, piece_row, piece_rows, exp_begin, hid, flags,
                   (cudaStream_t)stream);
+}
+
+// Expert parallelism over peer memory: row r's result is ADDED into rank (dst_of_row[r] / T_home)'s
+// residual stream, token dst_of_row[r] % T_home, through the peer pointers peer_x (device array of
+// G float*, NVLink P2P addresses) -- the combine fused into GEMM2's epilogue, no return all-to-all.
+extern "C" int mp_ffn_down_peer(float* const* peer_x, int T_home, int T, int dp, int Fp, int E, const void* v,
+                                int flags, const int32_t* dst_of_row, const int32_t* piece_row,
+                                const int32_t* piece_rows, const int32_t* exp_begin, void* ws, size_t ws_bytes,
+                                void* stream) {
+  FFN_CHECKS();
+  MP_REQUIRE(peer_x != nullptr && T_home >= 1 && !(flags & 2) && !(flags & 32), MP_ERR_CONFIG,
+             "mp_ffn_down_peer: needs the peer table, T_home >= 1, single-CTA kernels and residual adds");
+  return ffn_down(nullptr, T, dp, Fp, E, v, dst_of_row, piece_row, piece_rows, exp_begin, hid, flags,
+                  (cudaStream_t)stream, nullptr, 0, peer_x, T_home);
 }
 
 // Physical replicas: B operand rows of piece p come from weight slot piece_wbase[p] of a pool of W

@@ -365,7 +365,8 @@ class MoEPipeline:
         return n + 2
 
     # ------------------------------------------------------------------ expert parallelism
-    def enable_expert_parallel(self, group=None, peer_cap: int | None = 0, cap_factor: float = 1.25) -> None:
+    def enable_expert_parallel(self, group=None, peer_cap: int | None = 0, cap_factor: float = 1.25,
+                               p2p: bool = False) -> None:
         """Shard experts' work over the ranks of ``group`` (one process per GPU, NCCL):
         every rank keeps all weights, routes its own tokens and dispatches them to the GPU
         hosting their replica (paper_2605_11537_b200/ep.py). Residency is planned from the
@@ -377,7 +378,8 @@ class MoEPipeline:
         placement gives every GPU ~T rows, ~T / G from each source, so 25 % headroom covers
         statistically similar shards (a layer that needs more is re-run compactly); 0: compact
         dispatch (split sizes read back once per layer). The padding travels: the all-to-alls
-        move G x peer_cap rows."""
+        move G x peer_cap rows. ``p2p``: the fixed-split dispatch and combine over peer memory
+        (NVLink P2P through CUDA IPC mappings, no all-to-all; ep.py)."""
         import torch.distributed as dist
 
         from .errors import ConfigurationError
@@ -397,7 +399,9 @@ class MoEPipeline:
             want = math.ceil(cap_factor * cfg.tokens / self.world / 128) * 128
             peer_cap = cfg.tokens if self.world == 1 else min(cfg.tokens, want)
         k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.world * cfg.capacity + cfg.num_experts,
-                          peer_cap=peer_cap)
+                          peer_cap=peer_cap, p2p=p2p)
+        if p2p:
+            k.connect(group)
         self.ep = ExpertParallelMoE(k, cfg.num_layers, cfg.num_experts, group)
         self.ep.res = self.res  # one residency state for placement and execution
         GT = self.world * cfg.tokens

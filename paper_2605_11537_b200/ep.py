@@ -27,6 +27,14 @@ whole step can be captured in one CUDA graph; a layer that would need more than 
 rows for some peer sets an overflow flag and does nothing, and the caller re-runs the step
 in the compact mode (MoEPipeline.step does so, checking the flag once per step).
 
+Peer-memory mode (``p2p``, fixed splits): no all-to-all at all. Every rank maps the other
+ranks' receive buffers, receive-token arrays, barrier flags and residual streams into its
+address space once (CUDA IPC, NVLink P2P on NVSwitch); per layer the source writes its rows
+straight into the destination's receive block (``mp_ep_pack_peer``), a device barrier
+(``mp_peer_barrier``) hands them over, and the destination's GEMM2 epilogue ADDS each result
+row into the home rank's residual stream over NVLink (``mp_ffn_down_peer``: the combine fused
+into the GEMM), followed by a second barrier. Same bits as the all-to-all form.
+
 The kernel layer is pluggable: ``CudaEpKernels`` (the product) or, in the
 CPU multi-process tests only, a numpy restatement from ``oracle/``.
 """
@@ -55,13 +63,39 @@ class EpPlan:
     exp_begin: torch.Tensor
 
 
+class PeerMemory:
+    """Peer address tables of same-role buffers over a process group: torch's CUDA IPC
+    (``UntypedStorage._share_cuda_`` / ``_new_shared_cuda``, i.e. cudaIpcGetMemHandle /
+    cudaIpcOpenMemHandle) exchanged with ``all_gather_object``; entry ``rank`` is the local
+    pointer. The mapped storages are kept alive with this object."""
+
+    def __init__(self, group, world: int, rank: int, dev):
+        self.group, self.world, self.rank, self.dev = group, world, rank, dev
+        self._keep = []
+
+    def table(self, t: torch.Tensor) -> torch.Tensor:
+        """int64 device array: entry g = address of rank g's tensor in the same role as ``t``
+        (collective over the group: every rank calls it with its own tensor)."""
+        ptrs = [t.data_ptr()] * self.world
+        if self.world > 1:
+            off = t.storage_offset() * t.element_size()
+            objs = [None] * self.world
+            dist.all_gather_object(objs, (t.untyped_storage()._share_cuda_(), off), group=self.group)
+            for g, (handle, og) in enumerate(objs):
+                if g != self.rank:
+                    st = torch.UntypedStorage._new_shared_cuda(*handle)
+                    self._keep.append(st)
+                    ptrs[g] = st.data_ptr() + og
+        return torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+
+
 class CudaEpKernels:
     """Device implementation (libmoempmc.so) of the per-rank EP steps."""
 
     dispatch_dtype = torch.bfloat16
 
     def __init__(self, layers: list[DeviceMoeLayer], tokens: int, world: int, rank: int, max_slots: int,
-                 peer_cap: int = 0):
+                 peer_cap: int = 0, p2p: bool = False):
         self.layers = layers
         self.T, self.G, self.rank, self.max_slots = tokens, world, rank, max_slots
         self.peer_cap = int(peer_cap)  # rows per (source, destination) block; 0: compact, sizes read back
@@ -99,6 +133,72 @@ class CudaEpKernels:
         self.piece_rows = torch.empty(self.pstride, **i32)
         self.exp_begin = torch.empty(self.E + 1, **i32)
         self.recv_of_local = torch.zeros(self.cap_rows, **i32)
+        # peer-memory mode: receive-token indices (peer-written), barrier flags + epoch, the
+        # destination code of every local row; the peer tables are set by connect() / set_peers()
+        self.p2p = bool(p2p)
+        if self.p2p:
+            if self.peer_cap <= 0:
+                raise ConfigurationError("peer-memory expert parallelism needs the fixed-split layout (peer_cap > 0)")
+            self.recv_tok = torch.zeros(world * self.peer_cap, **i32)
+            self.flags = torch.zeros(world, **i32)
+            self.epoch = torch.zeros(1, **i32)
+            self.dst_of_row = torch.zeros(self.cap_rows, **i32)
+            self.t_recv = self.t_tok = self.t_flags = self.t_x = None
+            self._x_ptr = None
+            self._mem = None
+
+    # ---------------------------------------------------------------- peer-memory mode
+    def connect(self, group) -> None:
+        """Map the peers' receive buffers, receive-token arrays and flags (collective)."""
+        self._mem = PeerMemory(group, self.G, self.rank, self.dev)
+        self.set_peers(self._mem.table(self.recvbuf), self._mem.table(self.recv_tok), self._mem.table(self.flags))
+
+    def set_peers(self, t_recv: torch.Tensor, t_tok: torch.Tensor, t_flags: torch.Tensor) -> None:
+        self.t_recv, self.t_tok, self.t_flags = t_recv, t_tok, t_flags
+
+    def register_stream(self, x: torch.Tensor, t_x: torch.Tensor = None) -> None:
+        """Map every rank's residual stream (collective when the buffer changes; ``t_x`` given:
+        a table built by the caller, e.g. a simulated job on one device)."""
+        if t_x is not None:
+            self.t_x, self._x_ptr = t_x, x.data_ptr()
+        elif self._x_ptr != x.data_ptr():
+            if torch.cuda.is_current_stream_capturing():
+                raise ConfigurationError("peer-memory expert parallelism: run one eager step on this stream buffer "
+                                         "before capturing (its peer mapping is a collective)")
+            self.t_x, self._x_ptr = self._mem.table(x), x.data_ptr()
+
+    def barrier(self) -> None:
+        _lib.call("mp_peer_barrier", ptr(self.t_flags), self.rank, self.G, ptr(self.epoch), stream_ptr())
+
+    def dispatch_peer(self, x: torch.Tensor, plan: EpPlan) -> None:
+        """Rows straight into the destinations' receive blocks (peer stores); no barrier."""
+        _lib.call("mp_ep_pack_peer", ptr(x), x.shape[0], self.d, ptr(plan.send_pos), self.peer_cap, self.rank,
+                  ptr(self.t_recv), ptr(self.t_tok), stream_ptr())
+
+    def expert_ffn_peer(self, plan: EpPlan, l: int, ev=None) -> None:
+        """Grouped GEMMs on the received rows; GEMM2 adds every result row into its home rank's
+        stream (peer reductions); no barrier."""
+        n = self.G * self.peer_cap
+        lay = self.layers[l]
+        sp = stream_ptr()
+        if not getattr(self, "_layout_ready", False):
+            _lib.call("mp_ep_recv_layout", self.G, self.T, self.E, self.rank, self.max_slots, None,
+                      ptr(self.recv_of_local), ptr(self.ws), self.ws_n, sp)
+        self._layout_ready = False
+        _lib.call("mp_ep_gather_peer", ptr(self.recvbuf), n, self.d, ptr(self.recv_of_local), ptr(self.nloc),
+                  ptr(self.recv_tok), self.peer_cap, self.T, ptr(self.dst_of_row), ptr(self.ffn_ws), sp)
+        if ev is not None:
+            ev[0].record(sp)
+        vflag = 64 if lay.tiled and getattr(lay, "vbn", 0) == 256 else 0
+        _lib.call("mp_ffn_up", n, self.d, self.F, self.E, ptr(lay.U), lay.tiled, ptr(plan.piece_row),
+                  ptr(plan.piece_rows), ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
+        if ev is not None:
+            ev[1].record(sp)
+        _lib.call("mp_ffn_down_peer", ptr(self.t_x), self.T, n, self.d, self.F, self.E, ptr(lay.V),
+                  lay.tiled | vflag, ptr(self.dst_of_row), ptr(plan.piece_row), ptr(plan.piece_rows),
+                  ptr(plan.exp_begin), ptr(self.ffn_ws), self.ffn_n, sp)
+        if ev is not None:
+            ev[2].record(sp)
 
     def route(self, x: torch.Tensor, l: int) -> torch.Tensor:
         return route_device(x, self.layers[l])
@@ -227,6 +327,26 @@ class ExpertParallelMoE:
         k = self.k
         route = k.route(x, l)
         C = self._all_gather_counts(k.counts(route))
+        if getattr(k, "p2p", False) and k.peer_cap:
+            # peer memory: rows to the destinations, barrier, GEMMs whose epilogue adds the results
+            # into the home streams, barrier (the next layer's router reads them)
+            plan = k.plan(route, C, self.res[l])
+            k.register_stream(x)
+            timed = ev is not None and len(ev) >= 7
+            if timed:
+                ev[3].record(stream_ptr())
+            k.dispatch_peer(x, plan)
+            k.barrier()
+            if timed:
+                ev[4].record(stream_ptr())
+            k.expert_ffn_peer(plan, l, ev)
+            if timed:
+                ev[5].record(stream_ptr())
+            k.barrier()
+            if timed:
+                ev[6].record(stream_ptr())
+            self.last_route = route
+            return x
         early = hasattr(k, "recv_buffer")  # device kernels: pack before the host reads the split sizes
         plan = k.plan(route, C, self.res[l], x) if early else k.plan(route, C, self.res[l])
         sendbuf = k.pack(x, plan, sum(plan.send_counts))

@@ -215,3 +215,43 @@ def test_fixed_split_expert_parallel_step_graph_and_rollback():
             assert torch.equal(c.res, b.res)
     finally:
         dist.destroy_process_group()
+
+
+def test_peer_memory_expert_parallel_step_graph_and_rollback():
+    """Peer-memory EP (dispatch into the destination's receive block, combine fused into GEMM2's
+    epilogue, device barriers) at world size 1 -- the peer tables hold this process's own buffers
+    and the barrier waits only on itself: the eager step and a CUDA graph of the whole step give
+    the single-device step's bits; an undersized split is rolled back and re-run compactly."""
+    from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig
+
+    cfg = PipelineConfig(num_layers=3, num_experts=32, d_model=256, d_ff=512, tokens=4096, sru_layers=3,
+                         capacity=64, seed=5)
+    a = MoEPipeline(cfg)
+    emb, _, _ = a.wl.batch(cfg.tokens)
+    xa = emb.clone()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a.step(xa)
+        b = MoEPipeline(cfg)
+        b.enable_expert_parallel(peer_cap=None, p2p=True)
+        assert b.ep.k.p2p and b.ep.k.peer_cap == cfg.tokens
+        xb = emb.clone()
+        b.step(xb)  # eager (maps the stream buffer; plans residency for the replays)
+        torch.cuda.synchronize()
+        assert torch.equal(xa, xb)
+        g = b.capture(xb)
+        for _ in range(2):
+            xb.copy_(emb)
+            g.replay()
+        torch.cuda.synchronize()
+        assert not b.ep_overflowed()
+        assert torch.equal(xa, xb)
+        assert int(b.ep.k.epoch.item()) == int(b.ep.k.flags[0].item()) > 0
+        g.destroy()
+        c = MoEPipeline(cfg)
+        c.enable_expert_parallel(peer_cap=64, p2p=True)
+        xc = emb.clone()
+        c.step(xc)
+        torch.cuda.synchronize()
+        assert not c.ep_overflowed()
+        assert torch.equal(xa, xc)

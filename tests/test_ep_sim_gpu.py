@@ -171,3 +171,50 @@ def test_simulated_fixed_split_overflow_is_a_flagged_no_op():
     torch.cuda.synchronize()
     assert all(int(k.overflow.item()) == 1 for k in ks)
     assert torch.equal(torch.cat(xs).cpu(), torch.from_numpy(x0))
+
+
+@pytest.mark.parametrize("G,E,d,F,T,replicas", [(2, 16, 256, 512, 700, True), (4, 16, 768, 3072, 300, True),
+                                                 (8, 32, 256, 512, 300, False)])
+def test_simulated_peer_memory_ep_equals_single_device(G, E, d, F, T, replicas):
+    """Peer-memory dispatch / combine (no all-to-all): every rank writes its rows into the
+    destinations' receive blocks and the destinations' GEMM2 epilogues add the results into the
+    home streams through peer address tables -- here G ranks' buffers on one device, the ranks'
+    kernels issued one after another (no device barrier: nothing waits inside a kernel). Same
+    bits as the single-device forward."""
+    from paper_2605_11537_b200.ep import CudaEpKernels
+    from paper_2605_11537_b200.router_oracle import _device_moe, _run_layers_device
+
+    dev = require_device()
+    L = 2
+    params = _params(L, E, d, F, seed=13 * G + E)
+    rng = np.random.default_rng(200 + G)
+    pop = 1.0 / (rng.permutation(E) + 1.0) ** 1.2
+    e0 = rng.choice(E, size=G * T, p=pop / pop.sum())
+    x0 = (params.router_weights[0][e0] * 0.05 + rng.normal(size=(G * T, d)) * 0.5).astype(np.float32)
+    x_ref = torch.from_numpy(x0).to(dev)
+    _run_layers_device(x_ref, _device_moe(params, dev))
+    dm = _device_moe(params, dev)
+    _tile(dm, E, d, F, _lib.size_query("mp_ffn_down_bn", d))
+    res0 = (rng.integers(0, 4, size=(L, E)) if replicas else np.zeros((L, E))).astype(np.int32)
+    capacity = int(res0.sum(1).max()) + E
+    cap = -(-2 * T // G)
+    ks = [CudaEpKernels(dm.layers, T, G, r, G * capacity + E, peer_cap=cap, p2p=True) for r in range(G)]
+    res = [torch.from_numpy(res0.copy()).to(dev) for _ in range(G)]
+    xs = [torch.from_numpy(x0[r * T:(r + 1) * T].copy()).to(dev) for r in range(G)]
+    table = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=dev)
+    t_recv, t_tok, t_flags, t_x = (table([k.recvbuf for k in ks]), table([k.recv_tok for k in ks]),
+                                   table([k.flags for k in ks]), table(xs))
+    for k, x in zip(ks, xs):
+        k.set_peers(t_recv, t_tok, t_flags)
+        k.register_stream(x, t_x)
+    for l in range(L):
+        routes = [k.route(x, l) for k, x in zip(ks, xs)]
+        C = torch.stack([k.counts(r).clone() for k, r in zip(ks, routes)])
+        plans = [k.plan(r, C, res[g][l]) for g, (k, r) in enumerate(zip(ks, routes))]
+        for k, x, p in zip(ks, xs, plans):
+            k.dispatch_peer(x, p)
+        for k, p in zip(ks, plans):
+            k.expert_ffn_peer(p, l)
+    torch.cuda.synchronize()
+    assert all(int(k.overflow.item()) == 0 for k in ks)
+    assert torch.equal(torch.cat(xs), x_ref)
