@@ -664,6 +664,7 @@ def run_ours(args):
         "cuda_graph": graph is not None or overlap is not None,
         "overlap": overlap is not None,
         "ep_dispatch": ({"mode": ("peer-memory" if pipe.ep.k.p2p else "fixed-split") if ep_graph else "compact",
+                         "peer_barrier_timeouts": int(pipe.ep.k.peer_err.item()) if pipe.ep.k.p2p else 0,
                          "peer_cap_rows": pipe.ep.k.peer_cap,
                          "overflowed": pipe.ep_overflowed() if ep_graph else False, "all_to_all": a2a}
                         if ep else None),

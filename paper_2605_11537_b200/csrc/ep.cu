@@ -308,7 +308,8 @@ __global__ void k_ep_gather_peer(const __nv_bfloat16* __restrict__ buf, int n, i
 // stream -- the peer stores and reductions it hands over -- have completed with their memory
 // flushed when griddepcontrol.wait returns, and the system-scope fence orders them before the
 // flags (the pattern of an on-stream barrier: no fence in the producing kernels).
-__global__ void k_peer_barrier(int32_t* const* __restrict__ flags, int rank, int G, int32_t* __restrict__ epoch) {
+__global__ void k_peer_barrier(int32_t* const* __restrict__ flags, int rank, int G, int32_t* __restrict__ epoch,
+                               int32_t* __restrict__ err) {
   griddep_wait();
   const int lane = threadIdx.x;
   int e = 0;
@@ -324,11 +325,21 @@ __global__ void k_peer_barrier(int32_t* const* __restrict__ flags, int rank, int
   }
   if (lane < G) {
     const int32_t* f = flags[rank] + lane;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     int v;
-    for (;;) {
+    for (int it = 0;; ++it) {
       asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
       if (v >= e) break;
       __nanosleep(64);
+      if ((it & 1023) == 1023) {  // a rank that never arrives: flag it instead of hanging the GPU
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 5000000000ull) {
+          atomicOr(err, 1);
+          break;
+        }
+      }
     }
   }
   __syncwarp();
@@ -518,9 +529,10 @@ extern "C" int mp_ep_gather_peer(const void* buf, int n_max, int d, const int32_
   return MP_OK;
 }
 
-extern "C" int mp_peer_barrier(int32_t* const* flags, int rank, int G, int32_t* epoch, void* stream) {
-  MP_REQUIRE(G >= 1 && G <= 32 && rank >= 0 && rank < G, MP_ERR_CONFIG, "mp_peer_barrier: G in [1, 32]");
-  MP_CUDA_TRY(launch_pdl(k_peer_barrier, dim3(1), dim3(32), 0, (cudaStream_t)stream, flags, rank, G, epoch));
+extern "C" int mp_peer_barrier(int32_t* const* flags, int rank, int G, int32_t* epoch, int32_t* err, void* stream) {
+  MP_REQUIRE(G >= 1 && G <= 32 && rank >= 0 && rank < G && err != nullptr, MP_ERR_CONFIG,
+             "mp_peer_barrier: G in [1, 32], err required");
+  MP_CUDA_TRY(launch_pdl(k_peer_barrier, dim3(1), dim3(32), 0, (cudaStream_t)stream, flags, rank, G, epoch, err));
   return MP_OK;
 }
 

@@ -455,9 +455,13 @@ class MoEPipeline:
         k = self.ep.k
         if not k.peer_cap or torch.cuda.is_current_stream_capturing():
             return self._step_ep(x, events)
+        if k.p2p:
+            self.check_peer_barriers()
         x0, res0 = x.clone(), self.res.clone()
         k.overflow.zero_()
         n = self._step_ep(x, events)
+        if k.p2p:
+            self.check_peer_barriers()
         if int(k.overflow.item()):
             x.copy_(x0)
             self.res.copy_(res0)
@@ -468,6 +472,16 @@ class MoEPipeline:
                 k.peer_cap = cap
                 k.overflow.zero_()
         return n
+
+    def check_peer_barriers(self) -> None:
+        """Peer-memory EP: raise if a device barrier since the last check gave up waiting for a
+        rank (5 s); the steps since then are invalid."""
+        from .errors import DeviceError
+
+        k = self.ep.k
+        if getattr(k, "p2p", False) and int(k.peer_err.item()):
+            k.peer_err.zero_()
+            raise DeviceError("peer-memory expert parallelism: a device barrier timed out waiting for a rank")
 
     def ep_overflowed(self) -> bool:
         """Fixed-split dispatch: did any layer since the last reset need more than peer_cap rows

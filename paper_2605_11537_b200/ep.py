@@ -142,6 +142,7 @@ class CudaEpKernels:
             self.recv_tok = torch.zeros(world * self.peer_cap, **i32)
             self.flags = torch.zeros(world, **i32)
             self.epoch = torch.zeros(1, **i32)
+            self.peer_err = torch.zeros(1, **i32)  # a barrier timed out (a rank never arrived)
             self.dst_of_row = torch.zeros(self.cap_rows, **i32)
             self.t_recv = self.t_tok = self.t_flags = self.t_x = None
             self._x_ptr = None
@@ -168,7 +169,8 @@ class CudaEpKernels:
             self.t_x, self._x_ptr = self._mem.table(x), x.data_ptr()
 
     def barrier(self) -> None:
-        _lib.call("mp_peer_barrier", ptr(self.t_flags), self.rank, self.G, ptr(self.epoch), stream_ptr())
+        _lib.call("mp_peer_barrier", ptr(self.t_flags), self.rank, self.G, ptr(self.epoch), ptr(self.peer_err),
+                  stream_ptr())
 
     def dispatch_peer(self, x: torch.Tensor, plan: EpPlan) -> None:
         """Rows straight into the destinations' receive blocks (peer stores); no barrier."""

@@ -116,3 +116,55 @@ def test_token_sharded_sru_equals_whole_sequence(G):
     rel = ((h - h_ref).abs().max() / h_ref.abs().max()).item()
     assert rel < 1e-5, rel
     assert int(nf.item()) == 0
+
+
+def test_peer_memory_tables_map_another_process(tmp_path):
+    """ep.PeerMemory across two processes on this GPU (CUDA IPC through torch's storage sharing,
+    gloo for the handles): each rank's table entry for the other rank addresses that rank's
+    buffer view (storage offset included) -- read back with a plain gather kernel."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    require_device()
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    worker = Path(__file__).resolve().parent / "peer_worker.py"
+    out = tmp_path / "peer"
+    procs = [subprocess.Popen([sys.executable, str(worker), str(r), "2", str(port), str(out)]) for r in range(2)]
+    try:
+        for p in procs:
+            assert p.wait(timeout=240) == 0
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert [Path(f"{out}.{r}").read_text() for r in range(2)] == ["ok", "ok"]
+
+
+def test_peer_memory_ep_across_two_processes(tmp_path):
+    """The peer-memory EP data path between two processes on this GPU through real CUDA IPC
+    peer tables (receive rows and residual streams of the other process), host barriers in
+    place of the device barriers: each rank's shard equals the single-device forward."""
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    require_device()
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    worker = Path(__file__).resolve().parent / "peer_ep_worker.py"
+    out = tmp_path / "pep"
+    procs = [subprocess.Popen([sys.executable, str(worker), str(r), "2", str(port), str(out)]) for r in range(2)]
+    try:
+        for p in procs:
+            assert p.wait(timeout=300) == 0
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    assert [Path(f"{out}.{r}").read_text() for r in range(2)] == ["ok", "ok"]
