@@ -258,6 +258,22 @@ constexpr int kSpAgg = 8;  // u/f tokens in flight per thread in step 1
 // 3 blocks per SM (<= 80 registers): all T / 256 x d / 128 blocks of the bench shape resident
 // in one wave (two blocks per SM: 74 us, three: 53 us, four with spills: 65 us).
 
+#ifdef MP_DIAG
+// Diagnostic build only: per-block (ticket order) %globaltimer stamps of the last k_scan_fused
+// launch: [0] ticket taken, [1] chunk maps done, [2] carry-in known, [3] replay done.
+static __device__ unsigned long long g_scan_t[1024][4];
+#define SCAN_STAMP(b, i)                                             \
+  do {                                                               \
+    unsigned long long t_;                                           \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));          \
+    if ((b) < 1024) g_scan_t[b][i] = t_;                             \
+  } while (0)
+#else
+#define SCAN_STAMP(b, i) \
+  do {                   \
+  } while (0)
+#endif
+
 __device__ __forceinline__ int sp_ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -283,6 +299,7 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
   if (threadIdx.x == 0) s_ticket = atomicAdd(&flags[nstr * nblk], 1);
   __syncthreads();
   const int str = s_ticket % nstr, blk = s_ticket / nstr;
+  if (threadIdx.x == 0) SCAN_STAMP(s_ticket, 0);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cq = str * 32 + lane;
   const bool act = 4 * cq < d;
@@ -324,6 +341,7 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) SCAN_STAMP(s_ticket, 1);
   // ---- 2. block map; sA/sB become the exclusive prefix maps of the chunks inside the block
   const int me = str * nblk + blk;
   const int c = threadIdx.x;  // channel of the strip (threads < 128)
@@ -416,6 +434,7 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
   }
   __syncthreads();
   if (threadIdx.x == 0) sp_st_release(&flags[me], 2);
+  if (threadIdx.x == 0) SCAN_STAMP(s_ticket, 2);
   if (!act || t0 >= T) return;
   float cc[4];
 #pragma unroll
@@ -469,6 +488,13 @@ __global__ void __launch_bounds__(32 * kSpWarps, 3) k_scan_fused(const __nv_bflo
   }
   if (c_last && t1 == T) *reinterpret_cast<float4*>(c_last + 4 * cq) = make_float4(c0r, c1r, c2r, c3r);
   if (bad) atomicOr(nonfinite, 1);  // reference raises NumericError (src/predictor.py:170-171)
+#ifdef MP_DIAG
+  if ((threadIdx.x & 31) == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    if (s_ticket < 1024) atomicMax(&g_scan_t[s_ticket][3], t_);
+  }
+#endif
 }
 
 
@@ -649,3 +675,14 @@ extern "C" int mp_heads_argmax(const void* h_bf16, const void* heads, int T, int
   return launch_gemm<64, 8>(ta, tb, s, e, grid, st);
 }
 
+#ifdef MP_DIAG
+extern "C" __attribute__((visibility("default"))) int mp_debug_scan_trace(unsigned long long* out) {
+  MP_CUDA_TRY(cudaMemcpyFromSymbol(out, mp::g_scan_t, sizeof(mp::g_scan_t)));
+  return MP_OK;
+}
+extern "C" __attribute__((visibility("default"))) int mp_debug_scan_trace_reset() {
+  static unsigned long long zero[1024][4];
+  MP_CUDA_TRY(cudaMemcpyToSymbol(mp::g_scan_t, zero, sizeof(zero)));
+  return MP_OK;
+}
+#endif
