@@ -72,9 +72,10 @@ def parse_args():
                    help="fixed-split EP: rows per peer block = factor x tokens / GPUs")
     p.add_argument("--ep-compact", action="store_true",
                    help="expert parallelism with split sizes read back every layer (no step graph)")
-    p.add_argument("--ep-p2p", action="store_true",
-                   help="expert parallelism over peer memory: rows written into the destination's receive block, "
-                        "combine fused into GEMM2's epilogue over NVLink, device barriers (no all-to-all)")
+    p.add_argument("--ep-nccl", action="store_true",
+                   help="expert parallelism through NCCL all-to-alls instead of the default peer-memory dispatch "
+                        "(rows stored into the destination's receive block, combine fused into GEMM2's epilogue "
+                        "over NVLink, device barriers; verified at start-up, NCCL on any failure)")
     p.add_argument("--ffn-sms", type=int, default=0, help="--overlap on: persistent grid of the expert GEMMs")
     p.add_argument("--pred-sms", type=int, default=0, help="--overlap on: persistent grid of the predictor GEMMs")
     p.add_argument("--overlap", choices=["on", "off"], default="off",
@@ -470,7 +471,7 @@ def run_ours(args):
         # fixed-split dispatch (1.25 T / G rows per peer block): graph-capturable; --ep-compact reads
         # the split sizes back every layer instead
         pipe.enable_expert_parallel(peer_cap=0 if args.ep_compact else None, cap_factor=args.ep_cap_factor,
-                                    p2p=args.ep_p2p and not args.ep_compact)
+                                    p2p=not (args.ep_nccl or args.ep_compact))
     ep_graph = ep and not args.ep_compact
     weights_same = weights_hash_equal(pipe, world)
     batches = [pipe.wl.batch(T) for _ in range(max(1, args.batches))]

@@ -398,10 +398,23 @@ class MoEPipeline:
         if peer_cap is None:
             want = math.ceil(cap_factor * cfg.tokens / self.world / 128) * 128
             peer_cap = cfg.tokens if self.world == 1 else min(cfg.tokens, want)
-        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, self.world * cfg.capacity + cfg.num_experts,
-                          peer_cap=peer_cap, p2p=p2p)
+        max_slots = self.world * cfg.capacity + cfg.num_experts
+        k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, max_slots, peer_cap=peer_cap, p2p=p2p)
         if p2p:
-            k.connect(group)
+            # map the peers and check the mappings + device barrier once; if any rank sees a problem
+            # every rank falls back to the all-to-all form of the same fixed-split layout
+            try:
+                k.connect(group)
+                ok = k.verify_peers()
+            except Exception:  # noqa: BLE001 -- any failure to map peers selects the NCCL path
+                ok = False
+            if self.world > 1:
+                flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=self.dev)
+                dist.all_reduce(flag, group=group)
+                ok = int(flag.item()) == 0
+            if not ok:
+                k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, max_slots, peer_cap=peer_cap)
+        self.ep_p2p = bool(getattr(k, "p2p", False))
         self.ep = ExpertParallelMoE(k, cfg.num_layers, cfg.num_experts, group)
         self.ep.res = self.res  # one residency state for placement and execution
         GT = self.world * cfg.tokens

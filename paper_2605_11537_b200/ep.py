@@ -154,6 +154,31 @@ class CudaEpKernels:
         self._mem = PeerMemory(group, self.G, self.rank, self.dev)
         self.set_peers(self._mem.table(self.recvbuf), self._mem.table(self.recv_tok), self._mem.table(self.flags))
 
+    def verify_peers(self) -> bool:
+        """Check the peer mappings and the device barrier once (collective): every rank stores a
+        row and its index into every peer's receive block through the tables, a device barrier
+        hands them over, and each rank checks what its peers wrote. False (on every rank that
+        sees a problem) means: use the all-to-all path."""
+        G, pc, d = self.G, self.peer_cap, self.d
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        x = torch.full((G, d), float(self.rank + 1), device=self.dev)
+        send_pos = torch.arange(G, **i32) * pc  # token g -> rank g, row rank * peer_cap
+        self.recv_tok.fill_(-1)
+        torch.cuda.synchronize()
+        if G > 1:
+            dist.barrier(group=self._mem.group)
+        _lib.call("mp_ep_pack_peer", ptr(x), G, d, ptr(send_pos), pc, self.rank, ptr(self.t_recv), ptr(self.t_tok),
+                  stream_ptr())
+        self.barrier()
+        torch.cuda.synchronize()
+        rows = torch.arange(G, device=self.dev) * pc
+        ok = int(self.peer_err.item()) == 0
+        ok = ok and bool((self.recv_tok[rows] == self.rank).all().item())
+        want = (torch.arange(G, device=self.dev, dtype=torch.float32) + 1).to(torch.bfloat16)
+        ok = ok and bool(torch.equal(self.recvbuf[rows, 0], want))
+        self.peer_err.zero_()
+        return ok
+
     def set_peers(self, t_recv: torch.Tensor, t_tok: torch.Tensor, t_flags: torch.Tensor) -> None:
         self.t_recv, self.t_tok, self.t_flags = t_recv, t_tok, t_flags
 
