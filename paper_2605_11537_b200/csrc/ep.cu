@@ -286,6 +286,18 @@ __global__ void k_ep_pack_peer(const float* __restrict__ x, int T, int d, const 
   // flushed) and fences at system scope before it signals -- an on-stream barrier
 }
 
+// dst[g][rank * n + i] = src[i] for every rank g (peer stores): an all-gather of n int32 per
+// rank into every rank's (G x n) buffer; a device barrier completes it.
+__global__ void k_peer_allgather_i32(const int32_t* __restrict__ src, int n, int rank, int G,
+                                     int32_t* const* __restrict__ dst) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t v = src[i];
+  for (int g = 0; g < G; ++g) dst[g][(size_t)rank * n + i] = v;
+}
+
 // Receiver side of the peer-memory path: xperm[row] = recvbuf[idx[row]] and the destination
 // code of the row's result, home * T_home + t (home = idx / peer_cap, t from recv_tok).
 __global__ void k_ep_gather_peer(const __nv_bfloat16* __restrict__ buf, int n, int d, const int32_t* __restrict__ idx,
@@ -526,6 +538,14 @@ extern "C" int mp_ep_gather_peer(const void* buf, int n_max, int d, const int32_
   MP_CUDA_TRY(launch_pdl(k_ep_gather_peer, dim3(cdiv(n_max * 32, 256)), dim3(256), 0, (cudaStream_t)stream,
                          (const __nv_bfloat16*)buf, n_max, d, idx, n_dev, recv_tok, peer_cap, T_home, dst_of_row,
                          (__nv_bfloat16*)out));
+  return MP_OK;
+}
+
+extern "C" int mp_peer_allgather_i32(const int32_t* src, int n, int rank, int G, int32_t* const* dst, void* stream) {
+  MP_REQUIRE(n >= 0 && G >= 1 && rank >= 0 && rank < G, MP_ERR_CONFIG, "mp_peer_allgather_i32: bad sizes");
+  if (n == 0) return MP_OK;
+  MP_CUDA_TRY(launch_pdl(k_peer_allgather_i32, dim3(cdiv(n, 256)), dim3(256), 0, (cudaStream_t)stream, src, n, rank, G,
+                         dst));
   return MP_OK;
 }
 

@@ -144,7 +144,8 @@ class CudaEpKernels:
             self.epoch = torch.zeros(1, **i32)
             self.peer_err = torch.zeros(1, **i32)  # a barrier timed out (a rank never arrived)
             self.dst_of_row = torch.zeros(self.cap_rows, **i32)
-            self.t_recv = self.t_tok = self.t_flags = self.t_x = None
+            self.C_all = torch.zeros(world, self.E, **i32)  # every rank's expert counts (peer-written)
+            self.t_recv = self.t_tok = self.t_flags = self.t_x = self.t_C = None
             self._x_ptr = None
             self._mem = None
 
@@ -152,7 +153,8 @@ class CudaEpKernels:
     def connect(self, group) -> None:
         """Map the peers' receive buffers, receive-token arrays and flags (collective)."""
         self._mem = PeerMemory(group, self.G, self.rank, self.dev)
-        self.set_peers(self._mem.table(self.recvbuf), self._mem.table(self.recv_tok), self._mem.table(self.flags))
+        self.set_peers(self._mem.table(self.recvbuf), self._mem.table(self.recv_tok), self._mem.table(self.flags),
+                       self._mem.table(self.C_all))
 
     def verify_peers(self) -> bool:
         """Check the peer mappings and the device barrier once (collective): every rank stores a
@@ -179,8 +181,16 @@ class CudaEpKernels:
         self.peer_err.zero_()
         return ok
 
-    def set_peers(self, t_recv: torch.Tensor, t_tok: torch.Tensor, t_flags: torch.Tensor) -> None:
-        self.t_recv, self.t_tok, self.t_flags = t_recv, t_tok, t_flags
+    def set_peers(self, t_recv: torch.Tensor, t_tok: torch.Tensor, t_flags: torch.Tensor,
+                  t_C: torch.Tensor = None) -> None:
+        self.t_recv, self.t_tok, self.t_flags, self.t_C = t_recv, t_tok, t_flags, t_C
+
+    def allgather_counts_peer(self, counts: torch.Tensor, barrier: bool = True) -> torch.Tensor:
+        """Every rank's expert counts (G x E) by peer stores + a device barrier (no NCCL)."""
+        _lib.call("mp_peer_allgather_i32", ptr(counts), self.E, self.rank, self.G, ptr(self.t_C), stream_ptr())
+        if barrier:
+            self.barrier()
+        return self.C_all
 
     def register_stream(self, x: torch.Tensor, t_x: torch.Tensor = None) -> None:
         """Map every rank's residual stream (collective when the buffer changes; ``t_x`` given:
@@ -353,7 +363,10 @@ class ExpertParallelMoE:
     def layer(self, l: int, x: torch.Tensor, ev=None) -> torch.Tensor:
         k = self.k
         route = k.route(x, l)
-        C = self._all_gather_counts(k.counts(route))
+        if getattr(k, "p2p", False) and k.peer_cap and self.G > 1:
+            C = k.allgather_counts_peer(k.counts(route))  # peer stores + device barrier
+        else:
+            C = self._all_gather_counts(k.counts(route))
         if getattr(k, "p2p", False) and k.peer_cap:
             # peer memory: rows to the destinations, barrier, GEMMs whose epilogue adds the results
             # into the home streams, barrier (the next layer's router reads them)

@@ -48,11 +48,15 @@ def main(rank: int, world: int, port: int, out: str) -> None:
 
     for l in range(L):
         route = k.route(x, l)
-        counts = k.counts(route).cpu()
-        parts = [torch.empty_like(counts) for _ in range(world)]
-        dist.all_gather(parts, counts)
-        C = torch.stack(parts).to(dev)
-        plan = k.plan(route, C, res[l])
+        counts = k.counts(route)
+        k.allgather_counts_peer(counts, barrier=False)  # peer stores into every rank's C_all
+        host_barrier()
+        parts = [torch.empty_like(counts.cpu()) for _ in range(world)]
+        dist.all_gather(parts, counts.cpu())
+        ok_counts = bool(torch.equal(k.C_all.cpu(), torch.stack(parts)))
+        if not ok_counts:
+            raise SystemExit("peer all-gather of the counts differs from gloo's")
+        plan = k.plan(route, k.C_all, res[l])
         k.register_stream(x)
         k.dispatch_peer(x, plan)
         host_barrier()

@@ -202,15 +202,18 @@ def test_simulated_peer_memory_ep_equals_single_device(G, E, d, F, T, replicas):
     res = [torch.from_numpy(res0.copy()).to(dev) for _ in range(G)]
     xs = [torch.from_numpy(x0[r * T:(r + 1) * T].copy()).to(dev) for r in range(G)]
     table = lambda ts: torch.tensor([t.data_ptr() for t in ts], dtype=torch.int64, device=dev)
-    t_recv, t_tok, t_flags, t_x = (table([k.recvbuf for k in ks]), table([k.recv_tok for k in ks]),
-                                   table([k.flags for k in ks]), table(xs))
+    t_recv, t_tok, t_flags, t_x, t_C = (table([k.recvbuf for k in ks]), table([k.recv_tok for k in ks]),
+                                        table([k.flags for k in ks]), table(xs), table([k.C_all for k in ks]))
     for k, x in zip(ks, xs):
-        k.set_peers(t_recv, t_tok, t_flags)
+        k.set_peers(t_recv, t_tok, t_flags, t_C)
         k.register_stream(x, t_x)
     for l in range(L):
         routes = [k.route(x, l) for k, x in zip(ks, xs)]
+        for k, r in zip(ks, routes):  # the counts all-gather by peer stores (no barrier needed here)
+            k.allgather_counts_peer(k.counts(r), barrier=False)
         C = torch.stack([k.counts(r).clone() for k, r in zip(ks, routes)])
-        plans = [k.plan(r, C, res[g][l]) for g, (k, r) in enumerate(zip(ks, routes))]
+        assert all(torch.equal(k.C_all, C) for k in ks)
+        plans = [k.plan(r, k.C_all, res[g][l]) for g, (k, r) in enumerate(zip(ks, routes))]
         for k, x, p in zip(ks, xs, plans):
             k.dispatch_peer(x, p)
         for k, p in zip(ks, plans):
