@@ -375,8 +375,9 @@ MP_API int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const int32
  *   mp_peer_barrier    device barrier of the G ranks (epoch counter in *epoch, one per rank);
  *                      orders the peer-memory writes before it for every rank after it; a rank
  *                      missing for 5 s sets *err |= 1 instead of hanging (check it per step)
- *   mp_peer_allgather_i32  dst[g][rank * n + i] = src[i] for every rank g (e.g. the per-layer
- *                      expert counts, G x E on every rank after the next barrier)
+ *   mp_peer_allgather_i32  dst[g][row * dst_row_stride + rank * n + i] = src[row * n + i] for
+ *                      every rank g: all-gather of rows x n 32-bit words (expert counts, SRU
+ *                      carry maps, predicted assignments) completed by the next barrier
  *   mp_ep_gather_peer  mp_gather_rows_bf16_dn + dst_of_row[r] = home * T_home + t of the row
  *   mp_ffn_down_peer   GEMM2 whose epilogue ADDS row r into peer_x[home][t] (the combine)
  * Per layer: counts -> allgather_i32 -> barrier -> plan_cap -> pack_peer -> barrier ->
@@ -384,7 +385,8 @@ MP_API int mp_gather_rows_bf16_dn(const void* buf, int n_max, int d, const int32
 MP_API int mp_ep_pack_peer(const float* x, int T, int d, const int32_t* send_pos, int peer_cap, int rank,
                            void* const* recv_rows, int32_t* const* recv_tok, void* stream);
 MP_API int mp_peer_barrier(int32_t* const* flags, int rank, int G, int32_t* epoch, int32_t* err, void* stream);
-MP_API int mp_peer_allgather_i32(const int32_t* src, int n, int rank, int G, int32_t* const* dst, void* stream);
+MP_API int mp_peer_allgather_i32(const int32_t* src, int rows, int n, int rank, int G, int32_t* const* dst,
+                                 int dst_row_stride, void* stream);
 MP_API int mp_ep_gather_peer(const void* buf, int n_max, int d, const int32_t* idx, const int32_t* n_dev,
                              const int32_t* recv_tok, int peer_cap, int T_home, int32_t* dst_of_row, void* out,
                              void* stream);

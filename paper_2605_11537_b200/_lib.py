@@ -101,7 +101,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_gather_rows_bf16_dn": (_I, [_P, _I, _I, _P, _P, _P, _P]),
     "mp_ep_pack_peer": (_I, [_P, _I, _I, _P, _I, _I, _P, _P, _P]),
     "mp_peer_barrier": (_I, [_P, _I, _I, _P, _P, _P]),
-    "mp_peer_allgather_i32": (_I, [_P, _I, _I, _I, _P, _P]),
+    "mp_peer_allgather_i32": (_I, [_P, _I, _I, _I, _I, _P, _I, _P]),
     "mp_ep_gather_peer": (_I, [_P, _I, _I, _P, _P, _P, _I, _I, _P, _P, _P]),
     "mp_ffn_down_peer": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_f32_to_bf16": (_I, [_P, _P, _Z, _P]),

@@ -29,6 +29,8 @@
 
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace mp {
 
 __device__ __forceinline__ int runs_before(int x, int j, int c) {  // F(x)
@@ -286,16 +288,20 @@ __global__ void k_ep_pack_peer(const float* __restrict__ x, int T, int d, const 
   // flushed) and fences at system scope before it signals -- an on-stream barrier
 }
 
-// dst[g][rank * n + i] = src[i] for every rank g (peer stores): an all-gather of n int32 per
-// rank into every rank's (G x n) buffer; a device barrier completes it.
-__global__ void k_peer_allgather_i32(const int32_t* __restrict__ src, int n, int rank, int G,
-                                     int32_t* const* __restrict__ dst) {
+// dst[g][row * dst_row_stride + rank * n + i] = src[row * n + i] for every rank g (peer stores):
+// an all-gather of rows x n 32-bit words per rank (e.g. expert counts, SRU carry maps, predicted
+// assignments); a device barrier completes it.
+__global__ void k_peer_allgather_i32(const int32_t* __restrict__ src, int rows, int n, int rank, int G,
+                                     int32_t* const* __restrict__ dst, int dst_row_stride) {
   griddep_launch_dependents();
   griddep_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int32_t v = src[i];
-  for (int g = 0; g < G; ++g) dst[g][(size_t)rank * n + i] = v;
+  const size_t total = (size_t)rows * n;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < total; k += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(k / n), i = (int)(k - (size_t)row * n);
+    const int32_t v = src[k];
+    const size_t o = (size_t)row * dst_row_stride + (size_t)rank * n + i;
+    for (int g = 0; g < G; ++g) dst[g][o] = v;
+  }
 }
 
 // Receiver side of the peer-memory path: xperm[row] = recvbuf[idx[row]] and the destination
@@ -541,11 +547,15 @@ extern "C" int mp_ep_gather_peer(const void* buf, int n_max, int d, const int32_
   return MP_OK;
 }
 
-extern "C" int mp_peer_allgather_i32(const int32_t* src, int n, int rank, int G, int32_t* const* dst, void* stream) {
-  MP_REQUIRE(n >= 0 && G >= 1 && rank >= 0 && rank < G, MP_ERR_CONFIG, "mp_peer_allgather_i32: bad sizes");
-  if (n == 0) return MP_OK;
-  MP_CUDA_TRY(launch_pdl(k_peer_allgather_i32, dim3(cdiv(n, 256)), dim3(256), 0, (cudaStream_t)stream, src, n, rank, G,
-                         dst));
+extern "C" int mp_peer_allgather_i32(const int32_t* src, int rows, int n, int rank, int G, int32_t* const* dst,
+                                     int dst_row_stride, void* stream) {
+  MP_REQUIRE(rows >= 0 && n >= 0 && G >= 1 && rank >= 0 && rank < G && (rows <= 1 || dst_row_stride >= G * n),
+             MP_ERR_CONFIG, "mp_peer_allgather_i32: bad sizes");
+  const size_t total = (size_t)rows * n;
+  if (total == 0) return MP_OK;
+  const int grid = (int)std::min<size_t>((total + 255) / 256, 4096);
+  MP_CUDA_TRY(launch_pdl(k_peer_allgather_i32, dim3(grid), dim3(256), 0, (cudaStream_t)stream, src, rows, n, rank, G,
+                         dst, dst_row_stride));
   return MP_OK;
 }
 

@@ -426,6 +426,14 @@ class MoEPipeline:
         self.ws_gplace = torch.empty(self.ws_gplace_n, dtype=torch.uint8, device=self.dev)
         self.ws_ghist_n = _lib.size_query("mp_histogram_workspace_bytes", cfg.num_layers, GT, cfg.num_experts)
         self.ws_ghist = torch.empty(self.ws_ghist_n, dtype=torch.uint8, device=self.dev)
+        if self.ep_p2p and self.world > 1:
+            # the step's other all-gathers over peer memory too: the predicted assignments (once per
+            # step) and the sharded SRU's carry maps (per SRU layer; two buffers by layer parity, so a
+            # rank running ahead never overwrites maps a slower rank has not folded yet)
+            d = self.dp
+            self.sru_tots_pp = torch.zeros(2, self.world, 2 * d, device=self.dev)
+            self.t_sru_tots = [k._mem.table(self.sru_tots_pp[0]), k._mem.table(self.sru_tots_pp[1])]
+            self.t_g_assign = k._mem.table(self.g_assign)
         # tests: issue the collectives (NCCL all-gathers, all-to-alls) even when world == 1
         self.force_collectives = False
 
@@ -449,9 +457,16 @@ class MoEPipeline:
             h32, h16 = self.h32[i % 2], self.h16[i % 2]
             _lib.call("mp_sru_project", ptr(cur16), ptr(W), ptr(B), T, d, ptr(self.ws_sru), self.ws_sru_n, sp)
             _lib.call("mp_sru_scan_total", T, d, ptr(self.sru_tot), ptr(self.ws_sru), self.ws_sru_n, sp)
-            parts = list(self.sru_tots.unbind(0))
-            dist.all_gather(parts, self.sru_tot, group=self.group)
-            _lib.call("mp_sru_fold_carry", ptr(self.sru_tots), self.rank, d, None, ptr(self.sru_carry_in), sp)
+            if getattr(self, "ep_p2p", False) and self.world > 1:  # peer stores + device barrier
+                tots = self.sru_tots_pp[i % 2]
+                _lib.call("mp_peer_allgather_i32", ptr(self.sru_tot), 1, 2 * d, self.rank, self.world,
+                          ptr(self.t_sru_tots[i % 2]), 0, sp)
+                self.ep.k.barrier()
+            else:
+                tots = self.sru_tots
+                parts = list(self.sru_tots.unbind(0))
+                dist.all_gather(parts, self.sru_tot, group=self.group)
+            _lib.call("mp_sru_fold_carry", ptr(tots), self.rank, d, None, ptr(self.sru_carry_in), sp)
             _lib.call("mp_sru_scan_finish", ptr(cur32), T, d, ptr(self.sru_carry_in), ptr(h32), ptr(h16), None,
                       ptr(self.nonfinite), ptr(self.ws_sru), self.ws_sru_n, sp)
             n += 6  # GEMM | aggregate, carry | fold | carry, replay
@@ -513,7 +528,11 @@ class MoEPipeline:
         self.ep.force_collectives = self.force_collectives
         n = self.predict_sharded(x, sp) if coll else self.predict(x, sp)
         parts = list(self.g_assign.view(L, self.world, T).unbind(1))
-        if coll:
+        if coll and getattr(self, "ep_p2p", False) and self.world > 1:  # peer stores + device barrier
+            _lib.call("mp_peer_allgather_i32", ptr(self.assign), L, T, self.rank, self.world, ptr(self.t_g_assign),
+                      self.world * T, sp)
+            self.ep.k.barrier()
+        elif coll:
             gathered = [torch.empty(L, T, dtype=torch.int32, device=self.dev) for _ in range(self.world)]
             dist.all_gather(gathered, self.assign, group=self.group)
             for r in range(self.world):

@@ -187,7 +187,7 @@ class CudaEpKernels:
 
     def allgather_counts_peer(self, counts: torch.Tensor, barrier: bool = True) -> torch.Tensor:
         """Every rank's expert counts (G x E) by peer stores + a device barrier (no NCCL)."""
-        _lib.call("mp_peer_allgather_i32", ptr(counts), self.E, self.rank, self.G, ptr(self.t_C), stream_ptr())
+        _lib.call("mp_peer_allgather_i32", ptr(counts), 1, self.E, self.rank, self.G, ptr(self.t_C), 0, stream_ptr())
         if barrier:
             self.barrier()
         return self.C_all

@@ -63,6 +63,17 @@ def main(rank: int, world: int, port: int, out: str) -> None:
         k.expert_ffn_peer(plan, l)
         host_barrier()
     ok = int(k.overflow.item()) == 0 and bool(torch.equal(x, x_ref[rank * T:(rank + 1) * T]))
+    # the strided form (rows of n words into row-major (rows, G * n) buffers): the engine's
+    # all-gather of the predicted assignments
+    a = torch.randint(0, 1 << 20, (3, 50), dtype=torch.int32, device=dev, generator=torch.Generator(dev).manual_seed(rank))
+    g_a = torch.zeros(3, world * 50, dtype=torch.int32, device=dev)
+    t_a = k._mem.table(g_a)
+    host_barrier()
+    _lib.call("mp_peer_allgather_i32", ptr(a), 3, 50, rank, world, ptr(t_a), world * 50, stream_ptr())
+    host_barrier()
+    parts = [torch.empty(3, 50, dtype=torch.int32) for _ in range(world)]
+    dist.all_gather(parts, a.cpu())
+    ok = ok and bool(torch.equal(g_a.cpu(), torch.cat(parts, 1)))
     dist.barrier()
     with open(f"{out}.{rank}", "w") as f:
         f.write("ok" if ok else "mismatch")
