@@ -411,6 +411,10 @@ MP_API int mp_event_destroy(void* ev);
 /* L2 residency hint: persisting access-policy window over [ptr, ptr + bytes) for kernels
  * launched on `stream` (bytes = 0 clears). Host plumbing. */
 MP_API int mp_l2_persist(void* ptr, size_t bytes, float hit_ratio, void* stream);
+/* Host plumbing for peer memory: let kernels on the current device access memory of
+ * `peer_device` (cudaDeviceEnablePeerAccess; already enabled is OK). MP_ERR_CONFIG when the
+ * pair has no peer access (e.g. no NVLink / P2P between them). */
+MP_API int mp_enable_peer_access(int peer_device);
 
 /* Operand staging: y[i] = bf16(x[i]) (round to nearest even), n % 4 == 0. */
 MP_API int mp_f32_to_bf16(const float* x, void* y, size_t n, void* stream);

@@ -106,6 +106,7 @@ SIGNATURES: dict[str, tuple] = {
     "mp_ffn_down_peer": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _P, _P, _P, _P, _P, _Z, _P]),
     "mp_f32_to_bf16": (_I, [_P, _P, _Z, _P]),
     "mp_l2_persist": (_I, [_P, _Z, _F, _P]),
+    "mp_enable_peer_access": (_I, [_I]),
     "mp_graph_begin": (_I, [_P]),
     "mp_graph_end": (_I, [_P, _P]),
     "mp_graph_end_counted": (_I, [_P, _P, _P]),

@@ -329,6 +329,21 @@ extern "C" int mp_l2_persist(void* ptr, size_t bytes, float hit_ratio, void* str
 }
 
 
+extern "C" int mp_enable_peer_access(int peer_device) {
+  int dev = 0, can = 0;
+  MP_CUDA_TRY(cudaGetDevice(&dev));
+  if (peer_device == dev) return MP_OK;
+  MP_CUDA_TRY(cudaDeviceCanAccessPeer(&can, dev, peer_device));
+  MP_REQUIRE(can, MP_ERR_CONFIG, "mp_enable_peer_access: device %d cannot access device %d", dev, peer_device);
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    (void)cudaGetLastError();  // clear the sticky-free status
+    return MP_OK;
+  }
+  MP_CUDA_TRY(e);
+  return MP_OK;
+}
+
 #ifdef MP_DIAG
 extern "C" __attribute__((visibility("default"))) int mp_debug_set_epi(int flags) {
   MP_CUDA_TRY(cudaMemcpyToSymbol(mp::g_diag_epi, &flags, sizeof(int)));

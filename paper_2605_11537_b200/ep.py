@@ -83,6 +83,9 @@ class PeerMemory:
             dist.all_gather_object(objs, (t.untyped_storage()._share_cuda_(), off), group=self.group)
             for g, (handle, og) in enumerate(objs):
                 if g != self.rank:
+                    # kernels on this device dereference the peer's memory: peer access first (raises
+                    # before any kernel touches it when the pair has no P2P path)
+                    _lib.call("mp_enable_peer_access", int(handle[0]))
                     st = torch.UntypedStorage._new_shared_cuda(*handle)
                     self._keep.append(st)
                     ptrs[g] = st.data_ptr() + og
