@@ -66,6 +66,46 @@ class Workspace:
 WORKSPACE = Workspace()
 
 
+class _Staging:
+    """Two page-locked bounce buffers for host -> device copies of pageable (numpy) arrays:
+    the host copy of chunk i overlaps the DMA of chunk i - 1 (50 MB: ~1.6 ms against ~2.6-3.6 ms
+    for a pageable copy and ~6.7 ms for registering the array's pages)."""
+
+    CHUNK = 4 << 20
+
+    def __init__(self):
+        self.pin = None
+        self.ev = None
+
+    def to_device(self, src: torch.Tensor, dev) -> torch.Tensor:
+        out = torch.empty(src.shape, dtype=src.dtype, device=dev)
+        n = src.numel() * src.element_size()
+        if n < 2 * self.CHUNK:
+            out.copy_(src)
+            return out
+        if self.pin is None:
+            self.pin = [torch.empty(self.CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            self.ev = [torch.cuda.Event(), torch.cuda.Event()]
+        s8, d8 = src.view(-1).view(torch.uint8), out.view(-1).view(torch.uint8)
+        for k, i in enumerate(range(0, n, self.CHUNK)):
+            j, m = k % 2, min(self.CHUNK, n - i)
+            self.ev[j].synchronize()  # the DMA that last read this buffer is done
+            self.pin[j][:m].copy_(s8[i:i + m])
+            d8[i:i + m].copy_(self.pin[j][:m], non_blocking=True)
+            self.ev[j].record()
+        return out
+
+
+_STAGING_TLS = __import__("threading").local()  # one pair of bounce buffers per host thread
+
+
+def _staging() -> _Staging:
+    st = getattr(_STAGING_TLS, "st", None)
+    if st is None:
+        st = _STAGING_TLS.st = _Staging()
+    return st
+
+
 def upload_rows(arr, d: int, dp: int, dev, name: str = "embeddings") -> torch.Tensor:
     """(T, d) float rows -> (T, dp) float32 device tensor, zero padded. Non-finite values raise
     NumericError like src/validation.py:22-27, checked on the device (one flag read) instead of
@@ -76,7 +116,7 @@ def upload_rows(arr, d: int, dp: int, dev, name: str = "embeddings") -> torch.Te
     if a.dtype not in (np.float32, np.float64):
         a = a.astype(np.float32)
     a = np.ascontiguousarray(a)
-    t = torch.from_numpy(a).to(dev)
+    t = _staging().to_device(torch.from_numpy(a), dev)
     if not bool(torch.isfinite(t).all().item()):
         raise NumericError(f"{name} contains non-finite values")
     if t.ndim != 2 or t.shape[1] != d:
