@@ -24,7 +24,7 @@ with torch.cuda.stream(torch.cuda.Stream()):
     for k in range(3):
         print(["%.1f ms" % (v*1e3) for v in one(host[k % 2])])
     pr = cProfile.Profile(); pr.enable(); one(host[0]); pr.disable()
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(18)
 
     # moe_forward phases
     import paper_2605_11537_b200.router_oracle as R
