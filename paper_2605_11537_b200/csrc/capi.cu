@@ -345,6 +345,10 @@ extern "C" int mp_enable_peer_access(int peer_device) {
 }
 
 #ifdef MP_DIAG
+extern "C" __attribute__((visibility("default"))) int mp_debug_set_mma(int flags) {
+  MP_CUDA_TRY(cudaMemcpyToSymbol(mp::g_diag_mma, &flags, sizeof(int)));
+  return MP_OK;
+}
 extern "C" __attribute__((visibility("default"))) int mp_debug_set_epi(int flags) {
   MP_CUDA_TRY(cudaMemcpyToSymbol(mp::g_diag_epi, &flags, sizeof(int)));
   return MP_OK;

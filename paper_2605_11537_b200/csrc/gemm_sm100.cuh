@@ -61,6 +61,8 @@ static __device__ unsigned long long g_unit_t[4][kTraceUnits];
   do {                    \
     if ((u) < kTraceUnits) g_unit_t[k][u] = (v); \
   } while (0)
+// bit 0: issue every N = BN MMA as two N = BN/2 MMAs (the A tile is read twice; same result)
+static __device__ int g_diag_mma;
 #else
 #define MP_TRACE(k, u, v) \
   do {                    \
@@ -252,6 +254,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               bdesc = sw128_kmajor_desc(smem_u32(smem + stage * L::kBBytes));
             }
             tc_fence_after();
+#ifdef MP_DIAG
+            if (BN % 32 == 0 && (g_diag_mma & 1)) {
+              constexpr uint32_t idesc_h = Kind::idesc(kBlockM, BN / 2);
+              constexpr uint32_t boff = (BN / 2) * 128 / 16;  // B rows BN/2.. : + (BN/2) x 128 B
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                Kind::mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc_h, (kb | k) != 0);
+                Kind::mma(d_tmem + BN / 2, adesc + 2 * k, bdesc + boff + 2 * k, idesc_h, (kb | k) != 0);
+              }
+            } else
+#endif
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               // advance 32 B of K inside the swizzle atom: +2 in the >>4 address field

@@ -41,7 +41,7 @@ def main():
         print(f"M={M} N={N} K={K}: " + "  ".join(f"{k}={v:.1f}us ({fl / v / 1e6:.0f} TF)" for k, v in res.items()))
 
 
-if __name__ == "__main__" and not ({"--stream", "--pair", "--epi"} & set(sys.argv)):
+if __name__ == "__main__" and not ({"--stream", "--pair", "--epi", "--mma"} & set(sys.argv)):
     main()
 
 
@@ -141,3 +141,40 @@ def epi_probe():
 
 if __name__ == "__main__" and "--epi" in sys.argv:
     epi_probe()
+
+
+def mma_probe():
+    """Shared-memory traffic test (diagnostic build): the dense GEMM with every N = 256 MMA
+    issued as two N = 128 MMAs, so the A tile is read from shared memory twice per k-block
+    (96 -> 112 KB of shared-memory traffic per k-block, the same MMA work and result). A kernel
+    bound by shared-memory bandwidth slows by ~17 %; one bound by the MMA or by TMA does not."""
+    import ctypes
+
+    from paper_2605_11537_b200.build import PKG, build
+
+    lib = _lib.load_library(build(extra=["-DMP_DIAG"], out=PKG / "libmoempmc_trace.so"))
+    lib.mp_debug_set_mma.restype = ctypes.c_int
+    lib.mp_debug_set_mma.argtypes = [ctypes.c_int]
+    dev = require_device()
+    for (M, N, K) in [(16384, 3072, 768), (16384, 2304, 768), (32768, 4096, 4096)]:
+        A = torch.randn(M, K, device=dev).bfloat16()
+        B = torch.randn(N, K, device=dev).bfloat16()
+        C = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+        C2 = torch.empty_like(C)
+        fl = 2 * M * N * K
+        g = lambda ldc, out: _lib.call("mp_gemm_bf16", ptr(A), ptr(B), ptr(out), M, N, K, 0, ldc, None, 0, 0,
+                                       stream_ptr())
+        res = {}
+        for flag in (0, 1, 0, 1):
+            lib.mp_debug_set_mma(flag)
+            res[f"nostore_split{flag}"] = timeit(lambda: g(0, C))
+            res[f"store_split{flag}"] = timeit(lambda: g(N, C if flag == 0 else C2))
+        lib.mp_debug_set_mma(0)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(C, C2))
+        print(f"M={M} N={N} K={K}: " + "  ".join(f"{k}={v:.1f}us ({fl / v / 1e6:.0f} TF)" for k, v in res.items())
+              + f"  split==plain {same}")
+
+
+if __name__ == "__main__" and "--mma" in sys.argv:
+    mma_probe()
