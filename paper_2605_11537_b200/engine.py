@@ -401,17 +401,28 @@ class MoEPipeline:
         max_slots = self.world * cfg.capacity + cfg.num_experts
         k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, max_slots, peer_cap=peer_cap, p2p=p2p)
         if p2p:
-            # map the peers and check the mappings + device barrier once; if any rank sees a problem
-            # every rank falls back to the all-to-all form of the same fixed-split layout
-            try:
-                k.connect(group)
-                ok = k.verify_peers()
-            except Exception:  # noqa: BLE001 -- any failure to map peers selects the NCCL path
-                ok = False
-            if self.world > 1:
+            # map the peers, agree that every rank could, then check the mappings + device barrier
+            # once and agree again; any problem on any rank -> every rank takes the all-to-all form
+            # of the same fixed-split layout (each step below runs the same collectives on all ranks)
+            def agree(ok: bool) -> bool:
+                if self.world == 1:
+                    return ok
                 flag = torch.tensor([0 if ok else 1], dtype=torch.int32, device=self.dev)
                 dist.all_reduce(flag, group=group)
-                ok = int(flag.item()) == 0
+                return int(flag.item()) == 0
+
+            try:
+                k.connect(group)
+                ok = True
+            except Exception:  # noqa: BLE001 -- a peer that cannot be mapped selects the NCCL path
+                ok = False
+            ok = agree(ok)
+            if ok:
+                try:
+                    ok = k.verify_peers()
+                except Exception:  # noqa: BLE001
+                    ok = False
+                ok = agree(ok)
             if not ok:
                 k = CudaEpKernels(self.layers, cfg.tokens, self.world, self.rank, max_slots, peer_cap=peer_cap)
         self.ep_p2p = bool(getattr(k, "p2p", False))

@@ -72,6 +72,7 @@ class PeerMemory:
     def __init__(self, group, world: int, rank: int, dev):
         self.group, self.world, self.rank, self.dev = group, world, rank, dev
         self._keep = []
+        self.failed = False  # a peer mapping could not be made here (the collectives still ran)
 
     def table(self, t: torch.Tensor) -> torch.Tensor:
         """int64 device array: entry g = address of rank g's tensor in the same role as ``t``
@@ -83,12 +84,17 @@ class PeerMemory:
             dist.all_gather_object(objs, (t.untyped_storage()._share_cuda_(), off), group=self.group)
             for g, (handle, og) in enumerate(objs):
                 if g != self.rank:
-                    # kernels on this device dereference the peer's memory: peer access first (raises
-                    # before any kernel touches it when the pair has no P2P path)
-                    _lib.call("mp_enable_peer_access", int(handle[0]))
-                    st = torch.UntypedStorage._new_shared_cuda(*handle)
-                    self._keep.append(st)
-                    ptrs[g] = st.data_ptr() + og
+                    # kernels on this device dereference the peer's memory: peer access first. A
+                    # failure is recorded, not raised, so every rank still takes part in the
+                    # remaining exchanges; the caller checks ``failed`` with the other ranks.
+                    try:
+                        _lib.call("mp_enable_peer_access", int(handle[0]))
+                        st = torch.UntypedStorage._new_shared_cuda(*handle)
+                        self._keep.append(st)
+                        ptrs[g] = st.data_ptr() + og
+                    except Exception:  # noqa: BLE001
+                        self.failed = True
+                        ptrs[g] = 0
         return torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
 
 
@@ -158,6 +164,8 @@ class CudaEpKernels:
         self._mem = PeerMemory(group, self.G, self.rank, self.dev)
         self.set_peers(self._mem.table(self.recvbuf), self._mem.table(self.recv_tok), self._mem.table(self.flags),
                        self._mem.table(self.C_all))
+        if self._mem.failed:
+            raise ConfigurationError("peer memory: a peer's buffers could not be mapped on this GPU")
 
     def verify_peers(self) -> bool:
         """Check the peer mappings and the device barrier once (collective): every rank stores a
