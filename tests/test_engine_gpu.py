@@ -255,3 +255,31 @@ def test_peer_memory_expert_parallel_step_graph_and_rollback():
         torch.cuda.synchronize()
         assert not c.ep_overflowed()
         assert torch.equal(xa, xc)
+
+
+def test_peer_memory_setup_failure_falls_back_to_all_to_all(monkeypatch):
+    """A peer mapping that cannot be made (or a failed start-up check) selects the all-to-all
+    form of the same fixed-split layout -- and the step still gives the single-device bits."""
+    from paper_2605_11537_b200 import ep as EP
+    from paper_2605_11537_b200.engine import MoEPipeline, PipelineConfig
+
+    cfg = PipelineConfig(num_layers=2, num_experts=16, d_model=256, d_ff=512, tokens=2048, sru_layers=2,
+                         capacity=32, seed=9)
+    a = MoEPipeline(cfg)
+    emb, _, _ = a.wl.batch(cfg.tokens)
+    xa = emb.clone()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a.step(xa)
+        for broken in ("connect", "verify_peers"):
+            def fail(self, *args, **kwargs):
+                raise RuntimeError("no peer access")
+            with monkeypatch.context() as m:
+                m.setattr(EP.CudaEpKernels, broken, fail)
+                b = MoEPipeline(cfg)
+                b.enable_expert_parallel(peer_cap=None, p2p=True)
+            assert not b.ep_p2p and not b.ep.k.p2p and b.ep.k.peer_cap == cfg.tokens
+            xb = emb.clone()
+            b.step(xb)
+            torch.cuda.synchronize()
+            assert torch.equal(xa, xb)
