@@ -323,9 +323,9 @@ __global__ void k_ep_gather_peer(const __nv_bfloat16* __restrict__ buf, int n, i
 // Device-side barrier over G ranks' flag arrays in peer memory (G <= 32, one warp): epoch e
 // = ++*epoch; lane g publishes e into rank g's slot for this rank (release, system scope),
 // lane s waits until rank s's e has arrived here (acquire). The kernels before it on the
-// stream -- the peer stores and reductions it hands over -- have completed with their memory
-// flushed when griddepcontrol.wait returns, and the system-scope fence orders them before the
-// flags (the pattern of an on-stream barrier: no fence in the producing kernels).
+// stream -- the peer stores and reductions it hands over -- have completed before it starts
+// (stream order; griddepcontrol.wait covers a programmatic launch too), and the system-scope
+// fence orders them before the flags (an on-stream barrier: no fence in the producers).
 __global__ void k_peer_barrier(int32_t* const* __restrict__ flags, int rank, int G, int32_t* __restrict__ epoch,
                                int32_t* __restrict__ err) {
   griddep_wait();
